@@ -1,0 +1,491 @@
+#!/usr/bin/env python
+"""bench.py -- fused GRPO logprob + loss fwd/bwd throughput on B200.
+
+Workload (BASELINE.json configs[1]): GRPO loss at Qwen2.5-1.5B shapes --
+vocab 151,936, 64 prompts x 8 rollouts, 2,048-token responses = 1,048,576
+trainable rows per GPU per step, bf16 logits, fp32 arithmetic.  Loss =
+GRPO advantage (group mean / std) + PPO clip (0.2 / 0.28) + low_var_kl (k3,
+0.001) + masked token-mean, gradient d loss / d logits written in bf16.
+
+The step's logits are 318.6 GB, more than one B200 holds, so a step runs as 8
+micro-batches of 8 groups (131,072 rows, 39.8 GB) each.  All micro-batches
+read one resident synthetic logits buffer (N(0, 2^2) + a +13.5 bump at the
+target, seeded) and write dlogits out of place to a second 39.8 GB buffer;
+per-micro-batch targets are shared, rewards / old / ref logprobs differ.
+Every micro-batch still streams its full 2V bytes per row in and 2V out:
+the working set (80 GB) is ~600x the 126 MB L2, so no L2 flush is needed.
+
+One process per GPU (torchrun for N > 1); each rank processes its own
+1,048,576-row batch (weak scaling) and NCCL allreduces only the 32-double
+statistics vector per step.  `value` = rows of all ranks / max-over-ranks
+device time.  `e2e` = the same metric through the public API with pinned
+HOST logits: H2D of the logits + metadata and D2H of dlogits + stats inside
+the timed region.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "tokens/sec of fused GRPO logprob+loss fwd/bwd at 1/2/4/8 B200; HBM GB/s vs peak"
+UNIT = "tokens/s"
+V = 151936
+BUMP = 13.5
+ALGO_BYTES_PER_ROW = 4 * V + 24  # 2V read + 2V write + 24 B side data
+WORKLOAD = "grpo_ppo_clip_k3_token_mean_qwen2.5_1.5b_shapes"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--groups", type=int, default=64)
+    p.add_argument("--group-size", type=int, default=8)
+    p.add_argument("--resp-len", type=int, default=2048)
+    p.add_argument("--mb-groups", type=int, default=8, help="groups per micro-batch")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--e2e-groups", type=int, default=2)
+    p.add_argument("--cpu-rows", type=int, default=256)
+    p.add_argument("--quiet", action="store_true")
+    return p.parse_args()
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        try:
+            d = json.loads(f.read_text())
+            return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling during the timed region
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port (numpy float64), bounded sample
+
+def cpu_sample(seed: int, rows: int, group_size: int):
+    from oracle import rft_oracle as O
+    rng = np.random.default_rng(seed)
+    per = max(1, rows // group_size)
+    T = per * group_size
+    tgt = rng.integers(0, V, T)
+    x = rng.normal(0, 2.0, (T, V))
+    x[np.arange(T), tgt] += BUMP
+    x = x.astype(np.float32).astype(np.float64)
+    lp = O.row_forward(x, tgt)[1]
+    b = O.Batch(logits=x, target=tgt, seq_offsets=np.arange(0, T + 1, per),
+                group_offsets=np.array([0, group_size]),
+                reward=rng.integers(0, 2, group_size).astype(np.float64),
+                old_lp=lp + rng.normal(0, 0.05, T), ref_lp=lp + rng.normal(0, 0.1, T))
+    return b
+
+
+def oracle_cfg():
+    from oracle import rft_oracle as O
+    return O.Config(advantage_fn="grpo", policy_loss_fn="ppo_clip", kl_fn="k3", kl_coef=0.001,
+                    loss_agg_mode="token-mean", clip_lo=0.2, clip_hi=0.28)
+
+
+def cpu_run(args_tuple):
+    seed, rows, gsize = args_tuple
+    from oracle import rft_oracle as O
+    b = cpu_sample(seed, rows, gsize)
+    dz = np.empty((b.n_rows, V), np.float32)
+    t0 = time.perf_counter()
+    O.single_pass_blocked(b, oracle_cfg(), dz_out=dz, block=32)
+    return b.n_rows, time.perf_counter() - t0
+
+
+def cpu_baseline(rows: int, gsize: int):
+    n, dt = cpu_run((1234, rows, gsize))
+    return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"oracle/rft_oracle.single_pass_blocked (numpy f64, 1 thread) on {n} rows "
+                      f"x V={V} (1 group x {gsize} seqs), same loss config; {dt:.2f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle port on all host cores (the reference is
+    pure Python and cannot run on the GPU box)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import multiprocessing as mp
+    cores = os.cpu_count() or 1
+    try:
+        avail = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    except Exception:
+        avail = 64 << 30
+    per_worker = args.cpu_rows * V * 4 * 8  # rough peak bytes of one worker
+    workers = max(1, min(cores, int(0.5 * avail // per_worker), 64))
+    ctx = mp.get_context("fork")
+    rates = []
+    with ctx.Pool(workers) as pool:
+        for step in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            res = pool.map(cpu_run, [(1000 + step * workers + i, args.cpu_rows, args.group_size)
+                                     for i in range(workers)])
+            dt = time.perf_counter() - t0
+            if step >= args.warmup:
+                rates.append(sum(r[0] for r in res) / dt)
+    value = statistics.median(rates)
+    rows = workers * (args.cpu_rows // args.group_size) * args.group_size
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * rows / value,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": WORKLOAD, "vocab": V,
+                                        "sample_rows_per_step": rows},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
+                         "sample": f"{workers} processes x {args.cpu_rows} rows x V={V} of the "
+                                   "oracle port (numpy f64) per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_17826_b200 import RFTLoss, RFTLossConfig, logprob_fwd, pack_arrays
+    from paper_2505_17826_b200 import _native as N
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    L = N.lib()
+
+    G, K, Lr = args.groups, args.group_size, args.resp_len
+    mbg = min(args.mb_groups, G)
+    n_mb = G // mbg
+    mb_rows = mbg * K * Lr
+    T = n_mb * mb_rows
+    B = G * K
+    cfg = RFTLossConfig(advantage_fn="grpo", policy_loss_fn="ppo_clip", kl_fn="low_var_kl",
+                        kl_coef=0.001, loss_agg_mode="token-mean", clip_lo=0.2, clip_hi=0.28)
+    loss = RFTLoss(cfg)
+
+    # ---- resident synthetic inputs (outside timing) ----
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    logits = torch.empty((mb_rows, V), dtype=torch.bfloat16, device=dev)
+    for r0 in range(0, mb_rows, 8192):
+        logits[r0:r0 + 8192].normal_(0.0, 2.0, generator=gen)
+    rng = np.random.default_rng(1234 + rank)
+    tgt = rng.integers(0, V, mb_rows)
+    tgt_d = torch.as_tensor(tgt, device=dev)
+    logits[torch.arange(mb_rows, device=dev), tgt_d] += BUMP
+    dz = torch.empty_like(logits)
+    lens = [Lr] * (mbg * K)
+    gsz = [K] * mbg
+    probe = pack_arrays(logits, tgt, lens, gsz, np.zeros(mbg * K, np.float32))
+    lp_true = logprob_fwd(probe)[0].cpu().numpy().astype(np.float64)
+    batches, outs = [], []
+    for m in range(n_mb):
+        rew = rng.integers(0, 2, mbg * K).astype(np.float32)
+        if m == 0:
+            rew[:K] = 1.0  # an all-equal group (A = 0, std = 0)
+        old = (lp_true + rng.normal(0, 0.05, mb_rows)).astype(np.float32)
+        ref = (lp_true + rng.normal(0, 0.1, mb_rows)).astype(np.float32)
+        b = pack_arrays(logits, tgt, lens, gsz, rew, old_lp=old, ref_lp=ref)
+        batches.append(b)
+        outs.append(None)
+    assert loss.route(batches[0]) == 1, "expected the fused TMA route"
+    n_tok_g, n_seq_g = world * T, world * B
+    stats_all = torch.zeros((n_mb, N.NSTAT), dtype=torch.float64, device=dev)
+
+    def step():
+        for m in range(n_mb):
+            outs[m] = loss(batches[m], dlogits=dz, n_tok_global=n_tok_g, n_seq_global=n_seq_g,
+                           out=outs[m])
+        st = torch.stack([o.stats for o in outs]).sum(0)
+        if world > 1:
+            dist.all_reduce(st)
+        return st
+
+    for _ in range(args.warmup):
+        st = step()
+    torch.cuda.synchronize()
+    s0 = step().cpu().numpy()
+    torch.cuda.synchronize()
+
+    # ---- timed region ----
+    n_ev = args.steps * n_mb
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(n_ev)]
+    for a, b_ in evs:  # materialise the event handles
+        a.record()
+        b_.record()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = L.tg_launch_count()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record()
+    k = 0
+    for _ in range(args.steps):
+        for m in range(n_mb):
+            L.tg_set_timing_events(evs[k][0].cuda_event, evs[k][1].cuda_event)
+            k += 1
+            outs[m] = loss(batches[m], dlogits=dz, n_tok_global=n_tok_g, n_seq_global=n_seq_g,
+                           out=outs[m])
+        st = torch.stack([o.stats for o in outs]).sum(0)
+        if world > 1:
+            dist.all_reduce(st)
+    t_end.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = L.tg_launch_count() - launches0
+    clk = clocks.stop()
+    ms = t_start.elapsed_time(t_end)
+    fused_ms = [a.elapsed_time(b_) for a, b_ in evs]
+    tmax = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    ms = float(tmax.item())
+    stats = st.cpu().numpy()
+    value = world * T * args.steps / (ms / 1000.0)
+
+    # ---- roofline of the dominant kernel (k_fused_tma) ----
+    peak, peak_src = peaks()
+    f_ms = statistics.mean(fused_ms)
+    achieved = mb_rows * ALGO_BYTES_PER_ROW / (f_ms / 1000.0) / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / "fused_traffic.json"
+    if tf.exists():
+        try:
+            d = json.loads(tf.read_text())
+            if int(d.get("rows", 0)) == mb_rows and int(d.get("vocab", 0)) == V:
+                traffic = float(d["dram_bytes_per_launch"])
+        except Exception:
+            traffic = None
+
+    # ---- e2e: public API with pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, loss, dev, world, rank, n_tok_g, n_seq_g)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_baseline(args.cpu_rows, K)
+        except Exception as ex:  # pragma: no cover
+            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "port", "sample": repr(ex)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "vocab": V, "prompts": G, "repeats": K,
+                       "response_len": Lr, "rows_per_gpu_per_step": T,
+                       "micro_batches": n_mb, "rows_per_micro_batch": mb_rows,
+                       "loss": "grpo adv + ppo_clip(0.2,0.28) + low_var_kl(0.001) + token-mean",
+                       "l2": "inputs larger than L2 (80 GB working set)",
+                       "parallelism": f"dp{world} (groups sharded by rank; stats allreduce)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "k_fused_tma", "kernel_ms": f_ms,
+                         "algorithmic_bytes_per_launch": mb_rows * ALGO_BYTES_PER_ROW,
+                         "peak_source": peak_src,
+                         "frac_of_8tbs_nominal": achieved / 8000.0},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "check": {"loss": float(stats[0]), "n_tok": float(stats[N.STAT["n_tok"]]),
+                      "nonfinite": float(stats[N.STAT["nonfinite"]]),
+                      "clipfrac": float(stats[N.STAT["clip_count"]] /
+                                        max(stats[N.STAT["n_tok_rl"]], 1)),
+                      "mean_lp": float(stats[N.STAT["sum_lp"]] / max(stats[N.STAT["n_tok"]], 1)),
+                      "stats_match_warm": bool(np.allclose(s0, stats))},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(args, loss, dev, world, rank, n_tok_g, n_seq_g):
+    """Public API with HOST buffers: per step, e2e_groups calls; each call
+    copies its group's logits + metadata H2D from pinned memory (copy stream),
+    runs the loss (compute stream) and copies dlogits + stats D2H (second copy
+    stream), double-buffered so copies of one group overlap the next."""
+    import torch
+
+    from paper_2505_17826_b200.packing import PackedBatch
+
+    K, Lr = args.group_size, args.resp_len
+    rows = K * Lr
+    ng = args.e2e_groups
+    rng = np.random.default_rng(99 + rank)
+    host_in = torch.empty((ng, rows, V), dtype=torch.bfloat16, pin_memory=True)
+    host_out = torch.empty((ng, rows, V), dtype=torch.bfloat16, pin_memory=True)
+    dev_in = [torch.empty((rows, V), dtype=torch.bfloat16, device=dev) for _ in range(2)]
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(7 + rank)
+    for i in range(ng):  # synthetic host logits, generated on device once (setup)
+        dev_in[0].normal_(0.0, 2.0, generator=gen)
+        host_in[i].copy_(dev_in[0])
+    torch.cuda.synchronize(dev)
+    meta, tmeta = [], []
+    for i in range(ng):
+        t = torch.empty(rows, dtype=torch.int32, pin_memory=True)
+        t.copy_(torch.as_tensor(rng.integers(0, V, rows).astype(np.int32)))
+        m = torch.empty((2, rows), dtype=torch.float32, pin_memory=True)
+        m[0] = torch.as_tensor(rng.normal(-1.0, 0.05, rows).astype(np.float32))
+        m[1] = torch.as_tensor(rng.normal(-1.0, 0.1, rows).astype(np.float32))
+        tmeta.append(t)
+        meta.append(m)
+    dev_meta = [torch.empty((2, rows), dtype=torch.float32, device=dev) for _ in range(2)]
+    dev_tgt = [torch.empty(rows, dtype=torch.int32, device=dev) for _ in range(2)]
+    s_in, s_cmp, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    host_stats = torch.empty((ng, 32), dtype=torch.float64, pin_memory=True)
+    rewards = rng.integers(0, 2, K).astype(np.float32)
+    lens = [Lr] * K
+    so = torch.as_tensor(np.arange(0, rows + 1, Lr, dtype=np.int32), device=dev)
+    go = torch.as_tensor(np.array([0, K], np.int32), device=dev)
+    rw = torch.as_tensor(rewards, device=dev)
+    h2d_bytes = ng * (rows * V * 2 + 3 * rows * 4)  # logits + target + old_lp + ref_lp
+    d2h_bytes = ng * (rows * V * 2 + 32 * 8)
+
+    def one_step():
+        free = [torch.cuda.Event(), torch.cuda.Event()]
+        for i in range(ng):
+            slot = i % 2
+            with torch.cuda.stream(s_in):
+                if i >= 2:
+                    s_in.wait_event(free[slot])
+                dev_in[slot].copy_(host_in[i], non_blocking=True)
+                dev_meta[slot].copy_(meta[i], non_blocking=True)
+                dev_tgt[slot].copy_(tmeta[i], non_blocking=True)
+                ready = torch.cuda.Event()
+                ready.record(s_in)
+            with torch.cuda.stream(s_cmp):
+                s_cmp.wait_event(ready)
+                dm = dev_meta[slot]
+                pb = PackedBatch(logits=dev_in[slot], target=dev_tgt[slot],
+                                 seq_offsets=so, group_offsets=go, reward=rw, old_lp=dm[0],
+                                 ref_lp=dm[1], vocab=V, n_rows=rows, n_seqs=K, n_groups=1,
+                                 n_rl_rows=rows, n_rl_seqs=K, max_rows_per_seq=Lr)
+                out = loss(pb, dlogits="inplace", n_tok_global=n_tok_g, n_seq_global=n_seq_g,
+                           stream=s_cmp)
+                done = torch.cuda.Event()
+                done.record(s_cmp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(done)
+                host_out[i].copy_(dev_in[slot], non_blocking=True)
+                host_stats[i].copy_(out.stats, non_blocking=True)
+                free[slot].record(s_out)
+        torch.cuda.synchronize(dev)
+
+    one_step()  # warm
+    times = []
+    for _ in range(max(2, min(args.steps, 4))):
+        t0 = time.perf_counter()
+        one_step()
+        times.append(time.perf_counter() - t0)
+    dt = statistics.median(times)
+    return {"value": ng * rows / dt, "unit": UNIT, "h2d_bytes_per_step": h2d_bytes,
+            "d2h_bytes_per_step": d2h_bytes,
+            "note": f"{ng} groups x {rows} rows per step through RFTLoss with pinned host "
+                    "logits in / dlogits + stats out (copies overlap across groups)"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

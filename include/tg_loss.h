@@ -1,0 +1,230 @@
+/*
+ * tg_loss.h -- C ABI of the B200-native RFT trainer loss path ("tg" = task group).
+ *
+ * Drop-in boundary for Trinity-RFT's (reference: `triad`) trainer loss path:
+ *
+ *   reference entry point (file:line under /root/reference/pkg/src/triad)   replaced by
+ *   ----------------------------------------------------------------------  ---------------------
+ *   algorithms.group_loss           algorithms.py:351-365                  tg_loss_fwd_bwd
+ *     loss_opmd_simple              algorithms.py:220-253   (GRPO analogue) TG_PG_VANILLA + TG_ADV_OPMD
+ *     loss_opmd_kimi                algorithms.py:118-153                   TG_PG_OPMD_KIMI
+ *     loss_opmd_pairwise            algorithms.py:156-190                   TG_PG_OPMD_PAIRWISE
+ *     regularizer_g (anchor KL)     algorithms.py:193-217                   TgConfig.anchor_beta
+ *   algorithms.loss_sft             algorithms.py:256-274                   TG_PG_SFT / seq_kind = 1
+ *   algorithms.loss_dpo             algorithms.py:277-315                   TG_PG_DPO
+ *   algorithms.combine_reports      algorithms.py:368-379                   stats[] (sums + group count)
+ *   algorithms.experience_logprob   algorithms.py:81-85                     tg_logprob_fwd
+ *   policy.logprob / grad_logprob   policy.py:194-212, 253-270              (fused into both)
+ *   policy.scored_states            policy.py:181-191 (toy-table adapter)   tg_scored_states (host)
+ *   ExperienceBuffer.sample_batch   buffer.py:240-264 (group indexing)      tg_group_by_task (host)
+ *
+ * plus the north_star registry pieces the reference does not have (GRPO std
+ * advantage, RLOO, PPO clip / dual clip, k1/k2/k3(low_var_kl)/abs KL,
+ * entropy bonus, token / sequence aggregation modes).
+ *
+ * Conventions
+ *  - Plain pointers + sizes; all array pointers in TgBatch / TgOut are DEVICE
+ *    pointers (cudaMalloc / torch CUDA tensors).  `stream` is a cudaStream_t
+ *    passed as void*.  Calls are stream-ordered and never synchronise the host.
+ *  - The library never allocates device memory: the caller provides a
+ *    workspace of tg_workspace_size() bytes (256-byte aligned).
+ *  - Row t of `logits` scores `target[t]` (the host does the HF shift and drops
+ *    mask-false positions).  Rows of one sequence are contiguous; sequences of
+ *    one group are contiguous (seq_offsets / group_offsets are prefix sums).
+ *  - dlogits = d loss / d logits, written once per element; it MAY alias
+ *    `logits` (in place) when ld_out == ld and row_index == NULL.
+ *  - Errors: every entry point returns TG_OK or a TG_E* code; tg_last_error()
+ *    gives a message for the calling thread.  Data-dependent problems found on
+ *    the device (target outside [0, V), non-finite loss/gradient, pairwise
+ *    group of size < 2, DPO group of size != 2) are reported as counts in
+ *    stats[TG_S_INVALID] and stats[TG_S_NONFINITE]; the Python layer raises
+ *    AlgorithmError for them exactly where LossReport.__post_init__
+ *    (algorithms.py:65-69) or policy._check_generated_tokens (policy.py:175-178)
+ *    would have raised.
+ */
+#ifndef TG_LOSS_H_
+#define TG_LOSS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TG_ABI_VERSION 1
+
+/* return codes */
+enum { TG_OK = 0, TG_EINVAL = 1, TG_ECUDA = 2, TG_EUNSUPPORTED = 3, TG_EWORKSPACE = 4 };
+
+/* element type of logits / anchor_logits / dlogits (arithmetic is fp32) */
+enum { TG_DTYPE_BF16 = 0, TG_DTYPE_F32 = 1 };
+
+/* advantage_fn registry */
+enum {
+  TG_ADV_GIVEN = 0,     /* use TgBatch.advantage[seq]                                 */
+  TG_ADV_GRPO = 1,      /* (r - mean_g) / (std_g(unbiased) + std_eps); K = 1 -> 0     */
+  TG_ADV_RLOO = 2,      /* r_i - mean_{j != i} r_j; K = 1 -> 0                         */
+  TG_ADV_OPMD = 3,      /* (r - mean_g) / (1 + tau)      algorithms.py:234-242         */
+  TG_ADV_REINFORCE = 4  /* r                                                           */
+};
+
+/* policy_loss_fn registry */
+enum {
+  TG_PG_VANILLA = 0,        /* -A * lp                           (OPMD_SIMPLE form)     */
+  TG_PG_PPO_CLIP = 1,       /* max(-A rho, -A clip(rho)) [dual clip c]                   */
+  TG_PG_SFT = 2,            /* -lp (NLL)                          algorithms.py:256-274  */
+  TG_PG_OPMD_KIMI = 3,      /* sum_i (r_i - zeta - tau(LP_i - ref_i))^2   :118-153       */
+  TG_PG_OPMD_PAIRWISE = 4,  /* sum_{i<j} (a_i - a_j)^2                    :156-190       */
+  TG_PG_DPO = 5             /* mean softplus(-beta margin); groups are (chosen, rejected) */
+};
+
+/* kl_fn registry: token-level penalty kl_coef * kl(lp, ref_lp) */
+enum { TG_KL_NONE = 0, TG_KL_K1 = 1, TG_KL_K2 = 2, TG_KL_K3 = 3 /* low_var_kl */, TG_KL_ABS = 4 };
+
+/* entropy_loss_fn registry: loss -= entropy_coef * agg(H) */
+enum { TG_ENT_NONE = 0, TG_ENT_DEFAULT = 1 };
+
+/* loss_agg_mode registry: per-row weight w of RL rows */
+enum {
+  TG_AGG_SEQ_SUM = 0,                 /* w = 1 (the reference's semantics)             */
+  TG_AGG_TOKEN_MEAN = 1,              /* w = 1 / N_tok(RL, global)                     */
+  TG_AGG_SEQ_MEAN_TOKEN_SUM = 2,      /* w = 1 / B(RL, global)                         */
+  TG_AGG_SEQ_MEAN_TOKEN_MEAN = 3,     /* w = 1 / (B * n_i)                             */
+  TG_AGG_SEQ_MEAN_TOKEN_SUM_NORM = 4  /* w = 1 / agg_norm                              */
+};
+
+/* flags */
+enum {
+  TG_FLAG_FORCE_TWO_PASS = 1,  /* use the forward + backward streaming kernels even when
+                                  the fused single-pass kernel applies (testing / A-B)  */
+  TG_FLAG_NO_FUSED_TMA = 2     /* alias kept for clarity: same effect                   */
+};
+
+/* stats[] layout (double).  Sums are over this call's rows / groups; the
+   caller allreduces (sum) across ranks, then divides by n_groups for the
+   reference's averaged metrics (algorithms.py:377-378). */
+enum {
+  TG_S_LOSS = 0, TG_S_PG_LOSS, TG_S_KL_LOSS, TG_S_ENTROPY_LOSS, TG_S_ANCHOR_LOSS, TG_S_SFT_LOSS,
+  TG_S_N_GROUPS, TG_S_SUM_MEAN_REWARD, TG_S_SUM_BASELINE, TG_S_SUM_KL_ESTIMATE, TG_S_SUM_GROUP_SIZE,
+  TG_S_N_TOK, TG_S_N_TOK_RL, TG_S_CLIP_COUNT, TG_S_SUM_ENTROPY, TG_S_SUM_KL, TG_S_SUM_PPO_KL,
+  TG_S_SUM_LP, TG_S_NONFINITE, TG_S_N_SEQS, TG_S_SUM_ADV, TG_S_SUM_RATIO, TG_S_N_SFT_SEQS,
+  TG_S_SUM_SFT_REWARD, TG_S_SUM_DPO_MARGIN, TG_S_DUAL_CLIP_COUNT, TG_S_SUM_ANCHOR_KL,
+  TG_S_INVALID, TG_S_RESERVED28, TG_S_RESERVED29, TG_S_RESERVED30, TG_S_RESERVED31,
+  TG_NSTAT = 32
+};
+
+typedef struct TgConfig {
+  int32_t advantage_fn;     /* TG_ADV_*  */
+  int32_t policy_loss_fn;   /* TG_PG_*   */
+  int32_t kl_fn;            /* TG_KL_*   */
+  int32_t entropy_loss_fn;  /* TG_ENT_*  */
+  int32_t loss_agg_mode;    /* TG_AGG_*  */
+  int32_t flags;            /* TG_FLAG_* */
+  double tau;               /* OPMD temperature (>= 0; > 0 for KIMI / PAIRWISE)   */
+  double clip_lo, clip_hi;  /* PPO ratio clip range [1 - clip_lo, 1 + clip_hi]    */
+  double clip_c;            /* dual-clip constant (> 1), 0 = off                  */
+  double kl_coef;           /* token KL penalty coefficient                       */
+  double entropy_coef;      /* entropy bonus coefficient                          */
+  double std_eps;           /* GRPO std epsilon                                   */
+  double sft_weight;        /* weight of SFT (seq_kind = 1) rows: w = sft_weight / n_sft */
+  double anchor_beta;       /* beta of regularizer_g (needs anchor_logits)        */
+  double dpo_beta;          /* DPO beta (> 0)                                     */
+  double agg_norm;          /* divisor of TG_AGG_SEQ_MEAN_TOKEN_SUM_NORM          */
+  int64_t n_tok_global;     /* RL rows over all ranks (token-mean); 0 = this call's */
+  int64_t n_seq_global;     /* RL sequences over all ranks; 0 = this call's         */
+  int64_t n_sft_seq_global; /* SFT sequences over all ranks; 0 = this call's        */
+} TgConfig;
+
+typedef struct TgBatch {
+  int32_t dtype;                 /* TG_DTYPE_*                                           */
+  int32_t n_seqs;                /* B                                                    */
+  int32_t n_groups;              /* G                                                    */
+  int32_t reserved0;
+  int64_t n_rows;                /* T (trainable rows)                                   */
+  int64_t vocab;                 /* V                                                    */
+  int64_t ld;                    /* row pitch of logits, in elements (>= V)              */
+  const void* logits;            /* [*, ld]                                              */
+  const int64_t* row_index;      /* optional [T]: row t reads logits row row_index[t]    */
+  const void* anchor_logits;     /* optional [T, ld_anchor] (same dtype)                 */
+  int64_t ld_anchor;
+  const int32_t* target;         /* [T] token scored by row t                            */
+  const float* old_lp;           /* optional [T] behaviour logprob (PPO ratio, KL metric)*/
+  const float* ref_lp;           /* optional [T] reference-policy logprob (token KL)     */
+  const int32_t* seq_offsets;    /* [B+1] row prefix sums                                */
+  const int32_t* group_offsets;  /* [G+1] sequence prefix sums                           */
+  const float* reward;           /* [B]                                                  */
+  const float* seq_ref_lp;       /* optional [B] sequence reference logprob (OPMD / DPO);
+                                    default = sum of old_lp over the sequence
+                                    (records.py:119-121)                                 */
+  const float* advantage;        /* [B] for TG_ADV_GIVEN                                 */
+  const uint8_t* seq_kind;       /* optional [B]: 0 RL rollout, 1 SFT / expert           */
+} TgBatch;
+
+typedef struct TgOut {
+  void* dlogits;     /* [T, ld_out] d loss / d logits, or NULL (forward only)   */
+  int64_t ld_out;
+  float* lp;         /* optional [T] current-policy logprob of target          */
+  float* entropy;    /* optional [T] H_t                                        */
+  float* lse;        /* optional [T] log-sum-exp                                */
+  float* seq_lp;     /* optional [B] sum of lp over each sequence               */
+  float* seq_adv;    /* optional [B] advantage (or coupled coefficient)         */
+  double* stats;     /* [TG_NSTAT] device, required                             */
+} TgOut;
+
+/* Workspace bytes needed by tg_loss_fwd_bwd / tg_logprob_fwd for this batch. */
+size_t tg_workspace_size(const TgBatch* batch, const TgConfig* cfg);
+
+/* Loss + gradient.  Replaces group_loss over a batch of groups followed by
+   combine_reports (orchestrator.py:299-308, without apply_update). */
+int tg_loss_fwd_bwd(const TgBatch* batch, const TgConfig* cfg, TgOut* out,
+                    void* workspace, size_t workspace_bytes, void* stream);
+
+/* Forward-only logprob / entropy / lse (+ seq_lp) -- experience_logprob
+   (algorithms.py:81-85) for old / ref logprob recompute.  stats may be NULL. */
+int tg_logprob_fwd(const TgBatch* batch, TgOut* out, void* workspace,
+                   size_t workspace_bytes, void* stream);
+
+/* Which kernel route tg_loss_fwd_bwd takes for this input: 1 = fused single
+   pass (4V bytes/row), 2 = forward + backward streaming (6V), 3 = coupled. */
+int tg_route(const TgBatch* batch, const TgConfig* cfg);
+
+/* Timing hook (measurement only): when both are non-NULL cudaEvent_t handles,
+   the next tg_loss_fwd_bwd call on this thread records ev_begin on its stream
+   immediately before its first row kernel (k_fused_tma, or k_fwd on the
+   two-pass routes) and ev_end immediately after its last row kernel
+   (k_fused_tma / k_bwd).  The hook is consumed by that call. */
+int tg_set_timing_events(void* ev_begin, void* ev_end);
+
+/* Total CUDA kernel launches issued by this library in this process. */
+int64_t tg_launch_count(void);
+
+const char* tg_strerror(int code);
+const char* tg_last_error(void);
+int tg_abi_version(void);
+
+/* ---- host helpers (no device access) ------------------------------------ */
+
+/* Toy-table policy adapter (policy.py:152-161, 181-191; encoding.py:19-35):
+   for each experience e (tokens[tok_off[e]:tok_off[e+1]], mask likewise,
+   prompt length prompt_len[e]) write the bucket state and target token of
+   every mask-true position, in order.  Returns the number of rows written
+   (must equal the caller's capacity check) or -1 on error. */
+int64_t tg_scored_states(const int64_t* tokens, const uint8_t* mask, const int64_t* tok_off,
+                         const int64_t* prompt_len, int64_t n_exp, int64_t num_buckets,
+                         int64_t* states_out, int32_t* target_out, int64_t capacity);
+
+/* ExperienceBuffer.sample_batch(group_by_task=True) group indexing
+   (buffer.py:240-264) over READY experiences given in insertion order:
+   policy 0 = FIFO, 1 = PRIORITY (descending priority, ties by sample_id rank
+   given in `id_rank`).  Writes up to n_take groups of group_size indices into
+   groups_out and returns the number of groups. */
+int64_t tg_group_by_task(const int64_t* task_key, const double* priority,
+                         const int64_t* id_rank, const uint8_t* ready, int64_t n,
+                         int64_t group_size, int64_t n_take, int32_t policy,
+                         int64_t* groups_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TG_LOSS_H_ */

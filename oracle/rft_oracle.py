@@ -379,7 +379,7 @@ STAT_NAMES = [
     "n_tok", "n_tok_rl", "clip_count", "sum_entropy", "sum_kl", "sum_ppo_kl",
     "sum_lp", "nonfinite", "n_seqs", "sum_adv", "sum_ratio", "n_sft_seqs",
     "sum_sft_reward", "sum_dpo_margin", "dual_clip_count", "sum_anchor_kl",
-    "reserved27", "reserved28", "reserved29", "reserved30", "reserved31",
+    "invalid", "reserved28", "reserved29", "reserved30", "reserved31",
 ]
 STAT = {n: i for i, n in enumerate(STAT_NAMES)}
 NSTAT = len(STAT_NAMES)
@@ -399,7 +399,8 @@ def row_forward(logits: np.ndarray, target: np.ndarray, block: int = 512):
         l = m + np.log(s)
         lse[a:a + block] = l
         lp[a:a + block] = X[np.arange(X.shape[0]), target[a:a + block]] - l
-        ent[a:a + block] = l - (e * X).sum(axis=1) / s
+        # -inf logits (masked vocabulary entries) carry p = 0 and add nothing
+        ent[a:a + block] = l - (e * np.maximum(X, -1e30)).sum(axis=1) / s
     return lse, lp, ent
 
 
@@ -616,7 +617,7 @@ def general_loss(batch: Batch, cfg: Config, want_dz: bool = True) -> Dict[str, o
 
     dz = None
     if want_dz:
-        X = batch.logits
+        X = np.maximum(batch.logits, -1e30)   # p = 0 exactly where a logit is -inf
         p = np.exp(X - lse[:, None])
         dz = p * (s[:, None] + h[:, None] * ((X - lse[:, None]) + ent[:, None]))
         dz[np.arange(T), batch.target] -= s
@@ -660,3 +661,71 @@ def general_loss(batch: Batch, cfg: Config, want_dz: bool = True) -> Dict[str, o
 
 def stats_dict(st: np.ndarray) -> Dict[str, float]:
     return {n: float(st[i]) for i, n in enumerate(STAT_NAMES) if not n.startswith("reserved")}
+
+
+def single_pass_blocked(batch: Batch, cfg: Config, dz_out: Optional[np.ndarray] = None,
+                        block: int = 64) -> Dict[str, object]:
+    """Memory-bounded restatement of ``general_loss`` for the single-pass
+    policy losses (vanilla / ppo_clip / sft, any advantage / KL / entropy /
+    aggregation, no anchor): rows are processed in blocks, so Qwen-vocab
+    samples fit in host RAM.  Used as the timed CPU baseline (bench.py) and
+    checked against ``general_loss`` in tests/test_oracle.py."""
+    if cfg.policy_loss_fn not in ("vanilla", "ppo_clip", "sft") or cfg.anchor_beta > 0:
+        raise ValueError("single_pass_blocked handles single-pass losses without anchor")
+    T = batch.n_rows
+    B = batch.n_seqs
+    kind = batch.seq_kind if batch.seq_kind is not None else np.zeros(B, np.int64)
+    A = advantages(batch, cfg)
+    w = seq_weights(batch, cfg)
+    row_seq = np.repeat(np.arange(B), np.diff(batch.seq_offsets))
+    is_rl = kind[row_seq] == 0
+    lse = np.empty(T)
+    lp = np.empty(T)
+    ent = np.empty(T)
+    loss = np.zeros(4)  # pg, kl, ent, sft
+    c_ent = cfg.entropy_coef if cfg.entropy_loss_fn != "none" else 0.0
+    for a in range(0, T, block):
+        b = min(a + block, T)
+        X = np.maximum(np.asarray(batch.logits[a:b], dtype=np.float64), -1e30)
+        y = batch.target[a:b]
+        m = X.max(axis=1)
+        e = np.exp(X - m[:, None])
+        s_ = e.sum(axis=1)
+        l = m + np.log(s_)
+        lpb = X[np.arange(b - a), y] - l
+        hb = l - (e * X).sum(axis=1) / s_
+        lse[a:b], lp[a:b], ent[a:b] = l, lpb, hb
+        At, wt, rl = A[row_seq[a:b]], w[row_seq[a:b]], is_rl[a:b]
+        if cfg.policy_loss_fn == "ppo_clip":
+            old = batch.old_lp[a:b] if batch.old_lp is not None else lpb
+            rho = np.exp(np.clip(lpb - old, -20.0, 20.0))
+            l1 = -At * rho
+            l2 = -At * np.clip(rho, 1.0 - cfg.clip_lo, 1.0 + cfg.clip_hi)
+            pg = np.maximum(l1, l2)
+            s_pg = np.where(l2 > l1, 0.0, At * rho)
+            if cfg.clip_c > 0:
+                l3 = -At * cfg.clip_c
+                dual = (At < 0) & (l3 < pg)
+                pg = np.where(dual, l3, pg)
+                s_pg = np.where(dual, 0.0, s_pg)
+        elif cfg.policy_loss_fn == "sft":
+            pg, s_pg = -lpb, np.ones(b - a)
+        else:
+            pg, s_pg = -At * lpb, At.copy()
+        klv = np.zeros(b - a)
+        s_kl = np.zeros(b - a)
+        if cfg.kl_fn != "none":
+            ref = batch.ref_lp[a:b] if batch.ref_lp is not None else lpb
+            klv, dkl = _kl_value_grad(cfg.kl_fn, lpb, ref)
+            s_kl = -cfg.kl_coef * dkl
+        s = np.where(rl, wt * (s_pg + s_kl), wt)
+        h = np.where(rl, c_ent * wt, 0.0)
+        loss += [np.where(rl, wt * pg, 0).sum(), np.where(rl, wt * cfg.kl_coef * klv, 0).sum(),
+                 np.where(rl, -c_ent * wt * hb, 0).sum(), np.where(rl, 0, -wt * lpb).sum()]
+        p = e / s_[:, None]
+        dz = p * (s[:, None] + h[:, None] * ((X - l[:, None]) + hb[:, None]))
+        dz[np.arange(b - a), y] -= s
+        if dz_out is not None:
+            dz_out[a:b] = dz
+    return {"loss": float(loss.sum()), "pg_loss": loss[0], "kl_loss": loss[1],
+            "entropy_loss": loss[2], "sft_loss": loss[3], "lp": lp, "entropy": ent, "lse": lse}

@@ -1,0 +1,84 @@
+"""Build libtg_loss.so in-tree with nvcc for sm_100a (B200).
+
+    python -m paper_2505_17826_b200._build [--verbose]
+
+Outputs ``paper_2505_17826_b200/_lib/libtg_loss.so``.  The CUDA runtime is
+linked statically, so the library only needs the driver at load time.
+"""
+
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIBDIR = PKG / "_lib"
+LIB = LIBDIR / "libtg_loss.so"
+OBJDIR = ROOT / "build" / "obj"
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+              "-I", str(ROOT / "include"), "-I", str(CSRC)]
+CU_SOURCES = ["tg_fused_tma.cu", "tg_stream.cu", "tg_group.cu", "tg_api.cu"]
+CPP_SOURCES = ["tg_host.cpp"]
+
+
+def nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
+        if cand and Path(cand).exists():
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def _run(cmd, verbose):
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError(f"build step failed: {' '.join(cmd[:3])} ...")
+    if verbose and (res.stdout or res.stderr):
+        sys.stderr.write(res.stdout + res.stderr)
+    return res
+
+
+def _stale(target: Path, deps) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(Path(d).stat().st_mtime > t for d in deps)
+
+
+def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = False) -> Path:
+    OBJDIR.mkdir(parents=True, exist_ok=True)
+    LIBDIR.mkdir(parents=True, exist_ok=True)
+    headers = list(CSRC.glob("*.cuh")) + [ROOT / "include" / "tg_loss.h"]
+    objs = []
+    for src in CU_SOURCES:
+        obj = OBJDIR / (src + ".o")
+        objs.append(obj)
+        if force or _stale(obj, [CSRC / src, *headers]):
+            extra = ["-Xptxas", "-v"] if ptxas_verbose else []
+            _run([nvcc(), *ARCH, *NVCC_FLAGS, *extra, "-c", str(CSRC / src), "-o", str(obj)],
+                 verbose or ptxas_verbose)
+    for src in CPP_SOURCES:
+        obj = OBJDIR / (src + ".o")
+        objs.append(obj)
+        if force or _stale(obj, [CSRC / src, *headers]):
+            _run(["g++", "-O2", "-std=c++17", "-fPIC", "-I", str(ROOT / "include"), "-c",
+                  str(CSRC / src), "-o", str(obj)], verbose)
+    if force or _stale(LIB, objs):
+        _run([nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs)],
+             verbose)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(verbose="--verbose" in sys.argv, force="--force" in sys.argv,
+          ptxas_verbose="--ptxas" in sys.argv)
+    print(LIB)

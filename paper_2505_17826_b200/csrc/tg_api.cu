@@ -1,0 +1,479 @@
+// tg_api.cu -- extern "C" entry points of libtg_loss.so (include/tg_loss.h).
+//
+// Host-side validation mirrors the reference's error behaviour
+// (AlgorithmConfig.__post_init__ algorithms.py:44-56, loss-specific checks
+// algorithms.py:129-135, 164-167, 232-233, 286-289), then the launch plan:
+//
+//   route 1 (single-pass losses, TMA-eligible input):
+//       k_counts, k_prep -> k_rowmeta -> k_fused_tma -> k_seq_reduce -> k_finalize
+//   route 2 (anchor KL, unaligned input, forced):
+//       k_counts, k_prep -> k_rowmeta -> k_fwd -> k_rowcoef -> k_bwd -> k_seq_reduce -> k_finalize
+//   route 3 (sequence-coupled OPMD_KIMI / OPMD_PAIRWISE / DPO):
+//       k_counts, k_prep -> k_rowmeta -> k_fwd -> k_seq_reduce -> k_coupled -> k_rowcoef
+//       -> k_bwd -> k_finalize
+//
+// Everything is enqueued on the caller's stream; nothing synchronises.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <mutex>
+#include <string>
+
+#include "tg_common.cuh"
+
+namespace tg {
+size_t fused_smem_bytes(int n_slots);
+cudaError_t launch_fused(const KParams& P, const void* meta, int cl, int n_slots, int n_ctas,
+                         cudaStream_t stream);
+int fused_chunk_bytes();
+int fused_max_slots();
+size_t rowmeta_bytes();
+void launch_fwd(const KParams& P, bool anchor, bool vec, int grid, cudaStream_t st);
+void launch_bwd(const KParams& P, bool anchor, bool vec, int grid, cudaStream_t st);
+void launch_rowcoef(const KParams& P, const void* meta, bool coupled, bool anchor, int grid,
+                    cudaStream_t st);
+void launch_group_prep(const KParams& P, bool coupled, cudaStream_t st);
+void launch_rowmeta(const KParams& P, void* meta, cudaStream_t st);
+void launch_seq_reduce(const KParams& P, cudaStream_t st);
+void launch_coupled(const KParams& P, cudaStream_t st);
+void launch_finalize(const KParams& P, bool coupled, cudaStream_t st);
+}  // namespace tg
+
+using namespace tg;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local cudaEvent_t g_ev_begin = nullptr, g_ev_end = nullptr;
+std::atomic<int64_t> g_launches{0};
+
+void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+struct DevInfo {
+  int sms = 0;
+  int smem_optin = 0;
+};
+
+DevInfo dev_info() {
+  static std::mutex mu;
+  static DevInfo cache[64];
+  static bool have[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!have[dev]) {
+    cudaDeviceGetAttribute(&cache[dev].sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&cache[dev].smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    have[dev] = true;
+  }
+  return cache[dev];
+}
+
+constexpr int kMaxPartials = 1024;
+constexpr size_t kAlign = 256;
+
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+int esz_of(int dtype) { return dtype == TG_DTYPE_BF16 ? 2 : 4; }
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+struct Layout {
+  size_t meta, lp, ent, lse, rS, rA, rHz, rCa, rLseQ, rAkl, sA, sW, sK, sLP, sRef, gF, partials,
+      counts, seq_lp, total;
+};
+
+Layout layout(const TgBatch* b) {
+  const size_t T = size_t(b->n_rows > 0 ? b->n_rows : 0);
+  const size_t B = size_t(b->n_seqs > 0 ? b->n_seqs : 0);
+  const size_t G = size_t(b->n_groups > 0 ? b->n_groups : 0);
+  Layout L;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o += align_up(bytes);
+    return at;
+  };
+  L.meta = take(T * rowmeta_bytes());
+  L.lp = take(T * 4);
+  L.ent = take(T * 4);
+  L.lse = take(T * 4);
+  L.rS = take(T * 4);
+  L.rA = take(T * 4);
+  L.rHz = take(T * 4);
+  L.rCa = take(T * 4);
+  L.rLseQ = take(T * 4);
+  L.rAkl = take(T * 4);
+  L.sA = take(B * 4);
+  L.sW = take(B * 4);
+  L.sK = take(B * 4);
+  L.sLP = take(B * 8);
+  L.sRef = take(B * 8);
+  L.gF = take(G * 4 * 8);
+  L.partials = take(size_t(kMaxPartials) * TG_NSTAT * 8);
+  L.counts = take(4 * 8);
+  L.seq_lp = take(B * 4);
+  L.total = o + kAlign;  // slack for re-aligning an unaligned base pointer
+  return L;
+}
+
+bool coupled_pg(int pg) {
+  return pg == TG_PG_OPMD_KIMI || pg == TG_PG_OPMD_PAIRWISE || pg == TG_PG_DPO;
+}
+
+int validate_batch(const TgBatch* b) {
+  if (!b) return fail(TG_EINVAL, "batch is NULL");
+  if (b->dtype != TG_DTYPE_BF16 && b->dtype != TG_DTYPE_F32)
+    return fail(TG_EINVAL, "unknown dtype %d", b->dtype);
+  if (b->n_rows < 0 || b->n_seqs < 0 || b->n_groups < 0)
+    return fail(TG_EINVAL, "negative sizes (rows %lld, seqs %d, groups %d)",
+                (long long)b->n_rows, b->n_seqs, b->n_groups);
+  if (b->vocab < 1) return fail(TG_EINVAL, "vocab must be >= 1, got %lld", (long long)b->vocab);
+  if (b->ld < b->vocab)
+    return fail(TG_EINVAL, "ld %lld < vocab %lld", (long long)b->ld, (long long)b->vocab);
+  if (b->n_rows > 0 && (!b->logits || !b->target))
+    return fail(TG_EINVAL, "logits and target are required when n_rows > 0");
+  if (!b->seq_offsets) return fail(TG_EINVAL, "seq_offsets is required");
+  if (b->n_groups > 0 && !b->group_offsets) return fail(TG_EINVAL, "group_offsets is required");
+  if (b->n_seqs > 0 && !b->reward) return fail(TG_EINVAL, "reward is required");
+  if (b->anchor_logits && b->ld_anchor < b->vocab)
+    return fail(TG_EINVAL, "ld_anchor %lld < vocab", (long long)b->ld_anchor);
+  return TG_OK;
+}
+
+int validate_cfg(const TgBatch* b, const TgConfig* c) {
+  if (!c) return fail(TG_EINVAL, "config is NULL");
+  if (c->advantage_fn < TG_ADV_GIVEN || c->advantage_fn > TG_ADV_REINFORCE)
+    return fail(TG_EINVAL, "unknown advantage_fn %d", c->advantage_fn);
+  if (c->policy_loss_fn < TG_PG_VANILLA || c->policy_loss_fn > TG_PG_DPO)
+    return fail(TG_EINVAL, "unknown policy_loss_fn %d", c->policy_loss_fn);
+  if (c->kl_fn < TG_KL_NONE || c->kl_fn > TG_KL_ABS)
+    return fail(TG_EINVAL, "unknown kl_fn %d", c->kl_fn);
+  if (c->entropy_loss_fn != TG_ENT_NONE && c->entropy_loss_fn != TG_ENT_DEFAULT)
+    return fail(TG_EINVAL, "unknown entropy_loss_fn %d", c->entropy_loss_fn);
+  if (c->loss_agg_mode < TG_AGG_SEQ_SUM || c->loss_agg_mode > TG_AGG_SEQ_MEAN_TOKEN_SUM_NORM)
+    return fail(TG_EINVAL, "unknown loss_agg_mode %d", c->loss_agg_mode);
+  if (!(c->tau >= 0)) return fail(TG_EINVAL, "tau must be >= 0, got %g", c->tau);
+  if ((c->policy_loss_fn == TG_PG_OPMD_KIMI || c->policy_loss_fn == TG_PG_OPMD_PAIRWISE) &&
+      !(c->tau > 0))
+    return fail(TG_EINVAL, "%s requires tau > 0",
+                c->policy_loss_fn == TG_PG_OPMD_KIMI ? "OPMD_KIMI" : "OPMD_PAIRWISE");
+  if (!(c->anchor_beta >= 0)) return fail(TG_EINVAL, "beta must be >= 0, got %g", c->anchor_beta);
+  if (c->anchor_beta > 0 && !b->anchor_logits)
+    return fail(TG_EINVAL, "beta > 0 requires sft_params (anchor_logits)");
+  if (!(c->dpo_beta > 0)) return fail(TG_EINVAL, "dpo_beta must be > 0, got %g", c->dpo_beta);
+  if (!(c->clip_lo >= 0) || !(c->clip_hi >= 0))
+    return fail(TG_EINVAL, "clip ranges must be >= 0");
+  if (c->clip_c != 0 && !(c->clip_c > 1)) return fail(TG_EINVAL, "clip_c must be 0 or > 1");
+  if (!(c->std_eps >= 0)) return fail(TG_EINVAL, "std_eps must be >= 0");
+  if (!(c->sft_weight >= 0)) return fail(TG_EINVAL, "sft_weight must be >= 0");
+  if (c->loss_agg_mode == TG_AGG_SEQ_MEAN_TOKEN_SUM_NORM && !(c->agg_norm > 0))
+    return fail(TG_EINVAL, "agg_norm must be > 0");
+  if (c->advantage_fn == TG_ADV_GIVEN && !coupled_pg(c->policy_loss_fn) && b->n_seqs > 0 &&
+      !b->advantage)
+    return fail(TG_EINVAL, "advantage_fn GIVEN requires batch.advantage");
+  return TG_OK;
+}
+
+void fill_params(KParams& P, const TgBatch* b, const TgConfig* c, const TgOut* o, char* ws,
+                 const Layout& L) {
+  memset(&P, 0, sizeof(P));
+  P.logits = b->logits;
+  P.row_index = b->row_index;
+  P.anchor = b->anchor_logits;
+  P.n_rows = b->n_rows;
+  P.vocab = b->vocab;
+  P.ld = b->ld;
+  P.ld_anchor = b->ld_anchor;
+  P.ld_out = (o && o->dlogits) ? o->ld_out : b->ld;
+  P.dtype = b->dtype;
+  P.n_seqs = b->n_seqs;
+  P.n_groups = b->n_groups;
+  P.target = b->target;
+  P.old_lp = b->old_lp;
+  P.ref_lp = b->ref_lp;
+  P.seq_off = b->seq_offsets;
+  P.grp_off = b->group_offsets;
+  P.reward = b->reward;
+  P.seq_ref_lp = b->seq_ref_lp;
+  P.advantage = b->advantage;
+  P.seq_kind = b->seq_kind;
+  P.dz = o ? o->dlogits : nullptr;
+  P.lp = (o && o->lp) ? o->lp : reinterpret_cast<float*>(ws + L.lp);
+  P.ent = (o && o->entropy) ? o->entropy : reinterpret_cast<float*>(ws + L.ent);
+  P.lse = (o && o->lse) ? o->lse : reinterpret_cast<float*>(ws + L.lse);
+  P.seq_lp = (o && o->seq_lp) ? o->seq_lp : reinterpret_cast<float*>(ws + L.seq_lp);
+  P.seq_adv = o ? o->seq_adv : nullptr;
+  P.stats = o ? o->stats : nullptr;
+  P.sA = reinterpret_cast<float*>(ws + L.sA);
+  P.sW = reinterpret_cast<float*>(ws + L.sW);
+  P.sK = reinterpret_cast<float*>(ws + L.sK);
+  P.sLP = reinterpret_cast<double*>(ws + L.sLP);
+  P.sRef = reinterpret_cast<double*>(ws + L.sRef);
+  P.gF = reinterpret_cast<double*>(ws + L.gF);
+  P.rS = reinterpret_cast<float*>(ws + L.rS);
+  P.rA = reinterpret_cast<float*>(ws + L.rA);
+  P.rHz = reinterpret_cast<float*>(ws + L.rHz);
+  P.rCa = reinterpret_cast<float*>(ws + L.rCa);
+  P.rLseQ = reinterpret_cast<float*>(ws + L.rLseQ);
+  P.rAkl = reinterpret_cast<float*>(ws + L.rAkl);
+  P.partials = reinterpret_cast<double*>(ws + L.partials);
+  P.counts = reinterpret_cast<int64_t*>(ws + L.counts);
+  if (c) {
+    P.adv = c->advantage_fn;
+    P.pg = c->policy_loss_fn;
+    P.kl = c->kl_fn;
+    P.entf = c->entropy_loss_fn;
+    P.agg = c->loss_agg_mode;
+    P.flags = c->flags;
+    P.tau = float(c->tau);
+    P.clip_lo = float(c->clip_lo);
+    P.clip_hi = float(c->clip_hi);
+    P.clip_c = float(c->clip_c);
+    P.kl_coef = float(c->kl_coef);
+    P.ent_coef = float(c->entropy_coef);
+    P.std_eps = float(c->std_eps);
+    P.sft_w = float(c->sft_weight);
+    P.anchor_beta = float(c->anchor_beta);
+    P.dpo_beta = float(c->dpo_beta);
+    P.agg_norm = float(c->agg_norm);
+    P.n_tok_g = c->n_tok_global;
+    P.n_seq_g = c->n_seq_global;
+    P.n_sft_g = c->n_sft_seq_global;
+  }
+}
+
+// Fused-kernel plan: cluster size and ring slots, or cl = 0 if not eligible.
+struct FusedPlan {
+  int cl = 0, n_slots = 0, n_ctas = 0;
+};
+
+FusedPlan fused_plan(const TgBatch* b, const TgOut* o) {
+  FusedPlan fp;
+  const int esz = esz_of(b->dtype);
+  const int epv = 16 / esz;
+  if (!o || !o->dlogits) return fp;
+  if (!aligned16(b->logits) || (b->ld * esz) % 16 != 0) return fp;
+  if (!aligned16(o->dlogits) || (o->ld_out * esz) % 16 != 0 || o->ld_out < b->vocab) return fp;
+  const int64_t nvec = (b->vocab + epv - 1) / epv;
+  if (b->ld < nvec * epv) return fp;  // TMA reads whole 16-byte vectors
+  const DevInfo d = dev_info();
+  if (d.sms <= 0) return fp;
+  const size_t tail = fused_smem_bytes(0);
+  int n_slots = int((size_t(d.smem_optin) - tail) / size_t(fused_chunk_bytes()));
+  if (n_slots > fused_max_slots()) n_slots = fused_max_slots();
+  for (int cl = 1; cl <= 4; cl *= 2) {
+    const int64_t slice_vec = (nvec + cl - 1) / cl;
+    const int64_t nchunk = (slice_vec * 16 + fused_chunk_bytes() - 1) / fused_chunk_bytes();
+    if (nchunk + 2 <= n_slots) {
+      fp.cl = cl;
+      fp.n_slots = n_slots;
+      const int64_t clusters_max = d.sms / cl;
+      const int64_t clusters = b->n_rows < clusters_max ? b->n_rows : clusters_max;
+      fp.n_ctas = int(clusters * cl);
+      return fp;
+    }
+  }
+  return fp;
+}
+
+int route_of(const TgBatch* b, const TgConfig* c, const TgOut* o) {
+  if (coupled_pg(c->policy_loss_fn)) return 3;
+  if (c->anchor_beta > 0) return 2;
+  if (c->flags & (TG_FLAG_FORCE_TWO_PASS | TG_FLAG_NO_FUSED_TMA)) return 2;
+  if (!o || !o->dlogits) return 2;
+  if (fused_plan(b, o).cl == 0) return 2;
+  return 1;
+}
+
+int stream_grid(int64_t rows) {
+  const DevInfo d = dev_info();
+  const int64_t cap = int64_t(d.sms > 0 ? d.sms : 148) * 8;
+  return int(rows < cap ? (rows > 0 ? rows : 1) : cap);
+}
+
+bool vec_ok(const void* p, int64_t ld, int esz) {
+  return aligned16(p) && (ld * esz) % 16 == 0;
+}
+
+char* align_ws(void* ws) {
+  uintptr_t p = reinterpret_cast<uintptr_t>(ws);
+  p = (p + kAlign - 1) / kAlign * kAlign;
+  return reinterpret_cast<char*>(p);
+}
+
+int check_cuda(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(TG_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  return TG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t tg_workspace_size(const TgBatch* batch, const TgConfig* /*cfg*/) {
+  if (!batch) return 0;
+  return layout(batch).total;
+}
+
+int tg_route(const TgBatch* batch, const TgConfig* cfg) {
+  if (!batch || !cfg) return 0;
+  TgOut probe = {};
+  probe.dlogits = const_cast<void*>(batch->logits);
+  probe.ld_out = batch->ld;
+  return route_of(batch, cfg, &probe);
+}
+
+int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspace,
+                    size_t workspace_bytes, void* stream) {
+  int rc = validate_batch(b);
+  if (rc) return rc;
+  rc = validate_cfg(b, c);
+  if (rc) return rc;
+  if (!o || !o->stats) return fail(TG_EINVAL, "out.stats is required");
+  if (o->dlogits) {
+    if (o->ld_out < b->vocab) return fail(TG_EINVAL, "ld_out < vocab");
+    if (o->dlogits == b->logits && (b->row_index || o->ld_out != b->ld))
+      return fail(TG_EINVAL, "in-place dlogits requires ld_out == ld and no row_index");
+  }
+  const Layout L = layout(b);
+  if (!workspace || workspace_bytes < L.total)
+    return fail(TG_EWORKSPACE, "workspace too small: need %zu bytes, got %zu", L.total,
+                workspace_bytes);
+  char* ws = align_ws(workspace);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  KParams P;
+  fill_params(P, b, c, o, ws, L);
+  void* meta = ws + L.meta;
+  const int route = route_of(b, c, o);
+  const bool coupled = route == 3;
+  const bool anchor = c->anchor_beta > 0;
+  const int esz = esz_of(b->dtype);
+  cudaGetLastError();  // clear stale errors
+
+  cudaEvent_t ev_begin = g_ev_begin, ev_end = g_ev_end;
+  g_ev_begin = g_ev_end = nullptr;
+  launch_group_prep(P, coupled, st);
+  launch_rowmeta(P, meta, st);
+  count_launches(1 + (b->n_groups > 0 ? 1 : 0) + (b->n_seqs > 0 ? 1 : 0));
+  if (route == 1) {
+    const FusedPlan fp = fused_plan(b, o);
+    P.n_partials = fp.n_ctas;
+    if (fp.n_ctas > kMaxPartials) return fail(TG_EUNSUPPORTED, "too many CTAs");
+    if (b->n_rows > 0) {
+      if (ev_begin) cudaEventRecord(ev_begin, st);
+      cudaError_t e = launch_fused(P, meta, fp.cl, fp.n_slots, fp.n_ctas, st);
+      if (ev_end) cudaEventRecord(ev_end, st);
+      if (e != cudaSuccess) return fail(TG_ECUDA, "fused kernel launch: %s", cudaGetErrorString(e));
+      count_launches(1);
+    } else {
+      P.n_partials = 0;
+    }
+    launch_seq_reduce(P, st);
+    count_launches(b->n_seqs > 0 ? 1 : 0);
+  } else {
+    const bool vin = vec_ok(b->logits, b->ld, esz) &&
+                     (!anchor || vec_ok(b->anchor_logits, b->ld_anchor, esz));
+    const int grid = stream_grid(b->n_rows);
+    if (ev_begin) cudaEventRecord(ev_begin, st);
+    if (b->n_rows > 0) {
+      launch_fwd(P, anchor, vin, grid, st);
+      count_launches(1);
+    }
+    if (coupled) {
+      launch_seq_reduce(P, st);
+      launch_coupled(P, st);
+      count_launches((b->n_seqs > 0 ? 1 : 0) + (b->n_groups > 0 ? 1 : 0));
+    }
+    int cgrid = int((b->n_rows + 255) / 256);
+    if (cgrid < 1) cgrid = 1;
+    if (cgrid > kMaxPartials) cgrid = kMaxPartials;
+    P.n_partials = cgrid;
+    launch_rowcoef(P, meta, coupled, anchor, cgrid, st);
+    count_launches(1);
+    if (o->dlogits && b->n_rows > 0) {
+      const bool vout = vin && vec_ok(o->dlogits, o->ld_out, esz);
+      launch_bwd(P, anchor, vout, grid, st);
+      count_launches(1);
+    }
+    if (ev_end) cudaEventRecord(ev_end, st);
+    if (!coupled) {
+      launch_seq_reduce(P, st);
+      count_launches(b->n_seqs > 0 ? 1 : 0);
+    }
+  }
+  launch_finalize(P, coupled, st);
+  count_launches(1);
+  return check_cuda("tg_loss_fwd_bwd");
+}
+
+int tg_logprob_fwd(const TgBatch* b, TgOut* o, void* workspace, size_t workspace_bytes,
+                   void* stream) {
+  int rc = validate_batch(b);
+  if (rc) return rc;
+  if (!o) return fail(TG_EINVAL, "out is NULL");
+  const Layout L = layout(b);
+  if (!workspace || workspace_bytes < L.total)
+    return fail(TG_EWORKSPACE, "workspace too small: need %zu bytes, got %zu", L.total,
+                workspace_bytes);
+  char* ws = align_ws(workspace);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  KParams P;
+  fill_params(P, b, nullptr, o, ws, L);
+  P.dz = nullptr;
+  cudaGetLastError();
+  const int esz = esz_of(b->dtype);
+  if (b->n_rows > 0) {
+    launch_fwd(P, false, vec_ok(b->logits, b->ld, esz), stream_grid(b->n_rows), st);
+    count_launches(1);
+  }
+  if (o->seq_lp && b->n_seqs > 0) {
+    launch_seq_reduce(P, st);
+    count_launches(1);
+  }
+  return check_cuda("tg_logprob_fwd");
+}
+
+const char* tg_strerror(int code) {
+  switch (code) {
+    case TG_OK: return "ok";
+    case TG_EINVAL: return "invalid argument";
+    case TG_ECUDA: return "CUDA error";
+    case TG_EUNSUPPORTED: return "unsupported";
+    case TG_EWORKSPACE: return "workspace too small";
+    default: return "unknown error";
+  }
+}
+
+const char* tg_last_error(void) { return g_err.c_str(); }
+
+int tg_set_timing_events(void* ev_begin, void* ev_end) {
+  g_ev_begin = reinterpret_cast<cudaEvent_t>(ev_begin);
+  g_ev_end = reinterpret_cast<cudaEvent_t>(ev_end);
+  if ((ev_begin == nullptr) != (ev_end == nullptr)) {
+    g_ev_begin = g_ev_end = nullptr;
+    return fail(TG_EINVAL, "set both timing events or neither");
+  }
+  return TG_OK;
+}
+
+int64_t tg_launch_count(void) { return g_launches.load(); }
+
+int tg_abi_version(void) { return TG_ABI_VERSION; }
+
+}  // extern "C"

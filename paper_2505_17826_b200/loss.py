@@ -1,0 +1,223 @@
+"""Public API: the fused RFT loss over packed device tensors.
+
+``RFTLoss(cfg)(batch)`` enqueues the CUDA pipeline of ``tg_loss_fwd_bwd`` on
+the current torch stream and returns device tensors (loss statistics,
+per-row logprob / entropy, per-sequence LP and advantage, and dlogits).
+Nothing synchronises until ``LossOutput.metrics()`` reads the 256-byte stats
+vector back.  Replaces ``group_loss`` over a batch + ``combine_reports``
+(algorithms.py:351-379) -- see triad_compat.py for the reference-shaped
+wrappers.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Dict, Optional, Union
+
+import torch
+
+from . import _native as N
+from .config import AlgorithmError, RFTLossConfig
+from .packing import PackedBatch
+
+_DTYPES = {torch.bfloat16: N.TG_DTYPE_BF16, torch.float32: N.TG_DTYPE_F32}
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _check_dev(t: Optional[torch.Tensor], dev: torch.device, name: str, dtype=None):
+    if t is None:
+        return
+    if t.device != dev:
+        raise ValueError(f"{name} is on {t.device}, expected {dev}")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def c_batch(b: PackedBatch) -> N.TgBatch:
+    """PackedBatch -> TgBatch (device pointers, no copies)."""
+    lg = b.logits
+    if lg.dim() != 2:
+        raise ValueError("logits must be 2-D [rows, ld] (flatten [B, L, V] first)")
+    if lg.dtype not in _DTYPES:
+        raise ValueError(f"logits dtype {lg.dtype} unsupported (bf16 or f32)")
+    if lg.stride(1) != 1:
+        raise ValueError("logits rows must be contiguous (stride(1) == 1)")
+    dev = lg.device
+    if dev.type != "cuda":
+        raise RuntimeError("the RFT loss runs only on CUDA devices (no CPU fallback)")
+    _check_dev(b.target, dev, "target", torch.int32)
+    _check_dev(b.seq_offsets, dev, "seq_offsets", torch.int32)
+    _check_dev(b.group_offsets, dev, "group_offsets", torch.int32)
+    _check_dev(b.reward, dev, "reward", torch.float32)
+    for name in ("old_lp", "ref_lp", "seq_ref_lp", "advantage"):
+        _check_dev(getattr(b, name), dev, name, torch.float32)
+    _check_dev(b.seq_kind, dev, "seq_kind", torch.uint8)
+    _check_dev(b.row_index, dev, "row_index", torch.int64)
+    c = N.TgBatch()
+    c.dtype = _DTYPES[lg.dtype]
+    c.n_seqs, c.n_groups = b.n_seqs, b.n_groups
+    c.n_rows, c.vocab, c.ld = b.n_rows, b.vocab, lg.stride(0)
+    c.logits = lg.data_ptr()
+    c.row_index = _ptr(b.row_index)
+    if b.anchor_logits is not None:
+        a = b.anchor_logits
+        if a.dtype != lg.dtype or a.device != dev or a.stride(1) != 1:
+            raise ValueError("anchor_logits must match logits' dtype / device / row layout")
+        c.anchor_logits = a.data_ptr()
+        c.ld_anchor = a.stride(0)
+    c.target = b.target.data_ptr()
+    c.old_lp, c.ref_lp = _ptr(b.old_lp), _ptr(b.ref_lp)
+    c.seq_offsets, c.group_offsets = b.seq_offsets.data_ptr(), b.group_offsets.data_ptr()
+    c.reward = b.reward.data_ptr()
+    c.seq_ref_lp, c.advantage, c.seq_kind = _ptr(b.seq_ref_lp), _ptr(b.advantage), _ptr(b.seq_kind)
+    return c
+
+
+@dataclass
+class LossOutput:
+    stats: torch.Tensor                   # [32] float64 (layout _native.STAT_NAMES)
+    lp: torch.Tensor                      # [T] f32
+    entropy: torch.Tensor                 # [T] f32
+    lse: torch.Tensor                     # [T] f32
+    seq_lp: torch.Tensor                  # [B] f32
+    seq_adv: torch.Tensor                 # [B] f32 (advantage, or coupled coefficient)
+    dlogits: Optional[torch.Tensor] = None
+
+    def stats_dict(self) -> Dict[str, float]:
+        """Device -> host read of the statistics (the only sync)."""
+        host = self.stats.detach().cpu().tolist()
+        return {n: host[i] for i, n in enumerate(N.STAT_NAMES) if not n.startswith("reserved")}
+
+    def metrics(self, check: bool = True) -> Dict[str, float]:
+        """combine_reports-style metrics (algorithms.py:377-378): group means."""
+        return stats_to_metrics(self.stats_dict(), check=check)
+
+
+def stats_to_metrics(s: Dict[str, float], check: bool = True) -> Dict[str, float]:
+    if check:
+        if s["invalid"] > 0:
+            raise AlgorithmError(f"{int(s['invalid'])} invalid rows/groups in the batch "
+                                 "(target outside the vocabulary or bad group shape)")
+        if s["nonfinite"] > 0:
+            raise AlgorithmError(f"loss must be finite, got {s['loss']} "
+                                 f"({int(s['nonfinite'])} non-finite rows)")
+    ng = max(s["n_groups"], 1.0)
+    ntok = max(s["n_tok_rl"], 1.0)
+    out = dict(s)
+    out.update({
+        "mean_reward": s["sum_mean_reward"] / ng,
+        "baseline": s["sum_baseline"] / ng,
+        "kl_estimate": s["sum_kl_estimate"] / ng,
+        "group_size": s["sum_group_size"] / ng,
+        "clipfrac": s["clip_count"] / ntok,
+        "entropy": s["sum_entropy"] / ntok,
+        "token_kl": s["sum_kl"] / ntok,
+        "ppo_kl": s["sum_ppo_kl"] / ntok,
+        "mean_ratio": s["sum_ratio"] / ntok,
+    })
+    return out
+
+
+class _Workspace:
+    def __init__(self):
+        self.buf: Dict[int, torch.Tensor] = {}
+
+    def get(self, dev: torch.device, nbytes: int) -> torch.Tensor:
+        key = dev.index if dev.index is not None else torch.cuda.current_device()
+        t = self.buf.get(key)
+        if t is None or t.numel() < nbytes:
+            t = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
+            self.buf[key] = t
+        return t
+
+
+class RFTLoss:
+    """Fused RFT loss (advantage -> logprob -> loss -> dlogits) on B200.
+
+    ``dlogits``: "inplace" (overwrite logits with d loss / d logits), None
+    (forward-only loss), "new" (allocate), or a preallocated tensor of the
+    logits' dtype with rows of the same length.
+    """
+
+    def __init__(self, cfg: Optional[RFTLossConfig] = None, **kw):
+        self.cfg = cfg if cfg is not None else RFTLossConfig(**kw)
+        self._ws = _Workspace()
+
+    def route(self, batch: PackedBatch) -> int:
+        """1 = fused single pass, 2 = forward+backward streaming, 3 = sequence-coupled."""
+        return N.lib().tg_route(ctypes.byref(c_batch(batch)), ctypes.byref(self.cfg.to_c()))
+
+    def __call__(self, batch: PackedBatch, dlogits: Union[str, torch.Tensor, None] = "new", *,
+                 n_tok_global: int = 0, n_seq_global: int = 0, n_sft_seq_global: int = 0,
+                 out: Optional[LossOutput] = None, stream: Optional[torch.cuda.Stream] = None
+                 ) -> LossOutput:
+        L = N.lib()
+        cb = c_batch(batch)
+        cfg = self.cfg
+        if cfg.coupled and cfg.policy_loss_fn == "dpo" and n_seq_global == 0:
+            n_seq_global = batch.n_seqs
+        cc = cfg.to_c(n_tok_global, n_seq_global, n_sft_seq_global)
+        dev = batch.device
+        T, B = batch.n_rows, batch.n_seqs
+        if out is None:
+            f32 = dict(dtype=torch.float32, device=dev)
+            out = LossOutput(stats=torch.empty(N.NSTAT, dtype=torch.float64, device=dev),
+                             lp=torch.empty(T, **f32), entropy=torch.empty(T, **f32),
+                             lse=torch.empty(T, **f32), seq_lp=torch.empty(B, **f32),
+                             seq_adv=torch.empty(B, **f32))
+        if isinstance(dlogits, str):
+            if dlogits == "inplace":
+                if batch.row_index is not None:
+                    raise ValueError("in-place dlogits needs logits rows == trainable rows")
+                dz = batch.logits
+            elif dlogits == "new":
+                dz = torch.empty((T, batch.vocab), dtype=batch.logits.dtype, device=dev)
+            else:
+                raise ValueError(f"dlogits must be 'inplace', 'new', None or a tensor")
+        else:
+            dz = dlogits
+        co = N.TgOut()
+        if dz is not None:
+            if dz.dtype != batch.logits.dtype or dz.device != dev or dz.stride(1) != 1:
+                raise ValueError("dlogits must match logits' dtype / device with contiguous rows")
+            if dz.shape[0] < T or dz.shape[1] < batch.vocab:
+                raise ValueError("dlogits too small")
+            co.dlogits, co.ld_out = dz.data_ptr(), dz.stride(0)
+        co.lp, co.entropy, co.lse = out.lp.data_ptr(), out.entropy.data_ptr(), out.lse.data_ptr()
+        co.seq_lp, co.seq_adv, co.stats = (out.seq_lp.data_ptr(), out.seq_adv.data_ptr(),
+                                           out.stats.data_ptr())
+        nbytes = L.tg_workspace_size(ctypes.byref(cb), ctypes.byref(cc))
+        ws = self._ws.get(dev, nbytes)
+        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        with torch.cuda.device(dev):
+            N.check(L.tg_loss_fwd_bwd(ctypes.byref(cb), ctypes.byref(cc), ctypes.byref(co),
+                                      ws.data_ptr(), ws.numel(), s.cuda_stream))
+        out.dlogits = dz
+        return out
+
+
+def logprob_fwd(batch: PackedBatch, stream: Optional[torch.cuda.Stream] = None):
+    """Forward-only per-row logprob / entropy / lse and per-sequence LP
+    (experience_logprob, algorithms.py:81-85): 2V bytes per row."""
+    L = N.lib()
+    cb = c_batch(batch)
+    dev = batch.device
+    f32 = dict(dtype=torch.float32, device=dev)
+    lp, ent, lse = (torch.empty(batch.n_rows, **f32) for _ in range(3))
+    seq_lp = torch.empty(batch.n_seqs, **f32)
+    co = N.TgOut()
+    co.lp, co.entropy, co.lse, co.seq_lp = (lp.data_ptr(), ent.data_ptr(), lse.data_ptr(),
+                                            seq_lp.data_ptr())
+    nbytes = L.tg_workspace_size(ctypes.byref(cb), None)
+    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    with torch.cuda.device(dev):
+        N.check(L.tg_logprob_fwd(ctypes.byref(cb), ctypes.byref(co), ws.data_ptr(), ws.numel(),
+                                 s.cuda_stream))
+    return lp, ent, lse, seq_lp

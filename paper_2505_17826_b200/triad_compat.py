@@ -1,0 +1,312 @@
+"""Reference-shaped drop-in: ``group_loss`` / ``loss_sft`` / ``loss_dpo`` /
+``combine_reports`` / ``Trainer`` with the reference's signatures and error
+behaviour, computed by the CUDA path.
+
+The reference (``triad``) scores tokens with a bucketed logits *table*
+(policy.py:59-94): each mask-true token t reads row
+``state_t = FNV1a(context, t, prev) mod S`` (policy.py:152-191).  Here the
+states come from the C host helper ``tg_scored_states`` and the table is
+read in place by the kernels through ``row_index`` (no gather copy); the
+per-token gradient rows are scatter-added back by state into a dense table
+gradient, which is what ``SparseGrad.to_dense`` holds in the reference
+(policy.py:215-250).
+
+Objects are duck-typed: ``params`` needs ``logits`` [S, V], ``num_buckets``,
+``vocab.size`` (and ``version`` for the Trainer); groups / experiences as in
+records.py.  Arithmetic is fp32 on the device (tables are uploaded as f32),
+so results match the reference's float64 to ~1e-6 relative, not bit-exactly.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from .config import AlgorithmError, RFTLossConfig, Variant
+from .loss import RFTLoss, logprob_fwd, stats_to_metrics
+from .packing import HostGroups, PolicyError, flatten_groups, pack_arrays, scored_states
+
+
+@dataclass
+class AlgorithmConfig:
+    """algorithms.py:36-56, same validation."""
+
+    variant: Variant = Variant.OPMD_SIMPLE
+    tau: float = 1.0
+    beta: float = 0.0
+    dpo_beta: float = 0.1
+    learning_rate: float = 0.1
+
+    def __post_init__(self) -> None:
+        if isinstance(self.variant, str):
+            self.variant = Variant(self.variant)
+        if self.tau < 0:
+            raise AlgorithmError(f"tau must be >= 0, got {self.tau}")
+        if self.variant in (Variant.OPMD_KIMI, Variant.OPMD_PAIRWISE) and self.tau <= 0:
+            raise AlgorithmError(f"{self.variant.value} requires tau > 0")
+        if self.beta < 0:
+            raise AlgorithmError(f"beta must be >= 0, got {self.beta}")
+        if self.dpo_beta <= 0:
+            raise AlgorithmError(f"dpo_beta must be > 0, got {self.dpo_beta}")
+        if self.learning_rate <= 0:
+            raise AlgorithmError(f"learning_rate must be > 0, got {self.learning_rate}")
+
+
+class SparseGrad:
+    """policy.py:215-250: touched rows only (float64 numpy rows)."""
+
+    def __init__(self) -> None:
+        self.rows: Dict[int, np.ndarray] = {}
+
+    def add_row(self, state: int, vec: np.ndarray) -> None:
+        if state in self.rows:
+            self.rows[state] = self.rows[state] + vec
+        else:
+            self.rows[state] = np.array(vec, dtype=np.float64)
+
+    def axpy(self, coef: float, other: "SparseGrad") -> None:
+        for state, vec in other.rows.items():
+            self.add_row(state, coef * vec)
+
+    def scaled(self, coef: float) -> "SparseGrad":
+        out = SparseGrad()
+        for state, vec in self.rows.items():
+            out.rows[state] = coef * vec
+        return out
+
+    def to_dense(self, shape: Tuple[int, int]) -> np.ndarray:
+        dense = np.zeros(shape)
+        for state, vec in self.rows.items():
+            dense[state] += vec
+        return dense
+
+    def is_finite(self) -> bool:
+        return all(np.all(np.isfinite(v)) for v in self.rows.values())
+
+    def max_abs(self) -> float:
+        return max((float(np.max(np.abs(v))) for v in self.rows.values()), default=0.0)
+
+
+@dataclass
+class LossReport:
+    """algorithms.py:59-69."""
+
+    loss: float
+    gradient: SparseGrad
+    metrics: Dict[str, float] = field(default_factory=dict)
+
+    def __post_init__(self) -> None:
+        if not math.isfinite(self.loss):
+            raise AlgorithmError(f"loss must be finite, got {self.loss}")
+        if not self.gradient.is_finite():
+            raise AlgorithmError("gradient must be finite")
+
+
+def _device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("the RFT loss runs only on CUDA devices (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _table(params, dev) -> torch.Tensor:
+    return torch.as_tensor(np.asarray(params.logits, dtype=np.float32), device=dev).contiguous()
+
+
+def _check_vocab(h: HostGroups, target: np.ndarray, V: int) -> None:
+    """policy._check_generated_tokens (policy.py:175-178)."""
+    if target.size and (target.min() < 0 or target.max() >= V):
+        bad = int(target[(target < 0) | (target >= V)][0])
+        raise PolicyError(f"token {bad} outside vocabulary of size {V}")
+
+
+def _seq_logprob(table: torch.Tensor, states: np.ndarray, target: np.ndarray,
+                 seq_lengths: np.ndarray) -> np.ndarray:
+    """experience_logprob for every sequence under a table (algorithms.py:81-85)."""
+    dev = table.device
+    b = pack_arrays(table, target, seq_lengths, [len(seq_lengths)], np.zeros(len(seq_lengths)),
+                    row_index=states)
+    _, _, _, seq_lp = logprob_fwd(b)
+    return seq_lp.double().cpu().numpy()
+
+
+def _scatter(dz: torch.Tensor, states: np.ndarray, S: int) -> SparseGrad:
+    dev = dz.device
+    idx = torch.as_tensor(states, device=dev)
+    dense = torch.zeros((S, dz.shape[1]), dtype=torch.float64, device=dev)
+    dense.index_add_(0, idx, dz.double())
+    host = dense.cpu().numpy()
+    g = SparseGrad()
+    for s in sorted(set(int(x) for x in states)):
+        g.rows[s] = host[s].copy()
+    return g
+
+
+def _run(groups, params, cfg: RFTLossConfig, *, anchor=None, seq_ref_override=None,
+         seq_kind=None, metrics_override=None) -> LossReport:
+    dev = _device()
+    h = flatten_groups(groups)
+    S, V = int(params.num_buckets), int(params.vocab.size)
+    states, target = scored_states(h, S)
+    _check_vocab(h, target, V)
+    table = _table(params, dev)
+    seq_ref = h.seq_ref_lp if seq_ref_override is None else seq_ref_override
+    anchor_rows = None
+    if anchor is not None:
+        if tuple(np.shape(anchor.logits)) != tuple(np.shape(params.logits)):
+            raise AlgorithmError(f"parameter shapes differ: {np.shape(params.logits)} vs "
+                                 f"{np.shape(anchor.logits)}")
+        anchor_rows = _table(anchor, dev)[torch.as_tensor(states, device=dev)].contiguous()
+    batch = pack_arrays(table, target, h.seq_lengths, h.group_sizes, h.reward, old_lp=h.old_lp,
+                        seq_ref_lp=seq_ref, seq_kind=seq_kind, anchor_logits=anchor_rows,
+                        row_index=states)
+    out = RFTLoss(cfg)(batch, dlogits="new")
+    st = out.stats_dict()
+    if st["invalid"] > 0:
+        raise AlgorithmError("invalid group shape for this loss")
+    grad = _scatter(out.dlogits, states, S)
+    m = stats_to_metrics(st, check=False)
+    metrics = {k: m[k] for k in ("mean_reward", "baseline", "kl_estimate", "group_size")}
+    if metrics_override:
+        metrics.update(metrics_override(st))
+    return LossReport(loss=float(st["loss"]), gradient=grad, metrics=metrics)
+
+
+def group_losses(groups: Sequence, params, config: AlgorithmConfig,
+                 sft_params=None, ref_params=None) -> LossReport:
+    """``combine_reports([group_loss(g, ...) for g in groups])`` in one kernel
+    pipeline (orchestrator.py:299-304)."""
+    if config.variant not in (Variant.OPMD_KIMI, Variant.OPMD_PAIRWISE, Variant.OPMD_SIMPLE):
+        raise AlgorithmError(f"{config.variant.value} is not a group-based loss")
+    if not groups:
+        raise AlgorithmError("cannot combine an empty report list")
+    cfg = RFTLossConfig.from_variant(config.variant, config.tau, config.beta, config.dpo_beta)
+    anchor = None
+    if config.variant == Variant.OPMD_SIMPLE:
+        if config.beta > 0 and sft_params is None:
+            raise AlgorithmError("beta > 0 requires sft_params")
+        anchor = sft_params if config.beta > 0 else None
+    if config.variant == Variant.OPMD_PAIRWISE and any(len(g.experiences) < 2 for g in groups):
+        raise AlgorithmError("pairwise loss needs a group of at least 2 rollouts")
+    seq_ref = None
+    if config.variant == Variant.OPMD_KIMI and ref_params is not None:
+        h = flatten_groups(groups)
+        st, tg = scored_states(h, int(ref_params.num_buckets))
+        seq_ref = _seq_logprob(_table(ref_params, _device()), st, tg, h.seq_lengths)
+    return _run(groups, params, cfg, anchor=anchor, seq_ref_override=seq_ref)
+
+
+def group_loss(group, params, config: AlgorithmConfig, sft_params=None,
+               ref_params=None) -> LossReport:
+    """algorithms.py:351-365."""
+    return group_losses([group], params, config, sft_params=sft_params, ref_params=ref_params)
+
+
+class _OneGroup:
+    def __init__(self, exps, ref=None):
+        self.experiences = list(exps)
+        self.ref_logprobs = ref
+
+
+def loss_sft(batch: Sequence, params) -> LossReport:
+    """algorithms.py:256-274: mean over sequences of -sum_t lp."""
+    if not batch:
+        raise AlgorithmError("SFT batch must be nonempty")
+    cfg = RFTLossConfig.from_variant(Variant.SFT)
+    n = len(batch)
+    rewards = [e.reward for e in batch if e.reward is not None]
+
+    def metrics(st):
+        return {"mean_reward": float(np.mean(rewards)) if rewards else 0.0, "baseline": 0.0,
+                "kl_estimate": 0.0, "group_size": float(n)}
+
+    exps = [e if e.reward is not None else _with_reward(e) for e in batch]
+    return _run([_OneGroup(exps)], params, cfg, metrics_override=metrics)
+
+
+def _with_reward(e):
+    class _E:
+        pass
+    x = _E()
+    x.tokens, x.prompt_length, x.action_mask, x.logprobs = (e.tokens, e.prompt_length,
+                                                            e.action_mask, e.logprobs)
+    x.reward = 0.0
+    return x
+
+
+def loss_dpo(pairs: Sequence[Tuple], params, ref, dpo_beta: float) -> LossReport:
+    """algorithms.py:277-315."""
+    if not pairs:
+        raise AlgorithmError("DPO batch must be nonempty")
+    if dpo_beta <= 0:
+        raise AlgorithmError(f"dpo_beta must be > 0, got {dpo_beta}")
+    for c, r in pairs:
+        if list(c.tokens[: c.prompt_length]) != list(r.tokens[: r.prompt_length]):
+            raise AlgorithmError("chosen and rejected must share a prompt")
+    groups = [_OneGroup([c if c.reward is not None else _with_reward(c),
+                         r if r.reward is not None else _with_reward(r)]) for c, r in pairs]
+    h = flatten_groups(groups)
+    st, tg = scored_states(h, int(ref.num_buckets))
+    seq_ref = _seq_logprob(_table(ref, _device()), st, tg, h.seq_lengths)
+    cfg = RFTLossConfig.from_variant(Variant.DPO, dpo_beta=dpo_beta)
+    n = len(pairs)
+
+    def metrics(s):
+        return {"mean_reward": s["sum_dpo_margin"] / n, "baseline": 0.0, "kl_estimate": 0.0,
+                "group_size": float(n)}
+
+    return _run(groups, params, cfg, seq_ref_override=seq_ref, metrics_override=metrics)
+
+
+def combine_reports(reports: Sequence[LossReport]) -> LossReport:
+    """algorithms.py:368-379."""
+    if not reports:
+        raise AlgorithmError("cannot combine an empty report list")
+    grad = SparseGrad()
+    loss = 0.0
+    for rep in reports:
+        loss += rep.loss
+        grad.axpy(1.0, rep.gradient)
+    keys = reports[0].metrics.keys()
+    metrics = {k: float(np.mean([r.metrics[k] for r in reports])) for k in keys}
+    return LossReport(loss=loss, gradient=grad, metrics=metrics)
+
+
+def apply_update(params, gradient: SparseGrad, learning_rate: float):
+    """algorithms.py:329-348: SGD step, new table, version + 1."""
+    if not gradient.is_finite():
+        raise AlgorithmError("refusing to apply a non-finite gradient")
+    logits = np.array(params.logits)
+    for state, vec in gradient.rows.items():
+        if not 0 <= state < params.num_buckets:
+            raise AlgorithmError(f"gradient row {state} outside the logits table")
+        logits[state] -= learning_rate * vec
+    return type(params)(logits=logits, version=params.version + 1, vocab=params.vocab,
+                        num_buckets=params.num_buckets)
+
+
+class Trainer:
+    """orchestrator.Trainer (orchestrator.py:288-322) on the CUDA loss path."""
+
+    def __init__(self, params, algo: AlgorithmConfig) -> None:
+        self.params = params
+        self.algo = algo
+        self.anchor = params
+
+    def step_groups(self, groups) -> LossReport:
+        combined = group_losses(groups, self.params, self.algo, sft_params=self.anchor)
+        self.params = apply_update(self.params, combined.gradient, self.algo.learning_rate)
+        return combined
+
+    def step_sft(self, batch) -> LossReport:
+        report = loss_sft(batch, self.params)
+        self.params = apply_update(self.params, report.gradient, self.algo.learning_rate)
+        return report
+
+    def step_dpo(self, pairs) -> LossReport:
+        report = loss_dpo(pairs, self.params, self.anchor, self.algo.dpo_beta)
+        self.params = apply_update(self.params, report.gradient, self.algo.learning_rate)
+        return report

@@ -1,0 +1,143 @@
+"""CPU-side checks of the C ABI library: it loads, exports every symbol the
+header declares, its structs match ctypes, host helpers reproduce the
+reference's integer work bit-exactly, and argument validation mirrors the
+reference's errors (no device work is launched by any of these)."""
+
+import ctypes
+import re
+import subprocess
+import tempfile
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from _golden import groups_of, load
+from paper_2505_17826_b200 import _native as N
+from paper_2505_17826_b200 import AlgorithmError, RFTLossConfig
+from paper_2505_17826_b200.packing import flatten_groups, group_by_task, scored_states
+from paper_2505_17826_b200.registry import (ADVANTAGE_FNS, ENTROPY_LOSS_FNS, KL_FNS,
+                                            LOSS_AGG_MODES, POLICY_LOSS_FNS)
+from oracle import rft_oracle as O
+
+ROOT = Path(__file__).resolve().parents[1]
+HEADER = ROOT / "include" / "tg_loss.h"
+
+
+def header_functions():
+    src = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\*?\s+\*?(tg_[a-z_]+)\(", src, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    L = N.lib()
+    names = header_functions()
+    assert set(names) == set(N.EXPORTED), names
+    for n in names:
+        assert hasattr(L, n), n
+    nm = subprocess.run(["nm", "-D", "--defined-only", str(N.lib_path())], capture_output=True,
+                        text=True).stdout
+    for n in names:
+        assert re.search(rf"\bT {n}\b", nm), n
+
+
+def test_struct_layout_matches_header():
+    prog = r'''
+#include <stdio.h>
+#include <stddef.h>
+#include "tg_loss.h"
+int main(void) {
+  printf("%zu %zu %zu %zu %zu %zu\n", sizeof(TgConfig), sizeof(TgBatch), sizeof(TgOut),
+         offsetof(TgBatch, seq_kind), offsetof(TgConfig, n_sft_seq_global), offsetof(TgOut, stats));
+  printf("%d %d %d\n", TG_NSTAT, TG_S_INVALID, TG_S_SUM_ANCHOR_KL);
+  return 0;
+}'''
+    with tempfile.TemporaryDirectory() as d:
+        c = Path(d) / "p.c"
+        c.write_text(prog)
+        exe = Path(d) / "p"
+        subprocess.run(["gcc", "-I", str(ROOT / "include"), str(c), "-o", str(exe)], check=True)
+        out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()
+    sizes = list(map(int, out))
+    assert sizes[0] == ctypes.sizeof(N.TgConfig)
+    assert sizes[1] == ctypes.sizeof(N.TgBatch)
+    assert sizes[2] == ctypes.sizeof(N.TgOut)
+    assert sizes[3] == N.TgBatch.seq_kind.offset
+    assert sizes[4] == N.TgConfig.n_sft_seq_global.offset
+    assert sizes[5] == N.TgOut.stats.offset
+    assert sizes[6] == N.NSTAT == O.NSTAT
+    assert sizes[7] == N.STAT["invalid"] == O.STAT["invalid"]
+    assert sizes[8] == N.STAT["sum_anchor_kl"]
+    assert N.STAT_NAMES == O.STAT_NAMES
+
+
+@pytest.mark.parametrize("name", ["simple_tau05", "kimi", "pairwise", "simple_bf16_v512",
+                                  "simple_v4_uniform", "sft", "dpo", "regularizer_g"])
+def test_scored_states_match_reference(name):
+    fx = load(name)
+    h = flatten_groups(groups_of(fx))
+    states, target = scored_states(h, fx["theta"].shape[0])
+    assert np.array_equal(states, fx["states"])   # FNV bucket indexing: bit-exact
+    assert np.array_equal(target, fx["target"])
+
+
+@pytest.mark.parametrize("name", ["buffer_fifo", "buffer_priority"])
+def test_group_by_task_matches_reference_buffer(name):
+    fx = load(name)
+    ready = fx["ready"].astype(bool)
+    groups = group_by_task(fx["tasks"], ready, int(fx["group_size"]), int(fx["n_take"]),
+                           policy=str(fx["policy"]), priority=fx["priority"],
+                           id_rank=np.arange(len(ready)))
+    assert np.array_equal(np.array(groups, np.int64).reshape(-1, int(fx["group_size"])),
+                          fx["groups"])
+
+
+def _dummy_batch():
+    b = N.TgBatch()
+    b.dtype, b.n_seqs, b.n_groups = N.TG_DTYPE_BF16, 2, 1
+    b.n_rows, b.vocab, b.ld = 4, 32, 32
+    b.logits = b.target = b.seq_offsets = b.group_offsets = b.reward = 0x1000
+    o = N.TgOut()
+    o.stats = 0x2000
+    return b, o
+
+
+@pytest.mark.parametrize("mut,code", [
+    (lambda b, c: setattr(c, "tau", -1.0), N.TG_EINVAL),
+    (lambda b, c: (setattr(c, "policy_loss_fn", N.TG_PG_OPMD_KIMI), setattr(c, "tau", 0.0)),
+     N.TG_EINVAL),
+    (lambda b, c: setattr(c, "anchor_beta", 0.5), N.TG_EINVAL),      # beta > 0 needs anchor
+    (lambda b, c: setattr(c, "dpo_beta", 0.0), N.TG_EINVAL),
+    (lambda b, c: setattr(c, "kl_fn", 9), N.TG_EINVAL),
+    (lambda b, c: setattr(b, "ld", 16), N.TG_EINVAL),                 # ld < vocab
+    (lambda b, c: setattr(b, "dtype", 7), N.TG_EINVAL),
+    (lambda b, c: setattr(c, "clip_c", 0.5), N.TG_EINVAL),
+    (lambda b, c: None, N.TG_EWORKSPACE),                             # workspace too small
+])
+def test_validation_mirrors_reference_errors(mut, code):
+    L = N.lib()
+    b, o = _dummy_batch()
+    c = RFTLossConfig(advantage_fn="grpo", policy_loss_fn="ppo_clip").to_c()
+    mut(b, c)
+    rc = L.tg_loss_fwd_bwd(ctypes.byref(b), ctypes.byref(c), ctypes.byref(o), 0x3000, 16, None)
+    assert rc == code, L.tg_last_error()
+    assert L.tg_last_error().decode()
+
+
+def test_config_validation_and_registry():
+    for tbl in (ADVANTAGE_FNS, POLICY_LOSS_FNS, KL_FNS, ENTROPY_LOSS_FNS, LOSS_AGG_MODES):
+        assert tbl and all(c.doc for c in tbl.values())
+    assert RFTLossConfig(kl_fn="low_var_kl").kl_fn == "k3"
+    with pytest.raises(AlgorithmError):
+        RFTLossConfig(tau=-1)
+    with pytest.raises(AlgorithmError):
+        RFTLossConfig(policy_loss_fn="opmd_kimi", tau=0.0)
+    with pytest.raises(AlgorithmError):
+        RFTLossConfig(dpo_beta=0.0)
+    with pytest.raises(KeyError):
+        RFTLossConfig(advantage_fn="nope")
+    c = RFTLossConfig.from_variant("OPMD_SIMPLE", tau=0.5, beta=0.2)
+    assert (c.advantage_fn, c.policy_loss_fn, c.loss_agg_mode, c.anchor_beta) == \
+        ("opmd", "vanilla", "seq-sum", 0.2)
+    assert RFTLossConfig.from_variant("SFT").loss_agg_mode == "seq-mean-token-sum"
+    assert RFTLossConfig.from_variant("DPO").coupled

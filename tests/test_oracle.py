@@ -312,3 +312,21 @@ def test_dual_clip_counts_and_zero_gradient():
     st = O.stats_dict(out["stats"])
     assert st["clip_count"] + st["dual_clip_count"] > 0
     _fd_check(b, cfg)
+
+
+@pytest.mark.parametrize("cfg", [
+    O.Config(advantage_fn="grpo", policy_loss_fn="ppo_clip", kl_fn="k3", kl_coef=0.1,
+             entropy_loss_fn="default", entropy_coef=0.05, loss_agg_mode="token-mean"),
+    O.Config(advantage_fn="opmd", policy_loss_fn="vanilla", loss_agg_mode="seq-sum", tau=0.5),
+    O.Config(advantage_fn="rloo", policy_loss_fn="sft", loss_agg_mode="seq-mean-token-mean",
+             clip_c=3.0),
+])
+def test_blocked_single_pass_matches_general(cfg):
+    b = _small_batch(7, V=50)
+    b.seq_kind = np.array([0, 0, 0, 1])
+    ref = O.general_loss(b, cfg)
+    dz = np.zeros_like(b.logits)
+    out = O.single_pass_blocked(b, cfg, dz_out=dz, block=3)
+    assert out["loss"] == pytest.approx(ref["stats"][O.STAT["loss"]], rel=1e-12, abs=1e-14)
+    assert np.max(np.abs(dz - ref["dz"])) <= 1e-14
+    assert np.max(np.abs(out["lp"] - ref["lp"])) <= 1e-14
