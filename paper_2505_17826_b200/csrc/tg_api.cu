@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <atomic>
@@ -27,6 +28,7 @@
 namespace tg {
 size_t fused_smem_bytes(int n_slots);
 cudaError_t launch_fused(const KParams& P, const void* meta, int cl, int n_slots, int n_ctas,
+                         int prefetch_rows,
                          cudaStream_t stream);
 int fused_chunk_bytes();
 int fused_max_slots();
@@ -183,8 +185,9 @@ int validate_cfg(const TgBatch* b, const TgConfig* c) {
   if (!(c->sft_weight >= 0)) return fail(TG_EINVAL, "sft_weight must be >= 0");
   if (c->loss_agg_mode == TG_AGG_SEQ_MEAN_TOKEN_SUM_NORM && !(c->agg_norm > 0))
     return fail(TG_EINVAL, "agg_norm must be > 0");
-  if (c->advantage_fn == TG_ADV_GIVEN && !coupled_pg(c->policy_loss_fn) && b->n_seqs > 0 &&
-      !b->advantage)
+  if (c->advantage_fn == TG_ADV_GIVEN &&
+      (c->policy_loss_fn == TG_PG_VANILLA || c->policy_loss_fn == TG_PG_PPO_CLIP) &&
+      b->n_seqs > 0 && !b->advantage)
     return fail(TG_EINVAL, "advantage_fn GIVEN requires batch.advantage");
   return TG_OK;
 }
@@ -259,11 +262,21 @@ void fill_params(KParams& P, const TgBatch* b, const TgConfig* c, const TgOut* o
 
 // Fused-kernel plan: cluster size and ring slots, or cl = 0 if not eligible.
 struct FusedPlan {
-  int cl = 0, n_slots = 0, n_ctas = 0;
+  int cl = 0, n_slots = 0, n_ctas = 0, prefetch_rows = 1;
 };
+
+// Tuning overrides for measurement (A/B on the GPU without rebuilding):
+// TG_FUSED_CL=1|2|4 forces the cluster size, TG_PREFETCH_ROWS=n the L2
+// look-ahead depth (rows per cluster; 0 disables).
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
 
 FusedPlan fused_plan(const TgBatch* b, const TgOut* o) {
   FusedPlan fp;
+  fp.prefetch_rows = env_int("TG_PREFETCH_ROWS", 1);
+  const int force_cl = env_int("TG_FUSED_CL", 0);
   const int esz = esz_of(b->dtype);
   const int epv = 16 / esz;
   if (!o || !o->dlogits) return fp;
@@ -277,6 +290,7 @@ FusedPlan fused_plan(const TgBatch* b, const TgOut* o) {
   int n_slots = int((size_t(d.smem_optin) - tail) / size_t(fused_chunk_bytes()));
   if (n_slots > fused_max_slots()) n_slots = fused_max_slots();
   for (int cl = 1; cl <= 4; cl *= 2) {
+    if (force_cl && cl != force_cl) continue;
     const int64_t slice_vec = (nvec + cl - 1) / cl;
     const int64_t nchunk = (slice_vec * 16 + fused_chunk_bytes() - 1) / fused_chunk_bytes();
     if (nchunk + 2 <= n_slots) {
@@ -377,7 +391,7 @@ int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspa
     if (fp.n_ctas > kMaxPartials) return fail(TG_EUNSUPPORTED, "too many CTAs");
     if (b->n_rows > 0) {
       if (ev_begin) cudaEventRecord(ev_begin, st);
-      cudaError_t e = launch_fused(P, meta, fp.cl, fp.n_slots, fp.n_ctas, st);
+      cudaError_t e = launch_fused(P, meta, fp.cl, fp.n_slots, fp.n_ctas, fp.prefetch_rows, st);
       if (ev_end) cudaEventRecord(ev_end, st);
       if (e != cudaSuccess) return fail(TG_ECUDA, "fused kernel launch: %s", cudaGetErrorString(e));
       count_launches(1);

@@ -46,7 +46,7 @@ def c_batch(b: PackedBatch) -> N.TgBatch:
         raise ValueError("logits must be 2-D [rows, ld] (flatten [B, L, V] first)")
     if lg.dtype not in _DTYPES:
         raise ValueError(f"logits dtype {lg.dtype} unsupported (bf16 or f32)")
-    if lg.stride(1) != 1:
+    if lg.numel() and lg.stride(1) != 1:
         raise ValueError("logits rows must be contiguous (stride(1) == 1)")
     dev = lg.device
     if dev.type != "cuda":
@@ -62,7 +62,8 @@ def c_batch(b: PackedBatch) -> N.TgBatch:
     c = N.TgBatch()
     c.dtype = _DTYPES[lg.dtype]
     c.n_seqs, c.n_groups = b.n_seqs, b.n_groups
-    c.n_rows, c.vocab, c.ld = b.n_rows, b.vocab, lg.stride(0)
+    c.n_rows, c.vocab = b.n_rows, b.vocab
+    c.ld = lg.stride(0) if lg.numel() else max(b.vocab, 1)
     c.logits = lg.data_ptr()
     c.row_index = _ptr(b.row_index)
     if b.anchor_logits is not None:
