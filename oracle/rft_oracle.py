@@ -428,7 +428,8 @@ def advantages(batch: Batch, cfg: Config) -> np.ndarray:
         elif fn == "reinforce":
             a = r.copy()
         elif fn == "given":
-            a = np.array([float(batch.advantage[i]) for i in seqs])
+            a = (np.zeros(k) if batch.advantage is None
+                 else np.array([float(batch.advantage[i]) for i in seqs]))
         else:
             raise ValueError(f"unknown advantage_fn {fn}")
         A[seqs] = a

@@ -7,24 +7,27 @@
 // write of d loss / d logits (4V bytes per row, the HBM roofline minimum).
 //
 // Design (B200-first):
-//  * A thread-block cluster of CL CTAs (CL = 1 for V <= ~100k bf16, 2 for
+//  * A thread-block cluster of CL CTAs (CL = 1 for V <= ~110k bf16, 2 for
 //    Qwen's 151,936) owns one row at a time; CTA rank r owns a contiguous
 //    column slice of the row.  The slice never leaves the SM: a producer warp
 //    streams it into a shared-memory ring with 1-D bulk TMA
-//    (cp.async.bulk ... mbarrier::complete_tx), one chunk per ring slot with
-//    a full / empty mbarrier pair, and keeps HBM busy across row boundaries
-//    by prefetching upcoming rows' slices into L2 (cp.async.bulk.prefetch.L2)
-//    -- the ring holds ~1.5 slices, L2 holds the look-ahead.
-//  * 15 consumer warps (one 16-byte vector per thread per chunk) run phase 1
-//    on each chunk as it lands: online max / sum-exp / sum p*z and the target
-//    logit; -inf logits are clamped to -1e30 with packed bf16x2 max so no
-//    per-element guard is needed.  One named barrier reduces across warps;
-//    DSMEM (st.async into each peer's exchange slot, completing tx bytes on
-//    the peer's mbarrier) reduces across the cluster.  Every CTA merges the
-//    CL partials in rank order, so all CTAs get bit-identical lse / H.
-//  * The per-row epilogue (tg_rowcoef.cuh) turns (lp, H) into (s, h); phase 2
-//    re-reads the chunks from SMEM, writes dz = p (s + h((z - lse) + H)) - s[v=y]
-//    with 128-bit streaming stores and releases each slot to the producer.
+//    (cp.async.bulk ... mbarrier::complete_tx), one 7.5 KB chunk per ring
+//    slot with a full / empty mbarrier pair, and keeps HBM busy across row
+//    boundaries by prefetching upcoming rows' slices into L2
+//    (cp.async.bulk.prefetch.L2) -- the ring holds ~1.5 slices.
+//  * 15 consumer warps, one 16-byte vector per thread per chunk, consume
+//    kGroup chunks per step.  Phase 1 (as chunks land): online max / sum-exp /
+//    sum p*z and the target logit in packed fp32x2 arithmetic (FFMA2 / FADD2)
+//    with MUFU ex2; -inf logits are clamped to -1e30 with packed bf16x2 max;
+//    the running max is updated lazily behind a warp vote.  One named barrier
+//    collects per-warp partials; warp 0 reduces them, exchanges the CTA
+//    partial with its cluster peers through DSMEM (st.async completing tx
+//    bytes on the peer's mbarrier; rank-order merge => bit-identical lse on
+//    every CTA), evaluates the registry epilogue (tg_rowcoef.cuh) and
+//    broadcasts (a, h, lse) through a second named barrier.
+//  * Phase 2 re-reads the resident chunks from SMEM and writes
+//    dz = p (s + h((z - lse) + H)) - s[v = y] with 128-bit streaming stores,
+//    releasing each slot to the producer, which refills it with the next row.
 //  * Persistent grid: one CTA per SM (16 warps -> 128 registers / thread),
 //    clusters stride over rows.
 #include "tg_common.cuh"
@@ -34,11 +37,12 @@ namespace tg {
 
 // 15 consumer warps + 1 producer warp = 16 warps: with the 4-warp register
 // allocation granularity this leaves 128 registers per thread (17 warps would
-// cap it at 96 and spill).  One 16-byte vector per consumer thread per chunk.
+// cap it at 96 and spill).
 constexpr int kConsumerWarps = 15;
 constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kFusedThreads = kConsumers + 32;
-constexpr int kChunk = kConsumers * 16;  // 7680 bytes per TMA bulk copy / ring slot
+constexpr int kChunk = kConsumers * 16;  // 7680 bytes: one 16-byte vector per consumer thread
+constexpr int kGroup = 4;                // chunks consumed per step
 constexpr int kMaxSlots = 30;
 constexpr uint32_t kPrefetchPiece = 65536;  // bytes per L2 prefetch instruction
 
@@ -48,8 +52,29 @@ struct FusedSmemTail {
   uint64_t xbar[2];
   float4 xdata[2][4];
   float4 wpart[2][kConsumerWarps];
+  float4 bcast[2];  // (a, h, lse, s) of the current row, from warp 0
   double stats[16];
 };
+
+// ---- shared-memory / barrier primitives on 32-bit shared addresses ----------
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(addr)
+               : "memory");
+  return r;
+}
+
+__device__ __forceinline__ void wait_full(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+__device__ __forceinline__ void arrive_u32(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
 
 // ---- packed-element helpers (bf16: 8 per vector, fp32: 4 per vector) --------
 
@@ -74,10 +99,13 @@ struct Pk<bf16_t> {
     u.z = bmax2(u.z, kBf16NegBig2);
     u.w = bmax2(u.w, kBf16NegBig2);
   }
-  __device__ __forceinline__ static float vmax(const uint4& u) {
-    const uint32_t m = bmax2(bmax2(u.x, u.y), bmax2(u.z, u.w));
+  __device__ __forceinline__ static uint32_t pmax(const uint4& u) {
+    return bmax2(bmax2(u.x, u.y), bmax2(u.z, u.w));
+  }
+  __device__ __forceinline__ static float hmax(uint32_t m) {
     return fmaxf(__uint_as_float(m << 16), __uint_as_float(m & 0xffff0000u));
   }
+  __device__ __forceinline__ static float vmax(const uint4& u) { return hmax(pmax(u)); }
   // elements e >= n of the vector become -1e30 (columns past V)
   __device__ __forceinline__ static void mask_from(uint4& u, int n) {
     uint32_t* w = reinterpret_cast<uint32_t*>(&u);
@@ -118,10 +146,200 @@ struct Pk<float> {
   }
 };
 
+// max over kGroup vectors
+template <typename T>
+__device__ __forceinline__ float group_max(const uint4 (&u)[kGroup]) {
+  if constexpr (sizeof(T) == 2) {
+    uint32_t m = Pk<bf16_t>::pmax(u[0]);
+#pragma unroll
+    for (int g = 1; g < kGroup; ++g) m = bmax2(m, Pk<bf16_t>::pmax(u[g]));
+    return Pk<bf16_t>::hmax(m);
+  } else {
+    float m = Pk<float>::vmax(u[0]);
+#pragma unroll
+    for (int g = 1; g < kGroup; ++g) m = fmaxf(m, Pk<float>::vmax(u[g]));
+    return m;
+  }
+}
+
+// ---- packed fp32x2 arithmetic (FFMA2 / FADD2 / FMUL2 on sm_100a) -------------
+
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk2(uint64_t r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+// the two elements of 32-bit word w of a vector, as an fp32x2 pair
+template <typename T>
+__device__ __forceinline__ uint64_t pair(const uint4& u, int w);
+template <>
+__device__ __forceinline__ uint64_t pair<bf16_t>(const uint4& u, int w) {
+  const uint32_t x = w == 0 ? u.x : w == 1 ? u.y : w == 2 ? u.z : u.w;
+  return pk2(__uint_as_float(x << 16), __uint_as_float(x & 0xffff0000u));
+}
+template <>
+__device__ __forceinline__ uint64_t pair<float>(const uint4& u, int w) {
+  return w == 0 ? pk2(__uint_as_float(u.x), __uint_as_float(u.y))
+                : pk2(__uint_as_float(u.z), __uint_as_float(u.w));
+}
+__device__ __forceinline__ uint64_t ex2x2(uint64_t a) {
+  float a0, a1;
+  upk2(a, a0, a1);
+  return pk2(ex2(a0), ex2(a1));
+}
+
+// Phase-1 accumulators as fp32x2 lanes (merged into Online at the end).
+// The running max m is updated lazily: terms use p = 2^((x - m) log2e), which
+// stays finite while x <= m + kSlack, so the rescale only runs when a vector
+// max exceeds m by more than kSlack (a handful of times per row).  Sums of
+// < 2^31 terms of <= e^kSlack cannot overflow fp32.
+constexpr float kSlack = 16.0f;
+
+struct Acc2 {
+  float m;
+  uint64_t nm2;  // (-m log2e, -m log2e)
+  uint64_t s2, t2;
+};
+
+__device__ __forceinline__ void rescale(Acc2& acc, float vmax) {
+  if (vmax > acc.m) {
+    const float sc = ex2((acc.m - vmax) * kLog2e);  // m = -inf -> 0
+    const uint64_t sc2 = pk2(sc, sc);
+    acc.s2 = mul2(acc.s2, sc2);
+    acc.t2 = mul2(acc.t2, sc2);
+    acc.m = vmax;
+    const float nmL = -vmax * kLog2e;
+    acc.nm2 = pk2(nmL, nmL);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void accumulate(Acc2& acc, const uint4& u) {
+  const uint64_t l2e2 = pk2(kLog2e, kLog2e);
+#pragma unroll
+  for (int w = 0; w < Vec<T>::N / 2; ++w) {
+    const uint64_t x = pair<T>(u, w);
+    const uint64_t p = ex2x2(fma2(x, l2e2, acc.nm2));
+    acc.s2 = add2(acc.s2, p);
+    acc.t2 = fma2(p, x, acc.t2);
+  }
+}
+
+// dz of one vector: p * (a + hz * z), p = 2^(z log2e - lse log2e).  Without the
+// entropy term (kHasH = false) -inf logits need no clamp: p = 0 exactly.
+template <typename T, bool kHasH>
+__device__ __forceinline__ void dz_vec(uint4 u, float (&d)[Vec<T>::N], uint64_t nl2, uint64_t av2,
+                                       uint64_t hz2) {
+  const uint64_t l2e2 = pk2(kLog2e, kLog2e);
+  if (kHasH) Pk<T>::clamp(u);
+#pragma unroll
+  for (int w = 0; w < Vec<T>::N / 2; ++w) {
+    const uint64_t x = pair<T>(u, w);
+    const uint64_t p = ex2x2(fma2(x, l2e2, nl2));
+    upk2(kHasH ? mul2(p, fma2(hz2, x, av2)) : mul2(p, av2), d[2 * w], d[2 * w + 1]);
+  }
+}
+
 __device__ __forceinline__ void prefetch_l2(const char* p, uint32_t bytes) {
   for (uint32_t off = 0; off < bytes; off += kPrefetchPiece) {
     const uint32_t n = min(kPrefetchPiece, bytes - off);
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p + off), "r"(n) : "memory");
+  }
+}
+
+// Ring position: slot index and mbarrier phase parity.
+struct RingPos {
+  int slot;
+  uint32_t phase;
+  __device__ __forceinline__ void next(int n) {
+    if (++slot == n) {
+      slot = 0;
+      phase ^= 1u;
+    }
+  }
+};
+
+// Per-CTA slice geometry (vectors of 16 bytes).
+struct Slice {
+  int v0, v1, nchunk, tail_vec, tail_valid;
+};
+
+// ---- phase 2: stream dz for one row from the resident chunks ----------------
+template <typename T, bool kHasH>
+__device__ __forceinline__ void phase2_row(const Slice& sl, RingPos pos, int n_slots,
+                                           uint32_t ring_s, uint32_t empty_s, char* dzrow,
+                                           int vy, int ye, float s_t, uint64_t nl2, uint64_t av2,
+                                           uint64_t hz2, int tid, int lane) {
+  constexpr int EPV = Vec<T>::N;
+  int vbase = sl.v0;
+  for (int j = 0; j < sl.nchunk; j += kGroup) {
+    const int ng = min(kGroup, sl.nchunk - j);
+    const int gend = min(sl.v1, vbase + ng * kConsumers);
+    const bool special = (gend - vbase != kGroup * kConsumers) ||
+                         (sl.tail_vec >= vbase && sl.tail_vec < gend) ||
+                         (vy >= vbase && vy < gend);
+    RingPos p = pos;
+    if (!special) {
+#pragma unroll
+      for (int g = 0; g < kGroup; ++g) {
+        const int vec = vbase + g * kConsumers + tid;
+        float d[EPV];
+        dz_vec<T, kHasH>(lds128(ring_s + uint32_t(p.slot) * kChunk + tid * 16), d, nl2, av2, hz2);
+        st_stream(dzrow + int64_t(vec) * 16, Vec<T>::pack(d));
+        p.next(n_slots);
+      }
+    } else {
+      for (int g = 0; g < ng; ++g) {
+        const int vec = vbase + g * kConsumers + tid;
+        if (vec < sl.v1) {
+          float d[EPV];
+          dz_vec<T, kHasH>(lds128(ring_s + uint32_t(p.slot) * kChunk + tid * 16), d, nl2, av2,
+                           hz2);
+          if (vec == vy) {
+#pragma unroll
+            for (int e = 0; e < EPV; ++e)
+              if (e == ye) d[e] -= s_t;
+          }
+          if (vec == sl.tail_vec) {
+#pragma unroll
+            for (int e = 0; e < EPV; ++e)
+              if (e < sl.tail_valid) Vec<T>::store1(dzrow, int64_t(vec) * EPV + e, d[e]);
+          } else {
+            st_stream(dzrow + int64_t(vec) * 16, Vec<T>::pack(d));
+          }
+        }
+        p.next(n_slots);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      for (int g = 0; g < ng; ++g) {
+        arrive_u32(empty_s + uint32_t(pos.slot) * 8u);
+        pos.next(n_slots);
+      }
+    }
+    if (lane != 0) {
+      for (int g = 0; g < ng; ++g) pos.next(n_slots);
+    }
+    vbase += ng * kConsumers;
   }
 }
 
@@ -134,6 +352,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* ring = smem;
   FusedSmemTail* tail = reinterpret_cast<FusedSmemTail*>(smem + size_t(n_slots) * kChunk);
+  const uint32_t ring_s = smem_u32(ring);
+  const uint32_t full_s = smem_u32(&tail->full[0]);
+  const uint32_t empty_s = smem_u32(&tail->empty[0]);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -144,13 +365,14 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   const int V = int(P.vocab);
 
   // column slice of this CTA, in 16-byte vectors (32-bit: V < 2^31)
+  Slice sl;
   const int nvec = (V + EPV - 1) / EPV;
-  const int v0 = int((int64_t(rank) * nvec) / CL);
-  const int v1 = int((int64_t(rank + 1) * nvec) / CL);
-  const uint32_t slice_bytes = uint32_t(v1 - v0) * 16u;
-  const int nchunk = int((slice_bytes + kChunk - 1) / kChunk);
-  const int tail_vec = (V % EPV) ? nvec - 1 : -1;  // global vector holding columns >= V
-  const int tail_valid = V - (nvec - 1) * EPV;
+  sl.v0 = int((int64_t(rank) * nvec) / CL);
+  sl.v1 = int((int64_t(rank + 1) * nvec) / CL);
+  const uint32_t slice_bytes = uint32_t(sl.v1 - sl.v0) * 16u;
+  sl.nchunk = int((slice_bytes + kChunk - 1) / kChunk);
+  sl.tail_vec = (V % EPV) ? nvec - 1 : -1;  // global vector holding columns >= V
+  sl.tail_valid = V - (nvec - 1) * EPV;
 
   if (tid == 0) {
     for (int i = 0; i < n_slots; ++i) {
@@ -169,216 +391,189 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
 
   if (warp == kConsumerWarps) {
     // ===================== producer warp: bulk TMA into the ring =====================
-    if (lane == 0 && nchunk > 0) {
+    if (lane == 0 && sl.nchunk > 0) {
       const uint64_t pol = policy_evict_first();
       const char* base = reinterpret_cast<const char*>(P.logits);
       auto slice_ptr = [&](int64_t row) {
         const int64_t src_row = P.row_index ? P.row_index[row] : row;
-        return base + src_row * P.ld * ESZ + int64_t(v0) * 16;
+        return base + src_row * P.ld * ESZ + int64_t(sl.v0) * 16;
       };
       for (int i = 0; i < prefetch_rows; ++i) {
         const int64_t r = cid + int64_t(i) * ncl;
         if (r < NR) prefetch_l2(slice_ptr(r), slice_bytes);
       }
-      int slot = 0;
-      uint32_t phase = 0;
+      RingPos pos = {0, 0u};
       for (int64_t row = cid; row < NR; row += ncl) {
         if (prefetch_rows > 0) {
           const int64_t r = row + int64_t(prefetch_rows) * ncl;
           if (r < NR) prefetch_l2(slice_ptr(r), slice_bytes);
         }
         const char* src = slice_ptr(row);
-        for (int j = 0; j < nchunk; ++j) {
-          mbar_wait(&tail->empty[slot], phase ^ 1u);
+        for (int j = 0; j < sl.nchunk; ++j) {
+          mbar_wait(&tail->empty[pos.slot], pos.phase ^ 1u);
           const uint32_t off = uint32_t(j) * kChunk;
           const uint32_t bytes = min(uint32_t(kChunk), slice_bytes - off);
-          mbar_arrive_expect_tx(&tail->full[slot], bytes);
-          tma_load_1d(ring + size_t(slot) * kChunk, src + off, bytes, &tail->full[slot], pol);
-          if (++slot == n_slots) {
-            slot = 0;
-            phase ^= 1u;
-          }
+          mbar_arrive_expect_tx(&tail->full[pos.slot], bytes);
+          tma_load_1d(ring + size_t(pos.slot) * kChunk, src + off, bytes, &tail->full[pos.slot],
+                      pol);
+          pos.next(n_slots);
         }
       }
     }
     __syncwarp();
   } else {
     // ===================== consumer warps =====================
-    const bool writer = (rank == 0) && (tid == 0);
-    int slot0 = 0;  // ring slot of the current row's first chunk
-    uint32_t phase0 = 0;
+    RingPos pos0 = {0, 0u};  // ring position of the current row's first chunk
     int64_t k = 0;
-    RowMeta cur;
-    if (cid < NR) cur = load_meta(meta, cid);
+    int y_cur = (cid < NR) ? __ldg(&meta[cid].y) : 0;
     for (int64_t row = cid; row < NR; row += ncl, ++k) {
       const int64_t nrow = row + ncl;
-      RowMeta nxt = cur;
-      if (nrow < NR) nxt = load_meta(meta, nrow);  // prefetch next row's metadata
-      const int y = cur.y;
+      const int y_next = (nrow < NR) ? __ldg(&meta[nrow].y) : 0;  // prefetch
+      const int y = y_cur;
       const int vy = (y >= 0 && y < V) ? (y / EPV) : -1;  // global vector holding the target
       const int ye = (vy >= 0) ? y - vy * EPV : 0;
 
       // ---------------- phase 1: online max / sum-exp / sum p*z ----------------
-      Online acc = {kNegInf, 0.f, 0.f};
+      Acc2 a2 = {kNegInf, pk2(0.f, 0.f), pk2(0.f, 0.f), pk2(0.f, 0.f)};  // nm2 set on 1st use
       float zy = kNegInf;
       {
-        int slot = slot0;
-        uint32_t phase = phase0;
-        int vbase = v0;
-        for (int j = 0; j < nchunk; ++j, vbase += kConsumers) {
-          const int nv = min(kConsumers, v1 - vbase);
-          mbar_wait(&tail->full[slot], phase);
-          if (tid < nv) {
-            uint4 u = reinterpret_cast<const uint4*>(ring + size_t(slot) * kChunk)[tid];
-            Pk<T>::clamp(u);
-            const int vec = vbase + tid;
-            if (vec == tail_vec) Pk<T>::mask_from(u, tail_valid);
-            if (vec == vy) zy = Pk<T>::elem(u, ye);
-            const float vmax = Pk<T>::vmax(u);
-            if (vmax > acc.m) {
-              const float sc = ex2((acc.m - vmax) * kLog2e);
-              acc.s *= sc;
-              acc.t *= sc;
-              acc.m = vmax;
-            }
-            float x[EPV];
-            Vec<T>::unpack(u, x);
-            const float mL = acc.m * kLog2e;
+        RingPos p = pos0;
+        int vbase = sl.v0;
+        for (int j = 0; j < sl.nchunk; j += kGroup) {
+          const int ng = min(kGroup, sl.nchunk - j);
+          const int gend = min(sl.v1, vbase + ng * kConsumers);
+          const bool special = (gend - vbase != kGroup * kConsumers) ||
+                               (sl.tail_vec >= vbase && sl.tail_vec < gend) ||
+                               (vy >= vbase && vy < gend);
+          if (!special) {  // common case: kGroup full chunks, every lane busy
+            uint4 u[kGroup];
 #pragma unroll
-            for (int e = 0; e < EPV; ++e) {
-              const float p = ex2(fmaf(x[e], kLog2e, -mL));
-              acc.s += p;
-              acc.t = fmaf(p, x[e], acc.t);
+            for (int g = 0; g < kGroup; ++g) {
+              wait_full(full_s + uint32_t(p.slot) * 8u, p.phase);
+              u[g] = lds128(ring_s + uint32_t(p.slot) * kChunk + tid * 16);
+              p.next(n_slots);
+            }
+#pragma unroll
+            for (int g = 0; g < kGroup; ++g) Pk<T>::clamp(u[g]);
+            const float vmax = group_max<T>(u);
+            if (__any_sync(0xffffffffu, vmax > a2.m + kSlack)) rescale(a2, vmax);
+#pragma unroll
+            for (int g = 0; g < kGroup; ++g) accumulate<T>(a2, u[g]);
+          } else {
+            for (int g = 0; g < ng; ++g) {
+              wait_full(full_s + uint32_t(p.slot) * 8u, p.phase);
+              const int vec = vbase + g * kConsumers + tid;
+              if (vec < sl.v1) {
+                uint4 u = lds128(ring_s + uint32_t(p.slot) * kChunk + tid * 16);
+                Pk<T>::clamp(u);
+                if (vec == sl.tail_vec) Pk<T>::mask_from(u, sl.tail_valid);
+                if (vec == vy) zy = Pk<T>::elem(u, ye);
+                const float vmax = Pk<T>::vmax(u);
+                if (vmax > a2.m + kSlack) rescale(a2, vmax);
+                accumulate<T>(a2, u);
+              }
+              p.next(n_slots);
             }
           }
-          if (++slot == n_slots) {
-            slot = 0;
-            phase ^= 1u;
-          }
+          vbase += ng * kConsumers;
         }
       }
-      // ---------------- reductions: warp -> CTA -> cluster ----------------
+      // ---------------- reductions: warp -> CTA -> cluster (warp 0) ----------------
+      Online acc;
+      {
+        float s0, s1, t0, t1;
+        upk2(a2.s2, s0, s1);
+        upk2(a2.t2, t0, t1);
+        acc = {a2.m, s0 + s1, t0 + t1};
+      }
       acc = warp_merge(acc);
       zy = warp_max(zy);
       const int par = int(k & 1);
       if (lane == 0) tail->wpart[par][warp] = make_float4(acc.m, acc.s, acc.t, zy);
       named_bar_sync(1, kConsumers);
-      Online cta = {kNegInf, 0.f, 0.f};
-      float czy = kNegInf;
+      if (warp == 0) {
+        float4 v = (lane < kConsumerWarps) ? tail->wpart[par][lane]
+                                           : make_float4(kNegInf, 0.f, 0.f, kNegInf);
+        Online cta = warp_merge(Online{v.x, v.y, v.z});
+        const float czy = warp_max(v.w);
+        Online tot = cta;
+        float tzy = czy;
+        if constexpr (CL > 1) {
+          if (lane == 0) {
+            mbar_arrive_expect_tx(&tail->xbar[par], (CL - 1) * 16);
+            const uint32_t my_slot = smem_u32(&tail->xdata[par][rank]);
+            const uint32_t bar = smem_u32(&tail->xbar[par]);
 #pragma unroll
-      for (int w = 0; w < kConsumerWarps; ++w) {
-        const float4 v = tail->wpart[par][w];
-        cta = online_merge(cta, Online{v.x, v.y, v.z});
-        czy = fmaxf(czy, v.w);
-      }
-      Online tot = cta;
-      float tzy = czy;
-      if constexpr (CL > 1) {
-        if (tid == 0) {
-          mbar_arrive_expect_tx(&tail->xbar[par], (CL - 1) * 16);
-          const uint32_t my_slot = smem_u32(&tail->xdata[par][rank]);
-          const uint32_t bar = smem_u32(&tail->xbar[par]);
+            for (int r = 0; r < CL; ++r) {
+              if (r == int(rank)) continue;
+              st_async_v4(map_to_rank(my_slot, r), cta.m, cta.s, cta.t, czy, map_to_rank(bar, r));
+            }
+          }
+          mbar_wait_cluster(&tail->xbar[par], uint32_t((k >> 1) & 1));
+          tot = {kNegInf, 0.f, 0.f};
+          tzy = kNegInf;
 #pragma unroll
-          for (int r = 0; r < CL; ++r) {
-            if (r == int(rank)) continue;
-            st_async_v4(map_to_rank(my_slot, r), cta.m, cta.s, cta.t, czy, map_to_rank(bar, r));
+          for (int r = 0; r < CL; ++r) {  // fixed rank order: identical result on every CTA
+            const float4 w = (r == int(rank)) ? make_float4(cta.m, cta.s, cta.t, czy)
+                                              : tail->xdata[par][r];
+            tot = online_merge(tot, Online{w.x, w.y, w.z});
+            tzy = fmaxf(tzy, w.w);
           }
         }
-        mbar_wait_cluster(&tail->xbar[par], uint32_t((k >> 1) & 1));
-        tot = {kNegInf, 0.f, 0.f};
-        tzy = kNegInf;
-#pragma unroll
-        for (int r = 0; r < CL; ++r) {  // fixed rank order: identical result on every CTA
-          float4 v = (r == int(rank)) ? make_float4(cta.m, cta.s, cta.t, czy)
-                                      : tail->xdata[par][r];
-          tot = online_merge(tot, Online{v.x, v.y, v.z});
-          tzy = fmaxf(tzy, v.w);
+        if (lane == 0) {
+          const RowMeta cur = load_meta(meta, row);
+          const float lse = tot.m + logf(tot.s);
+          const float H = lse - tot.t / tot.s;
+          const bool bad_target = (cur.flags & 2u) != 0;
+          const float lp = tzy - lse;
+          RowTerms o = meta_terms(P, cur, lp, H);
+          if (bad_target) {
+            o.s = 0.f;
+            o.h = 0.f;
+          }
+          tail->bcast[par] = make_float4(o.s + o.h * (H - lse), o.h, lse, o.s);
+          if (rank == 0) {
+            P.lp[row] = lp;
+            P.ent[row] = H;
+            P.lse[row] = lse;
+            const bool nonfin = !(finite_f(lse) && finite_f(lp) && finite_f(H) &&
+                                  finite_f(o.s) && finite_f(o.h));
+            double* sd = tail->stats;
+            sd[0] += o.l_pg;
+            sd[1] += o.l_kl;
+            sd[2] += o.l_ent;
+            sd[3] += o.l_sft;
+            sd[4] += o.clipped;
+            sd[5] += o.dual;
+            if (o.rl) {
+              sd[6] += H;
+              sd[7] += o.kl;
+              sd[8] += o.ppo_kl;
+              sd[11] += o.ratio;
+              sd[12] += 1.0;
+            }
+            sd[9] += lp;
+            sd[10] += nonfin;
+            sd[13] += bad_target;
+            sd[14] += 1.0;
+          }
         }
       }
-      const float lse = tot.m + logf(tot.s);
-      const float H = lse - tot.t / tot.s;
-      const bool bad_target = (cur.flags & 2u) != 0;
-      const float lp = tzy - lse;
-      RowTerms o = meta_terms(P, cur, lp, H);
-      if (bad_target) {
-        o.s = 0.f;
-        o.h = 0.f;
-      }
-      if (writer) {
-        P.lp[row] = lp;
-        P.ent[row] = H;
-        P.lse[row] = lse;
-        const bool nonfin = !(finite_f(lse) && finite_f(lp) && finite_f(H) && finite_f(o.s) &&
-                              finite_f(o.h));
-        double* sd = tail->stats;
-        sd[0] += o.l_pg;
-        sd[1] += o.l_kl;
-        sd[2] += o.l_ent;
-        sd[3] += o.l_sft;
-        sd[4] += o.clipped;
-        sd[5] += o.dual;
-        if (o.rl) {
-          sd[6] += H;
-          sd[7] += o.kl;
-          sd[8] += o.ppo_kl;
-          sd[11] += o.ratio;
-          sd[12] += 1.0;
-        }
-        sd[9] += lp;
-        sd[10] += nonfin;
-        sd[13] += bad_target;
-        sd[14] += 1.0;
-      }
+      named_bar_sync(2, kConsumers);
       // ---------------- phase 2: dz from the resident slice ----------------
-      const float hz = o.h;
-      const float a = o.s + hz * (H - lse);
+      const float4 bc = tail->bcast[par];
+      const float a = bc.x, hz = bc.y, lse = bc.z, s_t = bc.w;
       const float lseL = lse * kLog2e;
-      const float s_t = o.s;
+      const uint64_t nl2 = pk2(-lseL, -lseL), av2 = pk2(a, a), hz2 = pk2(hz, hz);
       char* dzrow = reinterpret_cast<char*>(P.dz) + row * P.ld_out * ESZ;
-      {
-        int slot = slot0;
-        uint32_t phase = phase0;
-        int vbase = v0;
-        for (int j = 0; j < nchunk; ++j, vbase += kConsumers) {
-          const int nv = min(kConsumers, v1 - vbase);
-          if (tid < nv) {
-            uint4 u = reinterpret_cast<const uint4*>(ring + size_t(slot) * kChunk)[tid];
-            Pk<T>::clamp(u);
-            float x[EPV], d[EPV];
-            Vec<T>::unpack(u, x);
-            if (hz == 0.f) {
-#pragma unroll
-              for (int e = 0; e < EPV; ++e) d[e] = ex2(fmaf(x[e], kLog2e, -lseL)) * a;
-            } else {
-#pragma unroll
-              for (int e = 0; e < EPV; ++e)
-                d[e] = ex2(fmaf(x[e], kLog2e, -lseL)) * fmaf(hz, x[e], a);
-            }
-            const int vec = vbase + tid;
-            if (vec == vy) {
-#pragma unroll
-              for (int e = 0; e < EPV; ++e)
-                if (e == ye) d[e] -= s_t;
-            }
-            if (vec != tail_vec) {
-              st_stream(dzrow + int64_t(vec) * 16, Vec<T>::pack(d));
-            } else {
-#pragma unroll
-              for (int e = 0; e < EPV; ++e)
-                if (e < tail_valid) Vec<T>::store1(dzrow, int64_t(vec) * EPV + e, d[e]);
-            }
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tail->empty[slot]);
-          if (++slot == n_slots) {
-            slot = 0;
-            phase ^= 1u;
-          }
-        }
-        slot0 = slot;
-        phase0 = phase;
-      }
-      cur = nxt;
+      if (hz == 0.f)
+        phase2_row<T, false>(sl, pos0, n_slots, ring_s, empty_s, dzrow, vy, ye, s_t, nl2, av2,
+                             hz2, tid, lane);
+      else
+        phase2_row<T, true>(sl, pos0, n_slots, ring_s, empty_s, dzrow, vy, ye, s_t, nl2, av2,
+                            hz2, tid, lane);
+      for (int j = 0; j < sl.nchunk; ++j) pos0.next(n_slots);
+      y_cur = y_next;
     }
     // rank 0 of each cluster accumulated its rows; other ranks store zeros
     if (tid == 0) {
