@@ -282,6 +282,75 @@ struct Slice {
   int v0, v1, nchunk, tail_vec, tail_valid;
 };
 
+// ---- phase 1: one consumer step over up to kGroup chunks -------------------
+// Lanes past the slice end load a neutral (-1e30) vector and skip the sums but
+// still vote, so the lazy-rescale test is always a full-warp vote.
+template <typename T, bool kMaskTail>
+__device__ __forceinline__ void phase1_group(Acc2& acc, int ng, int vbase, const Slice& sl,
+                                             RingPos p, int n_slots, uint32_t ring_s,
+                                             uint32_t full_s, int tid) {
+  uint4 u[kGroup];
+  bool valid[kGroup];
+#pragma unroll
+  for (int g = 0; g < kGroup; ++g) {
+    valid[g] = false;
+    u[g] = make_uint4(kBf16NegBig2, kBf16NegBig2, kBf16NegBig2, kBf16NegBig2);
+    if (sizeof(T) == 4) u[g] = make_uint4(0xF149F2CAu, 0xF149F2CAu, 0xF149F2CAu, 0xF149F2CAu);
+    if (g < ng) {
+      wait_full(full_s + uint32_t(p.slot) * 8u, p.phase);
+      const int vec = vbase + g * kConsumers + tid;
+      valid[g] = vec < sl.v1;
+      if (valid[g]) {
+        u[g] = lds128(ring_s + uint32_t(p.slot) * kChunk + tid * 16);
+        Pk<T>::clamp(u[g]);
+        if (kMaskTail && vec == sl.tail_vec) Pk<T>::mask_from(u[g], sl.tail_valid);
+      }
+      p.next(n_slots);
+    }
+  }
+  const float vmax = group_max<T>(u);
+  if (__any_sync(0xffffffffu, vmax > acc.m + kSlack)) rescale(acc, vmax);
+#pragma unroll
+  for (int g = 0; g < kGroup; ++g)
+    if (valid[g]) accumulate<T>(acc, u[g]);
+}
+
+// ---- phase 2: dz for one consumer step ---------------------------------------
+template <typename T, bool kHasH, bool kCheck>
+__device__ __forceinline__ void phase2_group(int ng, int vbase, const Slice& sl, RingPos p,
+                                             int n_slots, uint32_t ring_s, char* dzrow, int vy,
+                                             int ye, float s_t, uint64_t nl2, uint64_t av2,
+                                             uint64_t hz2, int tid) {
+  constexpr int EPV = Vec<T>::N;
+#pragma unroll
+  for (int g = 0; g < kGroup; ++g) {
+    if (g < ng) {
+      const int vec = vbase + g * kConsumers + tid;
+      if (vec < sl.v1) {
+        float d[EPV];
+        dz_vec<T, kHasH>(lds128(ring_s + uint32_t(p.slot) * kChunk + tid * 16), d, nl2, av2,
+                         hz2);
+        bool done = false;
+        if (kCheck) {
+          if (vec == vy) {
+#pragma unroll
+            for (int e = 0; e < EPV; ++e)
+              if (e == ye) d[e] -= s_t;
+          }
+          if (vec == sl.tail_vec) {
+#pragma unroll
+            for (int e = 0; e < EPV; ++e)
+              if (e < sl.tail_valid) Vec<T>::store1(dzrow, int64_t(vec) * EPV + e, d[e]);
+            done = true;
+          }
+        }
+        if (!done) st_stream(dzrow + int64_t(vec) * 16, Vec<T>::pack(d));
+      }
+      p.next(n_slots);
+    }
+  }
+}
+
 // ---- phase 2: stream dz for one row from the resident chunks ----------------
 template <typename T, bool kHasH>
 __device__ __forceinline__ void phase2_row(const Slice& sl, RingPos pos, int n_slots,
@@ -293,42 +362,15 @@ __device__ __forceinline__ void phase2_row(const Slice& sl, RingPos pos, int n_s
   for (int j = 0; j < sl.nchunk; j += kGroup) {
     const int ng = min(kGroup, sl.nchunk - j);
     const int gend = min(sl.v1, vbase + ng * kConsumers);
-    const bool special = (gend - vbase != kGroup * kConsumers) ||
-                         (sl.tail_vec >= vbase && sl.tail_vec < gend) ||
+    // the group holding the target logit or the tail padding takes the checked variant
+    const bool special = (sl.tail_vec >= vbase && sl.tail_vec < gend) ||
                          (vy >= vbase && vy < gend);
-    RingPos p = pos;
-    if (!special) {
-#pragma unroll
-      for (int g = 0; g < kGroup; ++g) {
-        const int vec = vbase + g * kConsumers + tid;
-        float d[EPV];
-        dz_vec<T, kHasH>(lds128(ring_s + uint32_t(p.slot) * kChunk + tid * 16), d, nl2, av2, hz2);
-        st_stream(dzrow + int64_t(vec) * 16, Vec<T>::pack(d));
-        p.next(n_slots);
-      }
-    } else {
-      for (int g = 0; g < ng; ++g) {
-        const int vec = vbase + g * kConsumers + tid;
-        if (vec < sl.v1) {
-          float d[EPV];
-          dz_vec<T, kHasH>(lds128(ring_s + uint32_t(p.slot) * kChunk + tid * 16), d, nl2, av2,
-                           hz2);
-          if (vec == vy) {
-#pragma unroll
-            for (int e = 0; e < EPV; ++e)
-              if (e == ye) d[e] -= s_t;
-          }
-          if (vec == sl.tail_vec) {
-#pragma unroll
-            for (int e = 0; e < EPV; ++e)
-              if (e < sl.tail_valid) Vec<T>::store1(dzrow, int64_t(vec) * EPV + e, d[e]);
-          } else {
-            st_stream(dzrow + int64_t(vec) * 16, Vec<T>::pack(d));
-          }
-        }
-        p.next(n_slots);
-      }
-    }
+    if (special)
+      phase2_group<T, kHasH, true>(ng, vbase, sl, pos, n_slots, ring_s, dzrow, vy, ye, s_t, nl2,
+                                   av2, hz2, tid);
+    else
+      phase2_group<T, kHasH, false>(ng, vbase, sl, pos, n_slots, ring_s, dzrow, vy, ye, s_t, nl2,
+                                    av2, hz2, tid);
     __syncwarp();
     if (lane == 0) {
       for (int g = 0; g < ng; ++g) {
@@ -433,48 +475,23 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       const int vy = (y >= 0 && y < V) ? (y / EPV) : -1;  // global vector holding the target
       const int ye = (vy >= 0) ? y - vy * EPV : 0;
 
+      // per-row metadata for the epilogue: warp 0 / lane 0 only, latency hidden by phase 1
+      RowMeta cur;
+      if (tid == 0) cur = load_meta(meta, row);
+
       // ---------------- phase 1: online max / sum-exp / sum p*z ----------------
       Acc2 a2 = {kNegInf, pk2(0.f, 0.f), pk2(0.f, 0.f), pk2(0.f, 0.f)};  // nm2 set on 1st use
-      float zy = kNegInf;
       {
         RingPos p = pos0;
         int vbase = sl.v0;
         for (int j = 0; j < sl.nchunk; j += kGroup) {
           const int ng = min(kGroup, sl.nchunk - j);
           const int gend = min(sl.v1, vbase + ng * kConsumers);
-          const bool special = (gend - vbase != kGroup * kConsumers) ||
-                               (sl.tail_vec >= vbase && sl.tail_vec < gend) ||
-                               (vy >= vbase && vy < gend);
-          if (!special) {  // common case: kGroup full chunks, every lane busy
-            uint4 u[kGroup];
-#pragma unroll
-            for (int g = 0; g < kGroup; ++g) {
-              wait_full(full_s + uint32_t(p.slot) * 8u, p.phase);
-              u[g] = lds128(ring_s + uint32_t(p.slot) * kChunk + tid * 16);
-              p.next(n_slots);
-            }
-#pragma unroll
-            for (int g = 0; g < kGroup; ++g) Pk<T>::clamp(u[g]);
-            const float vmax = group_max<T>(u);
-            if (__any_sync(0xffffffffu, vmax > a2.m + kSlack)) rescale(a2, vmax);
-#pragma unroll
-            for (int g = 0; g < kGroup; ++g) accumulate<T>(a2, u[g]);
-          } else {
-            for (int g = 0; g < ng; ++g) {
-              wait_full(full_s + uint32_t(p.slot) * 8u, p.phase);
-              const int vec = vbase + g * kConsumers + tid;
-              if (vec < sl.v1) {
-                uint4 u = lds128(ring_s + uint32_t(p.slot) * kChunk + tid * 16);
-                Pk<T>::clamp(u);
-                if (vec == sl.tail_vec) Pk<T>::mask_from(u, sl.tail_valid);
-                if (vec == vy) zy = Pk<T>::elem(u, ye);
-                const float vmax = Pk<T>::vmax(u);
-                if (vmax > a2.m + kSlack) rescale(a2, vmax);
-                accumulate<T>(a2, u);
-              }
-              p.next(n_slots);
-            }
-          }
+          if (sl.tail_vec >= vbase && sl.tail_vec < gend)
+            phase1_group<T, true>(a2, ng, vbase, sl, p, n_slots, ring_s, full_s, tid);
+          else
+            phase1_group<T, false>(a2, ng, vbase, sl, p, n_slots, ring_s, full_s, tid);
+          for (int g = 0; g < ng; ++g) p.next(n_slots);
           vbase += ng * kConsumers;
         }
       }
@@ -487,15 +504,25 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         acc = {a2.m, s0 + s1, t0 + t1};
       }
       acc = warp_merge(acc);
-      zy = warp_max(zy);
       const int par = int(k & 1);
-      if (lane == 0) tail->wpart[par][warp] = make_float4(acc.m, acc.s, acc.t, zy);
+      if (lane == 0) tail->wpart[par][warp] = make_float4(acc.m, acc.s, acc.t, 0.f);
       named_bar_sync(1, kConsumers);
+      RowTerms o;
+      float lse = 0.f, H = 0.f, lp = 0.f;
+      bool bad_target = false;
       if (warp == 0) {
         float4 v = (lane < kConsumerWarps) ? tail->wpart[par][lane]
-                                           : make_float4(kNegInf, 0.f, 0.f, kNegInf);
+                                           : make_float4(kNegInf, 0.f, 0.f, 0.f);
         Online cta = warp_merge(Online{v.x, v.y, v.z});
-        const float czy = warp_max(v.w);
+        // the target logit, read straight from the still-resident chunk (raw, unclamped)
+        float czy = kNegInf;
+        if (vy >= sl.v0 && vy < sl.v1) {
+          const int off = vy - sl.v0;
+          int slot = pos0.slot + off / kConsumers;
+          slot -= (slot >= n_slots) ? n_slots : 0;
+          const uint4 w = lds128(ring_s + uint32_t(slot) * kChunk + (off % kConsumers) * 16);
+          czy = Vec<T>::N == 8 ? Pk<bf16_t>::elem(w, ye) : Pk<float>::elem(w, ye);
+        }
         Online tot = cta;
         float tzy = czy;
         if constexpr (CL > 1) {
@@ -521,49 +548,48 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
           }
         }
         if (lane == 0) {
-          const RowMeta cur = load_meta(meta, row);
-          const float lse = tot.m + logf(tot.s);
-          const float H = lse - tot.t / tot.s;
-          const bool bad_target = (cur.flags & 2u) != 0;
-          const float lp = tzy - lse;
-          RowTerms o = meta_terms(P, cur, lp, H);
+          lse = tot.m + logf(tot.s);
+          H = lse - tot.t / tot.s;
+          bad_target = (cur.flags & 2u) != 0;
+          lp = tzy - lse;
+          o = meta_terms(P, cur, lp, H);
           if (bad_target) {
             o.s = 0.f;
             o.h = 0.f;
           }
           tail->bcast[par] = make_float4(o.s + o.h * (H - lse), o.h, lse, o.s);
-          if (rank == 0) {
-            P.lp[row] = lp;
-            P.ent[row] = H;
-            P.lse[row] = lse;
-            const bool nonfin = !(finite_f(lse) && finite_f(lp) && finite_f(H) &&
-                                  finite_f(o.s) && finite_f(o.h));
-            double* sd = tail->stats;
-            sd[0] += o.l_pg;
-            sd[1] += o.l_kl;
-            sd[2] += o.l_ent;
-            sd[3] += o.l_sft;
-            sd[4] += o.clipped;
-            sd[5] += o.dual;
-            if (o.rl) {
-              sd[6] += H;
-              sd[7] += o.kl;
-              sd[8] += o.ppo_kl;
-              sd[11] += o.ratio;
-              sd[12] += 1.0;
-            }
-            sd[9] += lp;
-            sd[10] += nonfin;
-            sd[13] += bad_target;
-            sd[14] += 1.0;
-          }
         }
       }
       named_bar_sync(2, kConsumers);
+      if (tid == 0 && rank == 0) {  // outputs + statistics, off the critical path
+        P.lp[row] = lp;
+        P.ent[row] = H;
+        P.lse[row] = lse;
+        const bool nonfin = !(finite_f(lse) && finite_f(lp) && finite_f(H) && finite_f(o.s) &&
+                              finite_f(o.h));
+        double* sd = tail->stats;
+        sd[0] += o.l_pg;
+        sd[1] += o.l_kl;
+        sd[2] += o.l_ent;
+        sd[3] += o.l_sft;
+        sd[4] += o.clipped;
+        sd[5] += o.dual;
+        if (o.rl) {
+          sd[6] += H;
+          sd[7] += o.kl;
+          sd[8] += o.ppo_kl;
+          sd[11] += o.ratio;
+          sd[12] += 1.0;
+        }
+        sd[9] += lp;
+        sd[10] += nonfin;
+        sd[13] += bad_target;
+        sd[14] += 1.0;
+      }
       // ---------------- phase 2: dz from the resident slice ----------------
       const float4 bc = tail->bcast[par];
-      const float a = bc.x, hz = bc.y, lse = bc.z, s_t = bc.w;
-      const float lseL = lse * kLog2e;
+      const float a = bc.x, hz = bc.y, s_t = bc.w;
+      const float lseL = bc.z * kLog2e;
       const uint64_t nl2 = pk2(-lseL, -lseL), av2 = pk2(a, a), hz2 = pk2(hz, hz);
       char* dzrow = reinterpret_cast<char*>(P.dz) + row * P.ld_out * ESZ;
       if (hz == 0.f)
