@@ -289,6 +289,7 @@ FusedPlan fused_plan(const TgBatch* b, const TgOut* o) {
   const size_t tail = fused_smem_bytes(0);
   int n_slots = int((size_t(d.smem_optin) - tail) / size_t(fused_chunk_bytes()));
   if (n_slots > fused_max_slots()) n_slots = fused_max_slots();
+  if (n_slots < fused_max_slots()) return fp;  // the kernel's ring size is a compile-time 30
   for (int cl = 1; cl <= 4; cl *= 2) {
     if (force_cl && cl != force_cl) continue;
     const int64_t slice_vec = (nvec + cl - 1) / cl;

@@ -10,21 +10,20 @@
 //  * A thread-block cluster of CL CTAs (CL = 1 for V <= ~110k bf16, 2 for
 //    Qwen's 151,936) owns one row at a time; CTA rank r owns a contiguous
 //    column slice of the row.  The slice never leaves the SM: a producer warp
-//    streams it into a shared-memory ring with 1-D bulk TMA
-//    (cp.async.bulk ... mbarrier::complete_tx), one 7.5 KB chunk per ring
-//    slot with a full / empty mbarrier pair, and keeps HBM busy across row
-//    boundaries by prefetching upcoming rows' slices into L2
-//    (cp.async.bulk.prefetch.L2) -- the ring holds ~1.5 slices.
+//    streams it into a 30-slot shared-memory ring with 1-D bulk TMA
+//    (cp.async.bulk ... mbarrier::complete_tx), one 7.5 KB chunk per slot with
+//    a full / empty mbarrier pair, and prefetches upcoming rows' slices into
+//    L2 (cp.async.bulk.prefetch.L2) -- the ring holds ~1.5 slices.
 //  * 15 consumer warps, one 16-byte vector per thread per chunk, consume
 //    kGroup chunks per step.  Phase 1 (as chunks land): online max / sum-exp /
-//    sum p*z and the target logit in packed fp32x2 arithmetic (FFMA2 / FADD2)
-//    with MUFU ex2; -inf logits are clamped to -1e30 with packed bf16x2 max;
-//    the running max is updated lazily behind a warp vote.  One named barrier
-//    collects per-warp partials; warp 0 reduces them, exchanges the CTA
-//    partial with its cluster peers through DSMEM (st.async completing tx
-//    bytes on the peer's mbarrier; rank-order merge => bit-identical lse on
-//    every CTA), evaluates the registry epilogue (tg_rowcoef.cuh) and
-//    broadcasts (a, h, lse) through a second named barrier.
+//    sum p*z in packed fp32x2 arithmetic (FFMA2 / FADD2) with MUFU ex2; -inf
+//    logits are clamped to -1e30 with packed bf16x2 max; the running max is
+//    updated lazily behind a warp vote.  One named barrier collects per-warp
+//    partials; warp 0 reduces them, reads the target logit from the resident
+//    chunk, exchanges the CTA partial with its cluster peers through DSMEM
+//    (st.async completing tx bytes on the peer's mbarrier; rank-order merge =>
+//    bit-identical lse on every CTA), evaluates the registry epilogue
+//    (tg_rowcoef.cuh) and broadcasts (a, h, lse, s) through a second barrier.
 //  * Phase 2 re-reads the resident chunks from SMEM and writes
 //    dz = p (s + h((z - lse) + H)) - s[v = y] with 128-bit streaming stores,
 //    releasing each slot to the producer, which refills it with the next row.
@@ -43,12 +42,12 @@ constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kFusedThreads = kConsumers + 32;
 constexpr int kChunk = kConsumers * 16;  // 7680 bytes: one 16-byte vector per consumer thread
 constexpr int kGroup = 4;                // chunks consumed per step
-constexpr int kMaxSlots = 30;
+constexpr int kSlots = 30;               // ring slots: 225 KB of the 227 KB opt-in SMEM
 constexpr uint32_t kPrefetchPiece = 65536;  // bytes per L2 prefetch instruction
 
 struct FusedSmemTail {
-  uint64_t full[kMaxSlots];
-  uint64_t empty[kMaxSlots];
+  uint64_t full[kSlots];
+  uint64_t empty[kSlots];
   uint64_t xbar[2];
   float4 xdata[2][4];
   float4 wpart[2][kConsumerWarps];
@@ -58,12 +57,12 @@ struct FusedSmemTail {
 
 // ---- shared-memory / barrier primitives on 32-bit shared addresses ----------
 
+// volatile: stays ordered after the (volatile) mbarrier wait that publishes the data
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   uint4 r;
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "r"(addr)
-               : "memory");
+               : "r"(addr));
   return r;
 }
 
@@ -76,6 +75,22 @@ __device__ __forceinline__ void arrive_u32(uint32_t bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
+// Ring iterator: chunk address, its full / empty barrier addresses, phase parity.
+struct RingIt {
+  uint32_t addr, full, empty, phase;
+  __device__ __forceinline__ void next(uint32_t ring_s, uint32_t full_s, uint32_t empty_s) {
+    addr += kChunk;
+    full += 8;
+    empty += 8;
+    if (addr == ring_s + kSlots * kChunk) {
+      addr = ring_s;
+      full = full_s;
+      empty = empty_s;
+      phase ^= 1u;
+    }
+  }
+};
+
 // ---- packed-element helpers (bf16: 8 per vector, fp32: 4 per vector) --------
 
 __device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
@@ -85,6 +100,7 @@ __device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
 }
 
 constexpr uint32_t kBf16NegBig2 = 0xF149F149u;  // (-1.0e30, -1.0e30) as bf16x2
+constexpr uint32_t kF32NegBig = 0xF149F2CAu;    // -1.0e30f
 constexpr float kNegBig = -1.0e30f;
 
 template <typename T>
@@ -98,6 +114,9 @@ struct Pk<bf16_t> {
     u.y = bmax2(u.y, kBf16NegBig2);
     u.z = bmax2(u.z, kBf16NegBig2);
     u.w = bmax2(u.w, kBf16NegBig2);
+  }
+  __device__ __forceinline__ static uint4 neutral() {
+    return make_uint4(kBf16NegBig2, kBf16NegBig2, kBf16NegBig2, kBf16NegBig2);
   }
   __device__ __forceinline__ static uint32_t pmax(const uint4& u) {
     return bmax2(bmax2(u.x, u.y), bmax2(u.z, u.w));
@@ -131,6 +150,9 @@ struct Pk<float> {
     u.z = __float_as_uint(fmaxf(__uint_as_float(u.z), kNegBig));
     u.w = __float_as_uint(fmaxf(__uint_as_float(u.w), kNegBig));
   }
+  __device__ __forceinline__ static uint4 neutral() {
+    return make_uint4(kF32NegBig, kF32NegBig, kF32NegBig, kF32NegBig);
+  }
   __device__ __forceinline__ static float vmax(const uint4& u) {
     return fmaxf(fmaxf(__uint_as_float(u.x), __uint_as_float(u.y)),
                  fmaxf(__uint_as_float(u.z), __uint_as_float(u.w)));
@@ -139,7 +161,7 @@ struct Pk<float> {
     uint32_t* w = reinterpret_cast<uint32_t*>(&u);
 #pragma unroll
     for (int e = 0; e < 4; ++e)
-      if (e >= n) w[e] = __float_as_uint(kNegBig);
+      if (e >= n) w[e] = kF32NegBig;
   }
   __device__ __forceinline__ static float elem(const uint4& u, int e) {
     return __uint_as_float(e == 0 ? u.x : e == 1 ? u.y : e == 2 ? u.z : u.w);
@@ -265,71 +287,61 @@ __device__ __forceinline__ void prefetch_l2(const char* p, uint32_t bytes) {
   }
 }
 
-// Ring position: slot index and mbarrier phase parity.
-struct RingPos {
-  int slot;
-  uint32_t phase;
-  __device__ __forceinline__ void next(int n) {
-    if (++slot == n) {
-      slot = 0;
-      phase ^= 1u;
-    }
-  }
-};
-
 // Per-CTA slice geometry (vectors of 16 bytes).
 struct Slice {
   int v0, v1, nchunk, tail_vec, tail_valid;
 };
 
-// ---- phase 1: one consumer step over up to kGroup chunks -------------------
-// Lanes past the slice end load a neutral (-1e30) vector and skip the sums but
-// still vote, so the lazy-rescale test is always a full-warp vote.
-template <typename T, bool kMaskTail>
-__device__ __forceinline__ void phase1_group(Acc2& acc, int ng, int vbase, const Slice& sl,
-                                             RingPos p, int n_slots, uint32_t ring_s,
-                                             uint32_t full_s, int tid) {
+struct RingBase {
+  uint32_t ring, full, empty;
+};
+
+// ---- phase 1: one consumer step over kGroup chunks --------------------------
+// kPartial: the step may run past the slice end (lanes there use a neutral
+// -1e30 vector and skip the sums, but still vote, so the lazy-rescale test is
+// always a full-warp vote).  kMaskTail: the step holds the tail padding.
+template <typename T, bool kPartial, bool kMaskTail>
+__device__ __forceinline__ void phase1_step(Acc2& acc, RingIt& it, const RingBase& rb, int ng,
+                                            int vbase, const Slice& sl, int tid) {
   uint4 u[kGroup];
   bool valid[kGroup];
 #pragma unroll
   for (int g = 0; g < kGroup; ++g) {
-    valid[g] = false;
-    u[g] = make_uint4(kBf16NegBig2, kBf16NegBig2, kBf16NegBig2, kBf16NegBig2);
-    if (sizeof(T) == 4) u[g] = make_uint4(0xF149F2CAu, 0xF149F2CAu, 0xF149F2CAu, 0xF149F2CAu);
-    if (g < ng) {
-      wait_full(full_s + uint32_t(p.slot) * 8u, p.phase);
+    if (!kPartial || g < ng) {
+      wait_full(it.full, it.phase);
       const int vec = vbase + g * kConsumers + tid;
-      valid[g] = vec < sl.v1;
-      if (valid[g]) {
-        u[g] = lds128(ring_s + uint32_t(p.slot) * kChunk + tid * 16);
-        Pk<T>::clamp(u[g]);
-        if (kMaskTail && vec == sl.tail_vec) Pk<T>::mask_from(u[g], sl.tail_valid);
-      }
-      p.next(n_slots);
+      valid[g] = !kPartial || vec < sl.v1;
+      u[g] = valid[g] ? lds128(it.addr + tid * 16) : Pk<T>::neutral();
+      Pk<T>::clamp(u[g]);
+      if (kMaskTail && vec == sl.tail_vec) Pk<T>::mask_from(u[g], sl.tail_valid);
+      it.next(rb.ring, rb.full, rb.empty);
+    } else {
+      valid[g] = false;
+      u[g] = Pk<T>::neutral();
     }
   }
   const float vmax = group_max<T>(u);
   if (__any_sync(0xffffffffu, vmax > acc.m + kSlack)) rescale(acc, vmax);
 #pragma unroll
   for (int g = 0; g < kGroup; ++g)
-    if (valid[g]) accumulate<T>(acc, u[g]);
+    if (!kPartial || valid[g]) accumulate<T>(acc, u[g]);
 }
 
 // ---- phase 2: dz for one consumer step ---------------------------------------
 template <typename T, bool kHasH, bool kCheck>
-__device__ __forceinline__ void phase2_group(int ng, int vbase, const Slice& sl, RingPos p,
-                                             int n_slots, uint32_t ring_s, char* dzrow, int vy,
-                                             int ye, float s_t, uint64_t nl2, uint64_t av2,
-                                             uint64_t hz2, int tid) {
+__device__ __forceinline__ void phase2_step(RingIt& it, const RingBase& rb, int ng, int vbase,
+                                            const Slice& sl, char* dzrow, int vy, int ye,
+                                            float s_t, uint64_t nl2, uint64_t av2, uint64_t hz2,
+                                            int tid) {
   constexpr int EPV = Vec<T>::N;
+  char* dst = dzrow + int64_t(vbase + tid) * 16;
 #pragma unroll
   for (int g = 0; g < kGroup; ++g) {
-    if (g < ng) {
+    if (!kCheck || g < ng) {
       const int vec = vbase + g * kConsumers + tid;
-      if (vec < sl.v1) {
+      if (!kCheck || vec < sl.v1) {
         float d[EPV];
-        dz_vec<T, kHasH>(lds128(ring_s + uint32_t(p.slot) * kChunk + tid * 16), d, nl2, av2,
-                         hz2);
+        dz_vec<T, kHasH>(lds128(it.addr + tid * 16), d, nl2, av2, hz2);
         bool done = false;
         if (kCheck) {
           if (vec == vy) {
@@ -344,42 +356,36 @@ __device__ __forceinline__ void phase2_group(int ng, int vbase, const Slice& sl,
             done = true;
           }
         }
-        if (!done) st_stream(dzrow + int64_t(vec) * 16, Vec<T>::pack(d));
+        if (!done) st_stream(dst + g * kChunk, Vec<T>::pack(d));
       }
-      p.next(n_slots);
+      it.next(rb.ring, rb.full, rb.empty);
     }
   }
 }
 
-// ---- phase 2: stream dz for one row from the resident chunks ----------------
+// phase 2 over one row: kGroup-chunk steps; the step holding the target logit
+// or tail padding, and the last partial step, take the checked variant.
 template <typename T, bool kHasH>
-__device__ __forceinline__ void phase2_row(const Slice& sl, RingPos pos, int n_slots,
-                                           uint32_t ring_s, uint32_t empty_s, char* dzrow,
-                                           int vy, int ye, float s_t, uint64_t nl2, uint64_t av2,
-                                           uint64_t hz2, int tid, int lane) {
-  constexpr int EPV = Vec<T>::N;
+__device__ __forceinline__ void phase2_row(const Slice& sl, RingIt it, const RingBase& rb,
+                                           char* dzrow, int vy, int ye, float s_t, uint64_t nl2,
+                                           uint64_t av2, uint64_t hz2, int tid, int lane) {
   int vbase = sl.v0;
   for (int j = 0; j < sl.nchunk; j += kGroup) {
     const int ng = min(kGroup, sl.nchunk - j);
-    const int gend = min(sl.v1, vbase + ng * kConsumers);
-    // the group holding the target logit or the tail padding takes the checked variant
-    const bool special = (sl.tail_vec >= vbase && sl.tail_vec < gend) ||
-                         (vy >= vbase && vy < gend);
-    if (special)
-      phase2_group<T, kHasH, true>(ng, vbase, sl, pos, n_slots, ring_s, dzrow, vy, ye, s_t, nl2,
-                                   av2, hz2, tid);
+    const int gend = vbase + kGroup * kConsumers;
+    const bool check = (gend > sl.v1) || (sl.tail_vec >= vbase && sl.tail_vec < gend) ||
+                       (vy >= vbase && vy < gend);
+    RingIt rel = it;
+    if (check)
+      phase2_step<T, kHasH, true>(it, rb, ng, vbase, sl, dzrow, vy, ye, s_t, nl2, av2, hz2, tid);
     else
-      phase2_group<T, kHasH, false>(ng, vbase, sl, pos, n_slots, ring_s, dzrow, vy, ye, s_t, nl2,
-                                    av2, hz2, tid);
+      phase2_step<T, kHasH, false>(it, rb, ng, vbase, sl, dzrow, vy, ye, s_t, nl2, av2, hz2, tid);
     __syncwarp();
     if (lane == 0) {
       for (int g = 0; g < ng; ++g) {
-        arrive_u32(empty_s + uint32_t(pos.slot) * 8u);
-        pos.next(n_slots);
+        arrive_u32(rel.empty);
+        rel.next(rb.ring, rb.full, rb.empty);
       }
-    }
-    if (lane != 0) {
-      for (int g = 0; g < ng; ++g) pos.next(n_slots);
     }
     vbase += ng * kConsumers;
   }
@@ -387,16 +393,13 @@ __device__ __forceinline__ void phase2_row(const Slice& sl, RingPos pos, int n_s
 
 template <typename T, int CL>
 __global__ void __launch_bounds__(kFusedThreads, 1)
-    k_fused_tma(const KParams P, const RowMeta* __restrict__ meta, int n_slots,
-                int prefetch_rows) {
+    k_fused_tma(const KParams P, const RowMeta* __restrict__ meta, int prefetch_rows) {
   constexpr int EPV = Vec<T>::N;  // elements per 16-byte vector
   constexpr int ESZ = elem_bytes<T>();
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* ring = smem;
-  FusedSmemTail* tail = reinterpret_cast<FusedSmemTail*>(smem + size_t(n_slots) * kChunk);
-  const uint32_t ring_s = smem_u32(ring);
-  const uint32_t full_s = smem_u32(&tail->full[0]);
-  const uint32_t empty_s = smem_u32(&tail->empty[0]);
+  FusedSmemTail* tail = reinterpret_cast<FusedSmemTail*>(smem + size_t(kSlots) * kChunk);
+  const RingBase rb = {smem_u32(ring), smem_u32(&tail->full[0]), smem_u32(&tail->empty[0])};
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -417,7 +420,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   sl.tail_valid = V - (nvec - 1) * EPV;
 
   if (tid == 0) {
-    for (int i = 0; i < n_slots; ++i) {
+    for (int i = 0; i < kSlots; ++i) {
       mbar_init(&tail->full[i], 1);
       mbar_init(&tail->empty[i], kConsumerWarps);
     }
@@ -444,7 +447,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         const int64_t r = cid + int64_t(i) * ncl;
         if (r < NR) prefetch_l2(slice_ptr(r), slice_bytes);
       }
-      RingPos pos = {0, 0u};
+      RingIt it = {rb.ring, rb.full, rb.empty, 0u};
       for (int64_t row = cid; row < NR; row += ncl) {
         if (prefetch_rows > 0) {
           const int64_t r = row + int64_t(prefetch_rows) * ncl;
@@ -452,20 +455,27 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         }
         const char* src = slice_ptr(row);
         for (int j = 0; j < sl.nchunk; ++j) {
-          mbar_wait(&tail->empty[pos.slot], pos.phase ^ 1u);
+          while (!mbar_try_wait(it.empty, it.phase ^ 1u)) {
+          }
           const uint32_t off = uint32_t(j) * kChunk;
           const uint32_t bytes = min(uint32_t(kChunk), slice_bytes - off);
-          mbar_arrive_expect_tx(&tail->full[pos.slot], bytes);
-          tma_load_1d(ring + size_t(pos.slot) * kChunk, src + off, bytes, &tail->full[pos.slot],
-                      pol);
-          pos.next(n_slots);
+          asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                           it.full),
+                       "r"(bytes)
+                       : "memory");
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+              " [%0], [%1], %2, [%3], %4;" ::"r"(it.addr),
+              "l"(src + off), "r"(bytes), "r"(it.full), "l"(pol)
+              : "memory");
+          it.next(rb.ring, rb.full, rb.empty);
         }
       }
     }
     __syncwarp();
   } else {
     // ===================== consumer warps =====================
-    RingPos pos0 = {0, 0u};  // ring position of the current row's first chunk
+    RingIt pos0 = {rb.ring, rb.full, rb.empty, 0u};  // the current row's first chunk
     int64_t k = 0;
     int y_cur = (cid < NR) ? __ldg(&meta[cid].y) : 0;
     for (int64_t row = cid; row < NR; row += ncl, ++k) {
@@ -474,24 +484,25 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       const int y = y_cur;
       const int vy = (y >= 0 && y < V) ? (y / EPV) : -1;  // global vector holding the target
       const int ye = (vy >= 0) ? y - vy * EPV : 0;
-
-      // per-row metadata for the epilogue: warp 0 / lane 0 only, latency hidden by phase 1
+      // per-row metadata for the epilogue: thread 0 only, latency hidden by phase 1
       RowMeta cur;
       if (tid == 0) cur = load_meta(meta, row);
 
       // ---------------- phase 1: online max / sum-exp / sum p*z ----------------
       Acc2 a2 = {kNegInf, pk2(0.f, 0.f), pk2(0.f, 0.f), pk2(0.f, 0.f)};  // nm2 set on 1st use
       {
-        RingPos p = pos0;
+        RingIt it = pos0;
         int vbase = sl.v0;
         for (int j = 0; j < sl.nchunk; j += kGroup) {
           const int ng = min(kGroup, sl.nchunk - j);
-          const int gend = min(sl.v1, vbase + ng * kConsumers);
-          if (sl.tail_vec >= vbase && sl.tail_vec < gend)
-            phase1_group<T, true>(a2, ng, vbase, sl, p, n_slots, ring_s, full_s, tid);
+          const int gend = vbase + kGroup * kConsumers;
+          const bool has_tail = sl.tail_vec >= vbase && sl.tail_vec < gend;
+          if (gend <= sl.v1 && !has_tail)
+            phase1_step<T, false, false>(a2, it, rb, ng, vbase, sl, tid);
+          else if (!has_tail)
+            phase1_step<T, true, false>(a2, it, rb, ng, vbase, sl, tid);
           else
-            phase1_group<T, false>(a2, ng, vbase, sl, p, n_slots, ring_s, full_s, tid);
-          for (int g = 0; g < ng; ++g) p.next(n_slots);
+            phase1_step<T, true, true>(a2, it, rb, ng, vbase, sl, tid);
           vbase += ng * kConsumers;
         }
       }
@@ -511,17 +522,17 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       float lse = 0.f, H = 0.f, lp = 0.f;
       bool bad_target = false;
       if (warp == 0) {
-        float4 v = (lane < kConsumerWarps) ? tail->wpart[par][lane]
-                                           : make_float4(kNegInf, 0.f, 0.f, 0.f);
-        Online cta = warp_merge(Online{v.x, v.y, v.z});
+        const float4 v = (lane < kConsumerWarps) ? tail->wpart[par][lane]
+                                                 : make_float4(kNegInf, 0.f, 0.f, 0.f);
+        const Online cta = warp_merge(Online{v.x, v.y, v.z});
         // the target logit, read straight from the still-resident chunk (raw, unclamped)
         float czy = kNegInf;
         if (vy >= sl.v0 && vy < sl.v1) {
           const int off = vy - sl.v0;
-          int slot = pos0.slot + off / kConsumers;
-          slot -= (slot >= n_slots) ? n_slots : 0;
-          const uint4 w = lds128(ring_s + uint32_t(slot) * kChunk + (off % kConsumers) * 16);
-          czy = Vec<T>::N == 8 ? Pk<bf16_t>::elem(w, ye) : Pk<float>::elem(w, ye);
+          uint32_t addr = pos0.addr + uint32_t(off / kConsumers) * kChunk;
+          if (addr >= rb.ring + kSlots * kChunk) addr -= kSlots * kChunk;
+          const uint4 w = lds128(addr + uint32_t(off % kConsumers) * 16);
+          czy = Pk<T>::elem(w, ye);
         }
         Online tot = cta;
         float tzy = czy;
@@ -593,12 +604,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       const uint64_t nl2 = pk2(-lseL, -lseL), av2 = pk2(a, a), hz2 = pk2(hz, hz);
       char* dzrow = reinterpret_cast<char*>(P.dz) + row * P.ld_out * ESZ;
       if (hz == 0.f)
-        phase2_row<T, false>(sl, pos0, n_slots, ring_s, empty_s, dzrow, vy, ye, s_t, nl2, av2,
-                             hz2, tid, lane);
+        phase2_row<T, false>(sl, pos0, rb, dzrow, vy, ye, s_t, nl2, av2, hz2, tid, lane);
       else
-        phase2_row<T, true>(sl, pos0, n_slots, ring_s, empty_s, dzrow, vy, ye, s_t, nl2, av2,
-                            hz2, tid, lane);
-      for (int j = 0; j < sl.nchunk; ++j) pos0.next(n_slots);
+        phase2_row<T, true>(sl, pos0, rb, dzrow, vy, ye, s_t, nl2, av2, hz2, tid, lane);
+      for (int j = 0; j < sl.nchunk; ++j) pos0.next(rb.ring, rb.full, rb.empty);
       y_cur = y_next;
     }
     // rank 0 of each cluster accumulated its rows; other ranks store zeros
@@ -633,9 +642,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
 size_t fused_smem_bytes(int n_slots) { return size_t(n_slots) * kChunk + sizeof(FusedSmemTail); }
 
 template <typename T, int CL>
-static cudaError_t launch_fused_t(const KParams& P, const RowMeta* meta, int n_slots, int n_ctas,
+static cudaError_t launch_fused_t(const KParams& P, const RowMeta* meta, int n_ctas,
                                   int prefetch_rows, cudaStream_t stream) {
-  const size_t smem = fused_smem_bytes(n_slots);
+  const size_t smem = fused_smem_bytes(kSlots);
   cudaError_t e = cudaFuncSetAttribute(k_fused_tma<T, CL>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
@@ -651,26 +660,27 @@ static cudaError_t launch_fused_t(const KParams& P, const RowMeta* meta, int n_s
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_fused_tma<T, CL>, P, meta, n_slots, prefetch_rows);
+  return cudaLaunchKernelEx(&cfg, k_fused_tma<T, CL>, P, meta, prefetch_rows);
 }
 
 cudaError_t launch_fused(const KParams& P, const void* meta, int cl, int n_slots, int n_ctas,
                          int prefetch_rows, cudaStream_t stream) {
+  if (n_slots != kSlots) return cudaErrorInvalidValue;
   const RowMeta* m = reinterpret_cast<const RowMeta*>(meta);
   if (P.dtype == TG_DTYPE_BF16) {
-    if (cl == 1) return launch_fused_t<bf16_t, 1>(P, m, n_slots, n_ctas, prefetch_rows, stream);
-    if (cl == 2) return launch_fused_t<bf16_t, 2>(P, m, n_slots, n_ctas, prefetch_rows, stream);
-    if (cl == 4) return launch_fused_t<bf16_t, 4>(P, m, n_slots, n_ctas, prefetch_rows, stream);
+    if (cl == 1) return launch_fused_t<bf16_t, 1>(P, m, n_ctas, prefetch_rows, stream);
+    if (cl == 2) return launch_fused_t<bf16_t, 2>(P, m, n_ctas, prefetch_rows, stream);
+    if (cl == 4) return launch_fused_t<bf16_t, 4>(P, m, n_ctas, prefetch_rows, stream);
   } else {
-    if (cl == 1) return launch_fused_t<float, 1>(P, m, n_slots, n_ctas, prefetch_rows, stream);
-    if (cl == 2) return launch_fused_t<float, 2>(P, m, n_slots, n_ctas, prefetch_rows, stream);
-    if (cl == 4) return launch_fused_t<float, 4>(P, m, n_slots, n_ctas, prefetch_rows, stream);
+    if (cl == 1) return launch_fused_t<float, 1>(P, m, n_ctas, prefetch_rows, stream);
+    if (cl == 2) return launch_fused_t<float, 2>(P, m, n_ctas, prefetch_rows, stream);
+    if (cl == 4) return launch_fused_t<float, 4>(P, m, n_ctas, prefetch_rows, stream);
   }
   return cudaErrorInvalidValue;
 }
 
 int fused_chunk_bytes() { return kChunk; }
-int fused_max_slots() { return kMaxSlots; }
+int fused_max_slots() { return kSlots; }
 size_t rowmeta_bytes() { return sizeof(RowMeta); }
 
 }  // namespace tg
