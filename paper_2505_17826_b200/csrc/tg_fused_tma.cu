@@ -34,24 +34,29 @@
 
 namespace tg {
 
-// 15 consumer warps + 1 producer warp = 16 warps: with the 4-warp register
-// allocation granularity this leaves 128 registers per thread (17 warps would
-// cap it at 96 and spill).
-constexpr int kConsumerWarps = 15;
+// 14 consumer warps + 1 epilogue warp + 1 producer warp = 16 warps: with the
+// 4-warp register allocation granularity this leaves 128 registers per thread
+// (17 warps would cap it at 96 and spill).
+constexpr int kConsumerWarps = 14;
 constexpr int kConsumers = kConsumerWarps * 32;
-constexpr int kFusedThreads = kConsumers + 32;
-constexpr int kChunk = kConsumers * 16;  // 7680 bytes: one 16-byte vector per consumer thread
+constexpr int kEpilogueWarp = kConsumerWarps;
+constexpr int kProducerWarp = kConsumerWarps + 1;
+constexpr int kFusedThreads = kConsumers + 64;
+constexpr int kChunk = kConsumers * 16;  // 7168 bytes: one 16-byte vector per consumer thread
 constexpr int kGroup = 4;                // chunks consumed per step
-constexpr int kSlots = 30;               // ring slots: 225 KB of the 227 KB opt-in SMEM
+constexpr int kSlots = 32;               // ring slots: 224 KB of the 227 KB opt-in SMEM
+constexpr int kMaxPrefixGroups = 2;      // next-row phase-1 steps run before this row's phase 2
 constexpr uint32_t kPrefetchPiece = 65536;  // bytes per L2 prefetch instruction
 
 struct FusedSmemTail {
   uint64_t full[kSlots];
   uint64_t empty[kSlots];
-  uint64_t xbar[2];
+  uint64_t xbar[2];   // cluster exchange (DSMEM tx bytes from the peers)
+  uint64_t pbar[2];   // consumers -> epilogue warp: per-warp partials written
+  uint64_t bbar[2];   // epilogue warp -> consumers: (a, h, lse, s) written
   float4 xdata[2][4];
   float4 wpart[2][kConsumerWarps];
-  float4 bcast[2];  // (a, h, lse, s) of the current row, from warp 0
+  float4 bcast[2];  // (a, h, lse, s) of a row, from the epilogue warp
   double stats[16];
 };
 
@@ -391,6 +396,36 @@ __device__ __forceinline__ void phase2_row(const Slice& sl, RingIt it, const Rin
   }
 }
 
+// phase 1 over steps [g0, g1) of a row whose first chunk is at `row_it`
+template <typename T>
+__device__ __forceinline__ void phase1_range(Acc2& acc, RingIt row_it, const RingBase& rb,
+                                             const Slice& sl, int g0, int g1, int tid) {
+  RingIt it = row_it;
+  for (int c = 0; c < g0 * kGroup; ++c) it.next(rb.ring, rb.full, rb.empty);
+  int vbase = sl.v0 + g0 * kGroup * kConsumers;
+  for (int gi = g0; gi < g1; ++gi) {
+    const int ng = min(kGroup, sl.nchunk - gi * kGroup);
+    const int gend = vbase + kGroup * kConsumers;
+    const bool has_tail = sl.tail_vec >= vbase && sl.tail_vec < gend;
+    if (gend <= sl.v1 && !has_tail)
+      phase1_step<T, false, false>(acc, it, rb, ng, vbase, sl, tid);
+    else if (!has_tail)
+      phase1_step<T, true, false>(acc, it, rb, ng, vbase, sl, tid);
+    else
+      phase1_step<T, true, true>(acc, it, rb, ng, vbase, sl, tid);
+    vbase += ng * kConsumers;
+  }
+}
+
+__device__ __forceinline__ Acc2 acc_init() {
+  return Acc2{kNegInf, pk2(0.f, 0.f), pk2(0.f, 0.f), pk2(0.f, 0.f)};  // nm2 set on first use
+}
+
+__device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
 template <typename T, int CL>
 __global__ void __launch_bounds__(kFusedThreads, 1)
     k_fused_tma(const KParams P, const RowMeta* __restrict__ meta, int prefetch_rows) {
@@ -418,15 +453,20 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   sl.nchunk = int((slice_bytes + kChunk - 1) / kChunk);
   sl.tail_vec = (V % EPV) ? nvec - 1 : -1;  // global vector holding columns >= V
   sl.tail_valid = V - (nvec - 1) * EPV;
+  const int nsteps = (sl.nchunk + kGroup - 1) / kGroup;
+  // next-row phase-1 steps that fit in the ring beside this row's slice
+  const int pre = min(min(kMaxPrefixGroups, (kSlots - sl.nchunk) / kGroup), nsteps);
 
   if (tid == 0) {
     for (int i = 0; i < kSlots; ++i) {
       mbar_init(&tail->full[i], 1);
       mbar_init(&tail->empty[i], kConsumerWarps);
     }
-    mbar_init(&tail->xbar[0], 1);
-    mbar_init(&tail->xbar[1], 1);
-    for (int i = 0; i < 16; ++i) tail->stats[i] = 0.0;
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tail->xbar[i], 1);
+      mbar_init(&tail->pbar[i], kConsumerWarps);
+      mbar_init(&tail->bbar[i], 1);
+    }
     fence_mbar_init();
   }
   if (CL > 1)
@@ -434,7 +474,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   else
     __syncthreads();
 
-  if (warp == kConsumerWarps) {
+  if (warp == kProducerWarp) {
     // ===================== producer warp: bulk TMA into the ring =====================
     if (lane == 0 && sl.nchunk > 0) {
       const uint64_t pol = policy_evict_first();
@@ -455,8 +495,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         }
         const char* src = slice_ptr(row);
         for (int j = 0; j < sl.nchunk; ++j) {
-          while (!mbar_try_wait(it.empty, it.phase ^ 1u)) {
-          }
+          mbar_wait_u32(it.empty, it.phase ^ 1u);
           const uint32_t off = uint32_t(j) * kChunk;
           const uint32_t bytes = min(uint32_t(kChunk), slice_bytes - off);
           asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
@@ -473,146 +512,101 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       }
     }
     __syncwarp();
-  } else {
-    // ===================== consumer warps =====================
-    RingIt pos0 = {rb.ring, rb.full, rb.empty, 0u};  // the current row's first chunk
+  } else if (warp == kEpilogueWarp) {
+    // ===================== epilogue warp: row reductions + registry epilogue ==========
+    // Off the consumers' critical path: while it reduces row k, exchanges with
+    // the cluster peers and evaluates the loss terms, the consumers already run
+    // phase 1 of row k+1.
+    double sd[15];
+#pragma unroll
+    for (int i = 0; i < 15; ++i) sd[i] = 0.0;
+    RingIt pos0 = {rb.ring, rb.full, rb.empty, 0u};
     int64_t k = 0;
-    int y_cur = (cid < NR) ? __ldg(&meta[cid].y) : 0;
     for (int64_t row = cid; row < NR; row += ncl, ++k) {
-      const int64_t nrow = row + ncl;
-      const int y_next = (nrow < NR) ? __ldg(&meta[nrow].y) : 0;  // prefetch
-      const int y = y_cur;
-      const int vy = (y >= 0 && y < V) ? (y / EPV) : -1;  // global vector holding the target
-      const int ye = (vy >= 0) ? y - vy * EPV : 0;
-      // per-row metadata for the epilogue: thread 0 only, latency hidden by phase 1
-      RowMeta cur;
-      if (tid == 0) cur = load_meta(meta, row);
-
-      // ---------------- phase 1: online max / sum-exp / sum p*z ----------------
-      Acc2 a2 = {kNegInf, pk2(0.f, 0.f), pk2(0.f, 0.f), pk2(0.f, 0.f)};  // nm2 set on 1st use
-      {
-        RingIt it = pos0;
-        int vbase = sl.v0;
-        for (int j = 0; j < sl.nchunk; j += kGroup) {
-          const int ng = min(kGroup, sl.nchunk - j);
-          const int gend = vbase + kGroup * kConsumers;
-          const bool has_tail = sl.tail_vec >= vbase && sl.tail_vec < gend;
-          if (gend <= sl.v1 && !has_tail)
-            phase1_step<T, false, false>(a2, it, rb, ng, vbase, sl, tid);
-          else if (!has_tail)
-            phase1_step<T, true, false>(a2, it, rb, ng, vbase, sl, tid);
-          else
-            phase1_step<T, true, true>(a2, it, rb, ng, vbase, sl, tid);
-          vbase += ng * kConsumers;
-        }
-      }
-      // ---------------- reductions: warp -> CTA -> cluster (warp 0) ----------------
-      Online acc;
-      {
-        float s0, s1, t0, t1;
-        upk2(a2.s2, s0, s1);
-        upk2(a2.t2, t0, t1);
-        acc = {a2.m, s0 + s1, t0 + t1};
-      }
-      acc = warp_merge(acc);
       const int par = int(k & 1);
-      if (lane == 0) tail->wpart[par][warp] = make_float4(acc.m, acc.s, acc.t, 0.f);
-      named_bar_sync(1, kConsumers);
-      RowTerms o;
-      float lse = 0.f, H = 0.f, lp = 0.f;
-      bool bad_target = false;
-      if (warp == 0) {
-        const float4 v = (lane < kConsumerWarps) ? tail->wpart[par][lane]
-                                                 : make_float4(kNegInf, 0.f, 0.f, 0.f);
-        const Online cta = warp_merge(Online{v.x, v.y, v.z});
-        // the target logit, read straight from the still-resident chunk (raw, unclamped)
-        float czy = kNegInf;
-        if (vy >= sl.v0 && vy < sl.v1) {
-          const int off = vy - sl.v0;
-          uint32_t addr = pos0.addr + uint32_t(off / kConsumers) * kChunk;
-          if (addr >= rb.ring + kSlots * kChunk) addr -= kSlots * kChunk;
-          const uint4 w = lds128(addr + uint32_t(off % kConsumers) * 16);
-          czy = Pk<T>::elem(w, ye);
-        }
-        Online tot = cta;
-        float tzy = czy;
-        if constexpr (CL > 1) {
-          if (lane == 0) {
-            mbar_arrive_expect_tx(&tail->xbar[par], (CL - 1) * 16);
-            const uint32_t my_slot = smem_u32(&tail->xdata[par][rank]);
-            const uint32_t bar = smem_u32(&tail->xbar[par]);
-#pragma unroll
-            for (int r = 0; r < CL; ++r) {
-              if (r == int(rank)) continue;
-              st_async_v4(map_to_rank(my_slot, r), cta.m, cta.s, cta.t, czy, map_to_rank(bar, r));
-            }
-          }
-          mbar_wait_cluster(&tail->xbar[par], uint32_t((k >> 1) & 1));
-          tot = {kNegInf, 0.f, 0.f};
-          tzy = kNegInf;
-#pragma unroll
-          for (int r = 0; r < CL; ++r) {  // fixed rank order: identical result on every CTA
-            const float4 w = (r == int(rank)) ? make_float4(cta.m, cta.s, cta.t, czy)
-                                              : tail->xdata[par][r];
-            tot = online_merge(tot, Online{w.x, w.y, w.z});
-            tzy = fmaxf(tzy, w.w);
-          }
-        }
+      const uint32_t parity = uint32_t((k >> 1) & 1);
+      RowMeta cur;
+      if (lane == 0) cur = load_meta(meta, row);
+      const int y = __ldg(&meta[row].y);
+      const int vy = (y >= 0 && y < V) ? (y / EPV) : -1;
+      const int ye = (vy >= 0) ? y - vy * EPV : 0;
+      mbar_wait_u32(smem_u32(&tail->pbar[par]), parity);
+      const float4 v = (lane < kConsumerWarps) ? tail->wpart[par][lane]
+                                               : make_float4(kNegInf, 0.f, 0.f, 0.f);
+      const Online cta = warp_merge(Online{v.x, v.y, v.z});
+      // the target logit, read straight from the still-resident chunk (raw, unclamped)
+      float czy = kNegInf;
+      if (vy >= sl.v0 && vy < sl.v1) {
+        const int off = vy - sl.v0;
+        uint32_t addr = pos0.addr + uint32_t(off / kConsumers) * kChunk;
+        if (addr >= rb.ring + kSlots * kChunk) addr -= kSlots * kChunk;
+        czy = Pk<T>::elem(lds128(addr + uint32_t(off % kConsumers) * 16), ye);
+      }
+      Online tot = cta;
+      float tzy = czy;
+      if constexpr (CL > 1) {
         if (lane == 0) {
-          lse = tot.m + logf(tot.s);
-          H = lse - tot.t / tot.s;
-          bad_target = (cur.flags & 2u) != 0;
-          lp = tzy - lse;
-          o = meta_terms(P, cur, lp, H);
-          if (bad_target) {
-            o.s = 0.f;
-            o.h = 0.f;
+          mbar_arrive_expect_tx(&tail->xbar[par], (CL - 1) * 16);
+          const uint32_t my_slot = smem_u32(&tail->xdata[par][rank]);
+          const uint32_t bar = smem_u32(&tail->xbar[par]);
+#pragma unroll
+          for (int r = 0; r < CL; ++r) {
+            if (r == int(rank)) continue;
+            st_async_v4(map_to_rank(my_slot, r), cta.m, cta.s, cta.t, czy, map_to_rank(bar, r));
           }
-          tail->bcast[par] = make_float4(o.s + o.h * (H - lse), o.h, lse, o.s);
+        }
+        mbar_wait_cluster(&tail->xbar[par], parity);
+        tot = {kNegInf, 0.f, 0.f};
+        tzy = kNegInf;
+#pragma unroll
+        for (int r = 0; r < CL; ++r) {  // fixed rank order: identical result on every CTA
+          const float4 w = (r == int(rank)) ? make_float4(cta.m, cta.s, cta.t, czy)
+                                            : tail->xdata[par][r];
+          tot = online_merge(tot, Online{w.x, w.y, w.z});
+          tzy = fmaxf(tzy, w.w);
         }
       }
-      named_bar_sync(2, kConsumers);
-      if (tid == 0 && rank == 0) {  // outputs + statistics, off the critical path
-        P.lp[row] = lp;
-        P.ent[row] = H;
-        P.lse[row] = lse;
-        const bool nonfin = !(finite_f(lse) && finite_f(lp) && finite_f(H) && finite_f(o.s) &&
-                              finite_f(o.h));
-        double* sd = tail->stats;
-        sd[0] += o.l_pg;
-        sd[1] += o.l_kl;
-        sd[2] += o.l_ent;
-        sd[3] += o.l_sft;
-        sd[4] += o.clipped;
-        sd[5] += o.dual;
-        if (o.rl) {
-          sd[6] += H;
-          sd[7] += o.kl;
-          sd[8] += o.ppo_kl;
-          sd[11] += o.ratio;
-          sd[12] += 1.0;
+      if (lane == 0) {
+        const float lse = tot.m + logf(tot.s);
+        const float H = lse - tot.t / tot.s;
+        const bool bad_target = (cur.flags & 2u) != 0;
+        const float lp = tzy - lse;
+        RowTerms o = meta_terms(P, cur, lp, H);
+        if (bad_target) {
+          o.s = 0.f;
+          o.h = 0.f;
         }
-        sd[9] += lp;
-        sd[10] += nonfin;
-        sd[13] += bad_target;
-        sd[14] += 1.0;
+        tail->bcast[par] = make_float4(o.s + o.h * (H - lse), o.h, lse, o.s);
+        arrive_u32(smem_u32(&tail->bbar[par]));
+        if (rank == 0) {  // outputs + statistics, after the broadcast
+          P.lp[row] = lp;
+          P.ent[row] = H;
+          P.lse[row] = lse;
+          const bool nonfin = !(finite_f(lse) && finite_f(lp) && finite_f(H) && finite_f(o.s) &&
+                                finite_f(o.h));
+          sd[0] += o.l_pg;
+          sd[1] += o.l_kl;
+          sd[2] += o.l_ent;
+          sd[3] += o.l_sft;
+          sd[4] += o.clipped;
+          sd[5] += o.dual;
+          if (o.rl) {
+            sd[6] += H;
+            sd[7] += o.kl;
+            sd[8] += o.ppo_kl;
+            sd[11] += o.ratio;
+            sd[12] += 1.0;
+          }
+          sd[9] += lp;
+          sd[10] += nonfin;
+          sd[13] += bad_target;
+          sd[14] += 1.0;
+        }
       }
-      // ---------------- phase 2: dz from the resident slice ----------------
-      const float4 bc = tail->bcast[par];
-      const float a = bc.x, hz = bc.y, s_t = bc.w;
-      const float lseL = bc.z * kLog2e;
-      const uint64_t nl2 = pk2(-lseL, -lseL), av2 = pk2(a, a), hz2 = pk2(hz, hz);
-      char* dzrow = reinterpret_cast<char*>(P.dz) + row * P.ld_out * ESZ;
-      if (hz == 0.f)
-        phase2_row<T, false>(sl, pos0, rb, dzrow, vy, ye, s_t, nl2, av2, hz2, tid, lane);
-      else
-        phase2_row<T, true>(sl, pos0, rb, dzrow, vy, ye, s_t, nl2, av2, hz2, tid, lane);
       for (int j = 0; j < sl.nchunk; ++j) pos0.next(rb.ring, rb.full, rb.empty);
-      y_cur = y_next;
     }
     // rank 0 of each cluster accumulated its rows; other ranks store zeros
-    if (tid == 0) {
-      const double* sd = tail->stats;
+    if (lane == 0) {
       double* dst = P.partials + size_t(blockIdx.x) * TG_NSTAT;
       for (int i = 0; i < TG_NSTAT; ++i) dst[i] = 0.0;
       dst[TG_S_PG_LOSS] = sd[0];
@@ -630,6 +624,54 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       dst[TG_S_N_TOK_RL] = sd[12];
       dst[TG_S_INVALID] = sd[13];
       dst[TG_S_N_TOK] = sd[14];
+    }
+  } else {
+    // ===================== consumer warps =====================
+    RingIt pos0 = {rb.ring, rb.full, rb.empty, 0u};  // the current row's first chunk
+    Acc2 acc = acc_init();
+    if (cid < NR) phase1_range<T>(acc, pos0, rb, sl, 0, pre, tid);  // first row's prefix
+    int y_cur = (cid < NR) ? __ldg(&meta[cid].y) : 0;
+    int64_t k = 0;
+    for (int64_t row = cid; row < NR; row += ncl, ++k) {
+      const int64_t nrow = row + ncl;
+      const int y_next = (nrow < NR) ? __ldg(&meta[nrow].y) : 0;  // prefetch
+      const int y = y_cur;
+      const int vy = (y >= 0 && y < V) ? (y / EPV) : -1;  // global vector holding the target
+      const int ye = (vy >= 0) ? y - vy * EPV : 0;
+      const int par = int(k & 1);
+
+      // ---------------- phase 1 (rest of the row) ----------------
+      phase1_range<T>(acc, pos0, rb, sl, pre, nsteps, tid);
+      Online o;
+      {
+        float s0, s1, t0, t1;
+        upk2(acc.s2, s0, s1);
+        upk2(acc.t2, t0, t1);
+        o = warp_merge(Online{acc.m, s0 + s1, t0 + t1});
+      }
+      if (lane == 0) {
+        tail->wpart[par][warp] = make_float4(o.m, o.s, o.t, 0.f);
+        arrive_u32(smem_u32(&tail->pbar[par]));
+      }
+      // ---------------- phase 1 prefix of the next row (hides the epilogue) ----------
+      RingIt npos = pos0;
+      for (int j = 0; j < sl.nchunk; ++j) npos.next(rb.ring, rb.full, rb.empty);
+      acc = acc_init();
+      if (nrow < NR) phase1_range<T>(acc, npos, rb, sl, 0, pre, tid);
+
+      // ---------------- phase 2: dz from the resident slice ----------------
+      mbar_wait_u32(smem_u32(&tail->bbar[par]), uint32_t((k >> 1) & 1));
+      const float4 bc = tail->bcast[par];
+      const float a = bc.x, hz = bc.y, s_t = bc.w;
+      const float lseL = bc.z * kLog2e;
+      const uint64_t nl2 = pk2(-lseL, -lseL), av2 = pk2(a, a), hz2 = pk2(hz, hz);
+      char* dzrow = reinterpret_cast<char*>(P.dz) + row * P.ld_out * ESZ;
+      if (hz == 0.f)
+        phase2_row<T, false>(sl, pos0, rb, dzrow, vy, ye, s_t, nl2, av2, hz2, tid, lane);
+      else
+        phase2_row<T, true>(sl, pos0, rb, dzrow, vy, ye, s_t, nl2, av2, hz2, tid, lane);
+      pos0 = npos;
+      y_cur = y_next;
     }
   }
   if (CL > 1)
