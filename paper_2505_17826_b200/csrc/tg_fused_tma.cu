@@ -422,7 +422,7 @@ __device__ __forceinline__ Acc2 acc_init() {
 }
 
 __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) {
+  while (!mbar_try_wait_sleep(bar, parity)) {
   }
 }
 
