@@ -80,20 +80,21 @@ __device__ __forceinline__ void arrive_u32(uint32_t bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
-// Ring iterator: chunk address, its full / empty barrier addresses, phase parity.
+struct RingBase {
+  uint32_t ring, full, empty;  // shared addresses of slot 0's data / full / empty barrier
+};
+
+// Ring position as a running chunk counter: slot = c mod kSlots, mbarrier phase
+// parity = (c / kSlots) & 1 (kSlots is a power of two, so both are one op).
 struct RingIt {
-  uint32_t addr, full, empty, phase;
-  __device__ __forceinline__ void next(uint32_t ring_s, uint32_t full_s, uint32_t empty_s) {
-    addr += kChunk;
-    full += 8;
-    empty += 8;
-    if (addr == ring_s + kSlots * kChunk) {
-      addr = ring_s;
-      full = full_s;
-      empty = empty_s;
-      phase ^= 1u;
-    }
-  }
+  uint32_t c;
+  __device__ __forceinline__ uint32_t slot() const { return c & (kSlots - 1); }
+  __device__ __forceinline__ uint32_t phase() const { return (c / kSlots) & 1u; }
+  __device__ __forceinline__ uint32_t addr(const RingBase& rb) const { return rb.ring + slot() * kChunk; }
+  __device__ __forceinline__ uint32_t full(const RingBase& rb) const { return rb.full + slot() * 8u; }
+  __device__ __forceinline__ uint32_t empty(const RingBase& rb) const { return rb.empty + slot() * 8u; }
+  __device__ __forceinline__ void next() { ++c; }
+  __device__ __forceinline__ void advance(int n) { c += uint32_t(n); }
 };
 
 // ---- packed-element helpers (bf16: 8 per vector, fp32: 4 per vector) --------
@@ -297,10 +298,6 @@ struct Slice {
   int v0, v1, nchunk, tail_vec, tail_valid;
 };
 
-struct RingBase {
-  uint32_t ring, full, empty;
-};
-
 // ---- phase 1: one consumer step over kGroup chunks --------------------------
 // kPartial: the step may run past the slice end (lanes there use a neutral
 // -1e30 vector and skip the sums, but still vote, so the lazy-rescale test is
@@ -313,13 +310,13 @@ __device__ __forceinline__ void phase1_step(Acc2& acc, RingIt& it, const RingBas
 #pragma unroll
   for (int g = 0; g < kGroup; ++g) {
     if (!kPartial || g < ng) {
-      wait_full(it.full, it.phase);
+      wait_full(it.full(rb), it.phase());
       const int vec = vbase + g * kConsumers + tid;
       valid[g] = !kPartial || vec < sl.v1;
-      u[g] = valid[g] ? lds128(it.addr + tid * 16) : Pk<T>::neutral();
+      u[g] = valid[g] ? lds128(it.addr(rb) + tid * 16) : Pk<T>::neutral();
       Pk<T>::clamp(u[g]);
       if (kMaskTail && vec == sl.tail_vec) Pk<T>::mask_from(u[g], sl.tail_valid);
-      it.next(rb.ring, rb.full, rb.empty);
+      it.next();
     } else {
       valid[g] = false;
       u[g] = Pk<T>::neutral();
@@ -346,7 +343,7 @@ __device__ __forceinline__ void phase2_step(RingIt& it, const RingBase& rb, int 
       const int vec = vbase + g * kConsumers + tid;
       if (!kCheck || vec < sl.v1) {
         float d[EPV];
-        dz_vec<T, kHasH>(lds128(it.addr + tid * 16), d, nl2, av2, hz2);
+        dz_vec<T, kHasH>(lds128(it.addr(rb) + tid * 16), d, nl2, av2, hz2);
         bool done = false;
         if (kCheck) {
           if (vec == vy) {
@@ -363,7 +360,7 @@ __device__ __forceinline__ void phase2_step(RingIt& it, const RingBase& rb, int 
         }
         if (!done) st_stream(dst + g * kChunk, Vec<T>::pack(d));
       }
-      it.next(rb.ring, rb.full, rb.empty);
+      it.next();
     }
   }
 }
@@ -388,8 +385,8 @@ __device__ __forceinline__ void phase2_row(const Slice& sl, RingIt it, const Rin
     __syncwarp();
     if (lane == 0) {
       for (int g = 0; g < ng; ++g) {
-        arrive_u32(rel.empty);
-        rel.next(rb.ring, rb.full, rb.empty);
+        arrive_u32(rel.empty(rb));
+        rel.next();
       }
     }
     vbase += ng * kConsumers;
@@ -401,7 +398,7 @@ template <typename T>
 __device__ __forceinline__ void phase1_range(Acc2& acc, RingIt row_it, const RingBase& rb,
                                              const Slice& sl, int g0, int g1, int tid) {
   RingIt it = row_it;
-  for (int c = 0; c < g0 * kGroup; ++c) it.next(rb.ring, rb.full, rb.empty);
+  for (int c = 0; c < g0 * kGroup; ++c) it.next();
   int vbase = sl.v0 + g0 * kGroup * kConsumers;
   for (int gi = g0; gi < g1; ++gi) {
     const int ng = min(kGroup, sl.nchunk - gi * kGroup);
@@ -421,9 +418,10 @@ __device__ __forceinline__ Acc2 acc_init() {
   return Acc2{kNegInf, pk2(0.f, 0.f), pk2(0.f, 0.f), pk2(0.f, 0.f)};  // nm2 set on first use
 }
 
+// waits of the producer / epilogue warps back off with nanosleep so their
+// polling does not steal issue slots from the consumer warps on the same SMSP
 __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
-  while (!mbar_try_wait_sleep(bar, parity)) {
-  }
+  while (!mbar_try_wait(bar, parity)) __nanosleep(64);
 }
 
 template <typename T, int CL>
@@ -487,7 +485,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         const int64_t r = cid + int64_t(i) * ncl;
         if (r < NR) prefetch_l2(slice_ptr(r), slice_bytes);
       }
-      RingIt it = {rb.ring, rb.full, rb.empty, 0u};
+      RingIt it = {0u};
       for (int64_t row = cid; row < NR; row += ncl) {
         if (prefetch_rows > 0) {
           const int64_t r = row + int64_t(prefetch_rows) * ncl;
@@ -495,19 +493,19 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         }
         const char* src = slice_ptr(row);
         for (int j = 0; j < sl.nchunk; ++j) {
-          mbar_wait_u32(it.empty, it.phase ^ 1u);
+          mbar_wait_u32(it.empty(rb), it.phase() ^ 1u);
           const uint32_t off = uint32_t(j) * kChunk;
           const uint32_t bytes = min(uint32_t(kChunk), slice_bytes - off);
           asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
-                           it.full),
+                           it.full(rb)),
                        "r"(bytes)
                        : "memory");
           asm volatile(
               "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-              " [%0], [%1], %2, [%3], %4;" ::"r"(it.addr),
-              "l"(src + off), "r"(bytes), "r"(it.full), "l"(pol)
+              " [%0], [%1], %2, [%3], %4;" ::"r"(it.addr(rb)),
+              "l"(src + off), "r"(bytes), "r"(it.full(rb)), "l"(pol)
               : "memory");
-          it.next(rb.ring, rb.full, rb.empty);
+          it.next();
         }
       }
     }
@@ -520,7 +518,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     double sd[15];
 #pragma unroll
     for (int i = 0; i < 15; ++i) sd[i] = 0.0;
-    RingIt pos0 = {rb.ring, rb.full, rb.empty, 0u};
+    RingIt pos0 = {0u};
     int64_t k = 0;
     for (int64_t row = cid; row < NR; row += ncl, ++k) {
       const int par = int(k & 1);
@@ -538,9 +536,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       float czy = kNegInf;
       if (vy >= sl.v0 && vy < sl.v1) {
         const int off = vy - sl.v0;
-        uint32_t addr = pos0.addr + uint32_t(off / kConsumers) * kChunk;
-        if (addr >= rb.ring + kSlots * kChunk) addr -= kSlots * kChunk;
-        czy = Pk<T>::elem(lds128(addr + uint32_t(off % kConsumers) * 16), ye);
+        RingIt at = pos0;
+        at.advance(off / kConsumers);
+        czy = Pk<T>::elem(lds128(at.addr(rb) + uint32_t(off % kConsumers) * 16), ye);
       }
       Online tot = cta;
       float tzy = czy;
@@ -603,7 +601,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
           sd[14] += 1.0;
         }
       }
-      for (int j = 0; j < sl.nchunk; ++j) pos0.next(rb.ring, rb.full, rb.empty);
+      pos0.advance(sl.nchunk);
     }
     // rank 0 of each cluster accumulated its rows; other ranks store zeros
     if (lane == 0) {
@@ -627,7 +625,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     }
   } else {
     // ===================== consumer warps =====================
-    RingIt pos0 = {rb.ring, rb.full, rb.empty, 0u};  // the current row's first chunk
+    RingIt pos0 = {0u};  // the current row's first chunk
     Acc2 acc = acc_init();
     if (cid < NR) phase1_range<T>(acc, pos0, rb, sl, 0, pre, tid);  // first row's prefix
     int y_cur = (cid < NR) ? __ldg(&meta[cid].y) : 0;
@@ -655,7 +653,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       }
       // ---------------- phase 1 prefix of the next row (hides the epilogue) ----------
       RingIt npos = pos0;
-      for (int j = 0; j < sl.nchunk; ++j) npos.next(rb.ring, rb.full, rb.empty);
+      npos.advance(sl.nchunk);
       acc = acc_init();
       if (nrow < NR) phase1_range<T>(acc, npos, rb, sl, 0, pre, tid);
 
