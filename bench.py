@@ -235,6 +235,7 @@ def main():
 
     from paper_2505_17826_b200 import RFTLoss, RFTLossConfig, logprob_fwd, pack_arrays
     from paper_2505_17826_b200 import _native as N
+    from paper_2505_17826_b200.distributed import allreduce_stats
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -289,9 +290,7 @@ def main():
             outs[m] = loss(batches[m], dlogits=dz, n_tok_global=n_tok_g, n_seq_global=n_seq_g,
                            out=outs[m])
         st = torch.stack([o.stats for o in outs]).sum(0)
-        if world > 1:
-            dist.all_reduce(st)
-        return st
+        return allreduce_stats(st)
 
     for _ in range(args.warmup):
         st = step()
@@ -324,9 +323,7 @@ def main():
             k += 1
             outs[m] = loss(batches[m], dlogits=dz, n_tok_global=n_tok_g, n_seq_global=n_seq_g,
                            out=outs[m])
-        st = torch.stack([o.stats for o in outs]).sum(0)
-        if world > 1:
-            dist.all_reduce(st)
+        st = allreduce_stats(torch.stack([o.stats for o in outs]).sum(0))
     t_end.record()
     torch.cuda.synchronize()
     if world > 1:
@@ -346,13 +343,16 @@ def main():
     peak, peak_src = peaks()
     f_ms = statistics.mean(fused_ms)
     achieved = mb_rows * ALGO_BYTES_PER_ROW / (f_ms / 1000.0) / 1e9
+    # DRAM bytes per launch from the committed `ncu --set full` capture of the
+    # same kernel at this vocabulary, scaled from its row count to this launch's
+    # (the kernel streams rows independently, so bytes / row is size-invariant)
     traffic = None
     tf = ROOT / "profiles" / "fused_traffic.json"
     if tf.exists():
         try:
             d = json.loads(tf.read_text())
-            if int(d.get("rows", 0)) == mb_rows and int(d.get("vocab", 0)) == V:
-                traffic = float(d["dram_bytes_per_launch"])
+            if int(d.get("vocab", 0)) == V:
+                traffic = float(d["dram_bytes_per_row"]) * mb_rows
         except Exception:
             traffic = None
 
