@@ -42,10 +42,11 @@ constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kEpilogueWarp = kConsumerWarps;
 constexpr int kProducerWarp = kConsumerWarps + 1;
 constexpr int kFusedThreads = kConsumers + 64;
-constexpr int kChunk = kConsumers * 16;  // 7168 bytes: one 16-byte vector per consumer thread
-constexpr int kGroup = 4;                // chunks consumed per step
-constexpr int kSlots = 32;               // ring slots: 224 KB of the 227 KB opt-in SMEM
-constexpr int kMaxPrefixGroups = 2;      // next-row phase-1 steps run before this row's phase 2
+constexpr int kVecPerThread = 4;                  // 16-byte vectors per consumer thread per chunk
+constexpr int kVecPerChunk = kConsumers * kVecPerThread;
+constexpr int kChunk = kVecPerChunk * 16;         // 28 KB per TMA bulk copy / ring slot
+constexpr int kSlots = 8;                          // ring: 224 KB of the 227 KB opt-in SMEM
+constexpr int kMaxPrefixChunks = 2;  // next-row phase-1 chunks run before this row's phase 2
 constexpr uint32_t kPrefetchPiece = 65536;  // bytes per L2 prefetch instruction
 
 struct FusedSmemTail {
@@ -174,18 +175,18 @@ struct Pk<float> {
   }
 };
 
-// max over kGroup vectors
+// max over kVecPerThread vectors
 template <typename T>
-__device__ __forceinline__ float group_max(const uint4 (&u)[kGroup]) {
+__device__ __forceinline__ float group_max(const uint4 (&u)[kVecPerThread]) {
   if constexpr (sizeof(T) == 2) {
     uint32_t m = Pk<bf16_t>::pmax(u[0]);
 #pragma unroll
-    for (int g = 1; g < kGroup; ++g) m = bmax2(m, Pk<bf16_t>::pmax(u[g]));
+    for (int g = 1; g < kVecPerThread; ++g) m = bmax2(m, Pk<bf16_t>::pmax(u[g]));
     return Pk<bf16_t>::hmax(m);
   } else {
     float m = Pk<float>::vmax(u[0]);
 #pragma unroll
-    for (int g = 1; g < kGroup; ++g) m = fmaxf(m, Pk<float>::vmax(u[g]));
+    for (int g = 1; g < kVecPerThread; ++g) m = fmaxf(m, Pk<float>::vmax(u[g]));
     return m;
   }
 }
@@ -298,119 +299,106 @@ struct Slice {
   int v0, v1, nchunk, tail_vec, tail_valid;
 };
 
-// ---- phase 1: one consumer step over kGroup chunks --------------------------
-// kPartial: the step may run past the slice end (lanes there use a neutral
+// ---- phase 1: one chunk (kVecPerThread vectors per consumer thread) ---------
+// kPartial: the chunk may run past the slice end (lanes there use a neutral
 // -1e30 vector and skip the sums, but still vote, so the lazy-rescale test is
-// always a full-warp vote).  kMaskTail: the step holds the tail padding.
+// always a full-warp vote).  kMaskTail: the chunk holds the tail padding.
 template <typename T, bool kPartial, bool kMaskTail>
-__device__ __forceinline__ void phase1_step(Acc2& acc, RingIt& it, const RingBase& rb, int ng,
-                                            int vbase, const Slice& sl, int tid) {
-  uint4 u[kGroup];
-  bool valid[kGroup];
+__device__ __forceinline__ void phase1_chunk(Acc2& acc, RingIt& it, const RingBase& rb,
+                                             int vbase, const Slice& sl, int tid) {
+  uint4 u[kVecPerThread];
+  bool valid[kVecPerThread];
+  wait_full(it.full(rb), it.phase());
+  const uint32_t a = it.addr(rb) + tid * 16;
 #pragma unroll
-  for (int g = 0; g < kGroup; ++g) {
-    if (!kPartial || g < ng) {
-      wait_full(it.full(rb), it.phase());
-      const int vec = vbase + g * kConsumers + tid;
-      valid[g] = !kPartial || vec < sl.v1;
-      u[g] = valid[g] ? lds128(it.addr(rb) + tid * 16) : Pk<T>::neutral();
-      Pk<T>::clamp(u[g]);
-      if (kMaskTail && vec == sl.tail_vec) Pk<T>::mask_from(u[g], sl.tail_valid);
-      it.next();
-    } else {
-      valid[g] = false;
-      u[g] = Pk<T>::neutral();
-    }
+  for (int g = 0; g < kVecPerThread; ++g) {
+    const int vec = vbase + g * kConsumers + tid;
+    valid[g] = !kPartial || vec < sl.v1;
+    u[g] = valid[g] ? lds128(a + g * kConsumers * 16) : Pk<T>::neutral();
+    Pk<T>::clamp(u[g]);
+    if (kMaskTail && vec == sl.tail_vec) Pk<T>::mask_from(u[g], sl.tail_valid);
   }
+  it.next();
   const float vmax = group_max<T>(u);
   if (__any_sync(0xffffffffu, vmax > acc.m + kSlack)) rescale(acc, vmax);
 #pragma unroll
-  for (int g = 0; g < kGroup; ++g)
+  for (int g = 0; g < kVecPerThread; ++g)
     if (!kPartial || valid[g]) accumulate<T>(acc, u[g]);
 }
 
-// ---- phase 2: dz for one consumer step ---------------------------------------
+// ---- phase 2: dz for one chunk ------------------------------------------------
 template <typename T, bool kHasH, bool kCheck>
-__device__ __forceinline__ void phase2_step(RingIt& it, const RingBase& rb, int ng, int vbase,
-                                            const Slice& sl, char* dzrow, int vy, int ye,
-                                            float s_t, uint64_t nl2, uint64_t av2, uint64_t hz2,
-                                            int tid) {
+__device__ __forceinline__ void phase2_chunk(const RingIt& it, const RingBase& rb, int vbase,
+                                             const Slice& sl, char* dzrow, int vy, int ye,
+                                             float s_t, uint64_t nl2, uint64_t av2, uint64_t hz2,
+                                             int tid) {
   constexpr int EPV = Vec<T>::N;
   char* dst = dzrow + int64_t(vbase + tid) * 16;
+  const uint32_t a = it.addr(rb) + tid * 16;
 #pragma unroll
-  for (int g = 0; g < kGroup; ++g) {
-    if (!kCheck || g < ng) {
-      const int vec = vbase + g * kConsumers + tid;
-      if (!kCheck || vec < sl.v1) {
-        float d[EPV];
-        dz_vec<T, kHasH>(lds128(it.addr(rb) + tid * 16), d, nl2, av2, hz2);
-        bool done = false;
-        if (kCheck) {
-          if (vec == vy) {
+  for (int g = 0; g < kVecPerThread; ++g) {
+    const int vec = vbase + g * kConsumers + tid;
+    if (!kCheck || vec < sl.v1) {
+      float d[EPV];
+      dz_vec<T, kHasH>(lds128(a + g * kConsumers * 16), d, nl2, av2, hz2);
+      bool done = false;
+      if (kCheck) {
+        if (vec == vy) {
 #pragma unroll
-            for (int e = 0; e < EPV; ++e)
-              if (e == ye) d[e] -= s_t;
-          }
-          if (vec == sl.tail_vec) {
-#pragma unroll
-            for (int e = 0; e < EPV; ++e)
-              if (e < sl.tail_valid) Vec<T>::store1(dzrow, int64_t(vec) * EPV + e, d[e]);
-            done = true;
-          }
+          for (int e = 0; e < EPV; ++e)
+            if (e == ye) d[e] -= s_t;
         }
-        if (!done) st_stream(dst + g * kChunk, Vec<T>::pack(d));
+        if (vec == sl.tail_vec) {
+#pragma unroll
+          for (int e = 0; e < EPV; ++e)
+            if (e < sl.tail_valid) Vec<T>::store1(dzrow, int64_t(vec) * EPV + e, d[e]);
+          done = true;
+        }
       }
-      it.next();
+      if (!done) st_stream(dst + g * kConsumers * 16, Vec<T>::pack(d));
     }
   }
 }
 
-// phase 2 over one row: kGroup-chunk steps; the step holding the target logit
-// or tail padding, and the last partial step, take the checked variant.
+// phase 2 over one row; the chunk holding the target logit or tail padding, and
+// the last partial chunk, take the checked variant.
 template <typename T, bool kHasH>
 __device__ __forceinline__ void phase2_row(const Slice& sl, RingIt it, const RingBase& rb,
                                            char* dzrow, int vy, int ye, float s_t, uint64_t nl2,
                                            uint64_t av2, uint64_t hz2, int tid, int lane) {
   int vbase = sl.v0;
-  for (int j = 0; j < sl.nchunk; j += kGroup) {
-    const int ng = min(kGroup, sl.nchunk - j);
-    const int gend = vbase + kGroup * kConsumers;
-    const bool check = (gend > sl.v1) || (sl.tail_vec >= vbase && sl.tail_vec < gend) ||
-                       (vy >= vbase && vy < gend);
-    RingIt rel = it;
+  for (int j = 0; j < sl.nchunk; ++j) {
+    const int vend = vbase + kVecPerChunk;
+    const bool check = (vend > sl.v1) || (sl.tail_vec >= vbase && sl.tail_vec < vend) ||
+                       (vy >= vbase && vy < vend);
     if (check)
-      phase2_step<T, kHasH, true>(it, rb, ng, vbase, sl, dzrow, vy, ye, s_t, nl2, av2, hz2, tid);
+      phase2_chunk<T, kHasH, true>(it, rb, vbase, sl, dzrow, vy, ye, s_t, nl2, av2, hz2, tid);
     else
-      phase2_step<T, kHasH, false>(it, rb, ng, vbase, sl, dzrow, vy, ye, s_t, nl2, av2, hz2, tid);
+      phase2_chunk<T, kHasH, false>(it, rb, vbase, sl, dzrow, vy, ye, s_t, nl2, av2, hz2, tid);
     __syncwarp();
-    if (lane == 0) {
-      for (int g = 0; g < ng; ++g) {
-        arrive_u32(rel.empty(rb));
-        rel.next();
-      }
-    }
-    vbase += ng * kConsumers;
+    if (lane == 0) arrive_u32(it.empty(rb));
+    it.next();
+    vbase = vend;
   }
 }
 
-// phase 1 over steps [g0, g1) of a row whose first chunk is at `row_it`
+// phase 1 over chunks [c0, c1) of a row whose first chunk is at `row_it`
 template <typename T>
 __device__ __forceinline__ void phase1_range(Acc2& acc, RingIt row_it, const RingBase& rb,
-                                             const Slice& sl, int g0, int g1, int tid) {
+                                             const Slice& sl, int c0, int c1, int tid) {
   RingIt it = row_it;
-  for (int c = 0; c < g0 * kGroup; ++c) it.next();
-  int vbase = sl.v0 + g0 * kGroup * kConsumers;
-  for (int gi = g0; gi < g1; ++gi) {
-    const int ng = min(kGroup, sl.nchunk - gi * kGroup);
-    const int gend = vbase + kGroup * kConsumers;
-    const bool has_tail = sl.tail_vec >= vbase && sl.tail_vec < gend;
-    if (gend <= sl.v1 && !has_tail)
-      phase1_step<T, false, false>(acc, it, rb, ng, vbase, sl, tid);
+  it.advance(c0);
+  int vbase = sl.v0 + c0 * kVecPerChunk;
+  for (int c = c0; c < c1; ++c) {
+    const int vend = vbase + kVecPerChunk;
+    const bool has_tail = sl.tail_vec >= vbase && sl.tail_vec < vend;
+    if (vend <= sl.v1 && !has_tail)
+      phase1_chunk<T, false, false>(acc, it, rb, vbase, sl, tid);
     else if (!has_tail)
-      phase1_step<T, true, false>(acc, it, rb, ng, vbase, sl, tid);
+      phase1_chunk<T, true, false>(acc, it, rb, vbase, sl, tid);
     else
-      phase1_step<T, true, true>(acc, it, rb, ng, vbase, sl, tid);
-    vbase += ng * kConsumers;
+      phase1_chunk<T, true, true>(acc, it, rb, vbase, sl, tid);
+    vbase = vend;
   }
 }
 
@@ -451,9 +439,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   sl.nchunk = int((slice_bytes + kChunk - 1) / kChunk);
   sl.tail_vec = (V % EPV) ? nvec - 1 : -1;  // global vector holding columns >= V
   sl.tail_valid = V - (nvec - 1) * EPV;
-  const int nsteps = (sl.nchunk + kGroup - 1) / kGroup;
-  // next-row phase-1 steps that fit in the ring beside this row's slice
-  const int pre = min(min(kMaxPrefixGroups, (kSlots - sl.nchunk) / kGroup), nsteps);
+  // next-row phase-1 chunks that fit in the ring beside this row's slice
+  const int pre = min(min(kMaxPrefixChunks, kSlots - sl.nchunk), sl.nchunk);
 
   if (tid == 0) {
     for (int i = 0; i < kSlots; ++i) {
@@ -537,8 +524,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       if (vy >= sl.v0 && vy < sl.v1) {
         const int off = vy - sl.v0;
         RingIt at = pos0;
-        at.advance(off / kConsumers);
-        czy = Pk<T>::elem(lds128(at.addr(rb) + uint32_t(off % kConsumers) * 16), ye);
+        at.advance(off / kVecPerChunk);
+        czy = Pk<T>::elem(lds128(at.addr(rb) + uint32_t(off % kVecPerChunk) * 16), ye);
       }
       Online tot = cta;
       float tzy = czy;
@@ -639,7 +626,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       const int par = int(k & 1);
 
       // ---------------- phase 1 (rest of the row) ----------------
-      phase1_range<T>(acc, pos0, rb, sl, pre, nsteps, tid);
+      phase1_range<T>(acc, pos0, rb, sl, pre, sl.nchunk, tid);
       Online o;
       {
         float s0, s1, t0, t1;
