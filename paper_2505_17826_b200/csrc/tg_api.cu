@@ -31,6 +31,7 @@ cudaError_t launch_fused(const KParams& P, const void* meta, int cl, int n_slots
                          int prefetch_rows,
                          cudaStream_t stream);
 int fused_chunk_bytes();
+int fused_max_clusters(int dtype, int cl);
 int fused_max_slots();
 size_t rowmeta_bytes();
 void launch_fwd(const KParams& P, bool anchor, bool vec, int grid, cudaStream_t st);
@@ -289,16 +290,20 @@ FusedPlan fused_plan(const TgBatch* b, const TgOut* o) {
   const size_t tail = fused_smem_bytes(0);
   int n_slots = int((size_t(d.smem_optin) - tail) / size_t(fused_chunk_bytes()));
   if (n_slots > fused_max_slots()) n_slots = fused_max_slots();
-  if (n_slots < fused_max_slots()) return fp;  // the kernel's ring size is a compile-time 30
-  for (int cl = 1; cl <= 4; cl *= 2) {
-    if (force_cl && cl != force_cl) continue;
+  if (n_slots < fused_max_slots()) return fp;  // the kernel's ring size is compile-time
+  static const int kOrder[4] = {1, 2, 4, 3};
+  for (int oi = 0; oi < 4; ++oi) {
+    const int cl = kOrder[oi];
+    if (force_cl ? cl != force_cl : cl == 3) continue;  // CL = 3 only on request
     const int64_t slice_vec = (nvec + cl - 1) / cl;
     const int64_t nchunk = (slice_vec * 16 + fused_chunk_bytes() - 1) / fused_chunk_bytes();
     if (nchunk + 2 <= n_slots) {
+      // persistent grid: as many clusters as can be co-resident, at most one per row
+      int64_t clusters_max = fused_max_clusters(b->dtype, cl);
+      if (clusters_max <= 0) clusters_max = d.sms / cl;
+      const int64_t clusters = b->n_rows < clusters_max ? b->n_rows : clusters_max;
       fp.cl = cl;
       fp.n_slots = n_slots;
-      const int64_t clusters_max = d.sms / cl;
-      const int64_t clusters = b->n_rows < clusters_max ? b->n_rows : clusters_max;
       fp.n_ctas = int(clusters * cl);
       return fp;
     }

@@ -46,7 +46,7 @@ constexpr int kVecPerThread = 4;                  // 16-byte vectors per consume
 constexpr int kVecPerChunk = kConsumers * kVecPerThread;
 constexpr int kChunk = kVecPerChunk * 16;         // 28 KB per TMA bulk copy / ring slot
 constexpr int kSlots = 8;                          // ring: 224 KB of the 227 KB opt-in SMEM
-constexpr int kMaxPrefixChunks = 2;  // next-row phase-1 chunks run before this row's phase 2
+constexpr int kMaxPrefixChunks = 8;  // next-row phase-1 chunks run before this row's phase 2
 constexpr uint32_t kPrefetchPiece = 65536;  // bytes per L2 prefetch instruction
 
 struct FusedSmemTail {
@@ -697,13 +697,54 @@ cudaError_t launch_fused(const KParams& P, const void* meta, int cl, int n_slots
   if (P.dtype == TG_DTYPE_BF16) {
     if (cl == 1) return launch_fused_t<bf16_t, 1>(P, m, n_ctas, prefetch_rows, stream);
     if (cl == 2) return launch_fused_t<bf16_t, 2>(P, m, n_ctas, prefetch_rows, stream);
+    if (cl == 3) return launch_fused_t<bf16_t, 3>(P, m, n_ctas, prefetch_rows, stream);
     if (cl == 4) return launch_fused_t<bf16_t, 4>(P, m, n_ctas, prefetch_rows, stream);
   } else {
     if (cl == 1) return launch_fused_t<float, 1>(P, m, n_ctas, prefetch_rows, stream);
     if (cl == 2) return launch_fused_t<float, 2>(P, m, n_ctas, prefetch_rows, stream);
+    if (cl == 3) return launch_fused_t<float, 3>(P, m, n_ctas, prefetch_rows, stream);
     if (cl == 4) return launch_fused_t<float, 4>(P, m, n_ctas, prefetch_rows, stream);
   }
   return cudaErrorInvalidValue;
+}
+
+// Clusters of `cl` fused CTAs that can be co-resident (the kernel is persistent:
+// a grid larger than this would run a second wave).  0 on error.
+template <typename T, int CL>
+static int max_clusters_t() {
+  const size_t smem = fused_smem_bytes(kSlots);
+  if (cudaFuncSetAttribute(k_fused_tma<T, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(smem)) != cudaSuccess)
+    return 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CL);
+  cfg.blockDim = dim3(kFusedThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, k_fused_tma<T, CL>, &cfg) != cudaSuccess) return 0;
+  return n;
+}
+
+int fused_max_clusters(int dtype, int cl) {
+  if (dtype == TG_DTYPE_BF16) {
+    if (cl == 1) return max_clusters_t<bf16_t, 1>();
+    if (cl == 2) return max_clusters_t<bf16_t, 2>();
+    if (cl == 3) return max_clusters_t<bf16_t, 3>();
+    if (cl == 4) return max_clusters_t<bf16_t, 4>();
+  } else {
+    if (cl == 1) return max_clusters_t<float, 1>();
+    if (cl == 2) return max_clusters_t<float, 2>();
+    if (cl == 3) return max_clusters_t<float, 3>();
+    if (cl == 4) return max_clusters_t<float, 4>();
+  }
+  return 0;
 }
 
 int fused_chunk_bytes() { return kChunk; }
