@@ -10,27 +10,31 @@
 //  * A thread-block cluster of CL CTAs (CL = 1 for V <= ~110k bf16, 2 for
 //    Qwen's 151,936) owns one row at a time; CTA rank r owns a contiguous
 //    column slice of the row.  The slice never leaves the SM: a producer warp
-//    streams it into a 30-slot shared-memory ring with 1-D bulk TMA
-//    (cp.async.bulk ... mbarrier::complete_tx), one 7.5 KB chunk per slot with
-//    a full / empty mbarrier pair, and prefetches upcoming rows' slices into
-//    L2 (cp.async.bulk.prefetch.L2) -- the ring holds ~1.5 slices.
-//  * 15 consumer warps, one 16-byte vector per thread per chunk, consume
-//    kGroup chunks per step.  Phase 1 (as chunks land): online max / sum-exp /
-//    sum p*z in packed fp32x2 arithmetic (FFMA2 / FADD2) with MUFU ex2; -inf
-//    logits are clamped to -1e30 with packed bf16x2 max; the running max is
-//    updated lazily behind a warp vote.  One named barrier collects per-warp
-//    partials; warp 0 reduces them, reads the target logit from the resident
-//    chunk, exchanges the CTA partial with its cluster peers through DSMEM
-//    (st.async completing tx bytes on the peer's mbarrier; rank-order merge =>
-//    bit-identical lse on every CTA), evaluates the registry epilogue
-//    (tg_rowcoef.cuh) and broadcasts (a, h, lse, s) through a second barrier.
+//    streams it into an 8-slot shared-memory ring (28 KB chunks, 224 KB) with
+//    1-D bulk TMA (cp.async.bulk ... mbarrier::complete_tx), a full / empty
+//    mbarrier pair per slot, and prefetches upcoming rows' slices into L2
+//    (cp.async.bulk.prefetch.L2).
+//  * 14 consumer warps, four 16-byte vectors per thread per chunk.  Phase 1
+//    (as chunks land): online max / sum-exp / sum p*z in packed fp32x2
+//    arithmetic (FFMA2 / FADD2) with MUFU ex2; -inf logits are clamped to
+//    -1e30 with packed bf16x2 max; the running max is updated lazily behind a
+//    warp vote.  Each warp posts its partial and arrives on an mbarrier.
+//  * A dedicated epilogue warp merges the partials, reads the target logit
+//    from the resident chunk, exchanges the CTA partial with its cluster peers
+//    through DSMEM (st.async completing tx bytes on the peer's mbarrier;
+//    rank-order merge => bit-identical lse on every CTA), evaluates the
+//    registry epilogue (tg_rowcoef.cuh) and broadcasts (a, h, lse, s) through
+//    a second mbarrier.  Meanwhile the consumers already run phase 1 of the
+//    next row on the ring's free slots, so the epilogue is off their path.
 //  * Phase 2 re-reads the resident chunks from SMEM and writes
 //    dz = p (s + h((z - lse) + H)) - s[v = y] with 128-bit streaming stores,
 //    releasing each slot to the producer, which refills it with the next row.
 //  * Persistent grid: one CTA per SM (16 warps -> 128 registers / thread),
-//    clusters stride over rows.
+//    as many clusters as can be co-resident, striding over rows.
 #include "tg_common.cuh"
 #include "tg_rowcoef.cuh"
+
+#include <mutex>
 
 namespace tg {
 
@@ -732,7 +736,7 @@ static int max_clusters_t() {
   return n;
 }
 
-int fused_max_clusters(int dtype, int cl) {
+static int fused_max_clusters_uncached(int dtype, int cl) {
   if (dtype == TG_DTYPE_BF16) {
     if (cl == 1) return max_clusters_t<bf16_t, 1>();
     if (cl == 2) return max_clusters_t<bf16_t, 2>();
@@ -745,6 +749,23 @@ int fused_max_clusters(int dtype, int cl) {
     if (cl == 4) return max_clusters_t<float, 4>();
   }
   return 0;
+}
+
+// cached per (device, dtype, cluster size): the occupancy query is slow
+int fused_max_clusters(int dtype, int cl) {
+  static std::mutex mu;
+  static int cache[64][2][5];
+  static bool have[64][2][5] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || cl < 1 || cl > 4) return fused_max_clusters_uncached(dtype, cl);
+  const int di = dtype == TG_DTYPE_BF16 ? 0 : 1;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!have[dev][di][cl]) {
+    cache[dev][di][cl] = fused_max_clusters_uncached(dtype, cl);
+    have[dev][di][cl] = true;
+  }
+  return cache[dev][di][cl];
 }
 
 int fused_chunk_bytes() { return kChunk; }
