@@ -267,7 +267,7 @@ struct FusedPlan {
 };
 
 // Tuning overrides for measurement (A/B on the GPU without rebuilding):
-// TG_FUSED_CL=1|2|4 forces the cluster size, TG_PREFETCH_ROWS=n the L2
+// TG_FUSED_CL=1|2|3|4 forces the cluster size, TG_PREFETCH_ROWS=n the L2
 // look-ahead depth (rows per cluster; 0 disables).
 int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
@@ -276,7 +276,9 @@ int env_int(const char* name, int dflt) {
 
 FusedPlan fused_plan(const TgBatch* b, const TgOut* o) {
   FusedPlan fp;
-  fp.prefetch_rows = env_int("TG_PREFETCH_ROWS", 1);
+  // L2 look-ahead measured neutral at 1 row and harmful beyond (extra DRAM
+  // reads from prefetched lines evicted before use): off by default
+  fp.prefetch_rows = env_int("TG_PREFETCH_ROWS", 0);
   const int force_cl = env_int("TG_FUSED_CL", 0);
   const int esz = esz_of(b->dtype);
   const int epv = 16 / esz;
