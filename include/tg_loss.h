@@ -203,6 +203,23 @@ const char* tg_strerror(int code);
 const char* tg_last_error(void);
 int tg_abi_version(void);
 
+/* ---- on-device packer ----------------------------------------------------- */
+
+/* Padded token batch -> packed rows, on the device.
+   mask[B*L] marks trainable TARGET positions; row r for target position
+   (b, l), l >= 1, gets row_index[r] = b*L + l - 1 (HF shift into the
+   [B*L, V] logits), target[r] = ids[b*L + l] and, when the dense inputs are
+   given, old_out[r] / ref_out[r] from old_dense / ref_dense[b*L + l].  Rows
+   keep (b, l) order; seq_offsets[B+1] and *n_rows (device int64) are written.
+   Rows beyond `capacity` are counted but not written.  Workspace: 4*B bytes.
+   Replaces the per-token Python assembly of Experience / TaskGroup records
+   (records.py:21-131, workflows.py:128-183). */
+int tg_pack_rows(const uint8_t* mask, const void* ids, int ids_is_int64, int32_t B, int32_t L,
+                 const float* old_dense, const float* ref_dense, int64_t* row_index,
+                 int32_t* target, float* old_out, float* ref_out, int64_t capacity,
+                 int32_t* seq_offsets, int64_t* n_rows, void* workspace,
+                 size_t workspace_bytes, void* stream);
+
 /* ---- host helpers (no device access) ------------------------------------ */
 
 /* Toy-table policy adapter (policy.py:152-161, 181-191; encoding.py:19-35):

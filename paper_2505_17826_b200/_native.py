@@ -71,7 +71,7 @@ class TgOut(ctypes.Structure):
 EXPORTED = [
     "tg_workspace_size", "tg_loss_fwd_bwd", "tg_logprob_fwd", "tg_route", "tg_strerror",
     "tg_last_error", "tg_abi_version", "tg_scored_states", "tg_group_by_task",
-    "tg_set_timing_events", "tg_launch_count",
+    "tg_set_timing_events", "tg_launch_count", "tg_pack_rows",
 ]
 
 _lib = None
@@ -124,6 +124,10 @@ def lib() -> ctypes.CDLL:
     L.tg_set_timing_events.argtypes = [c_void_p, c_void_p]
     L.tg_launch_count.restype = c_int64
     L.tg_launch_count.argtypes = []
+    L.tg_pack_rows.restype = c_int
+    L.tg_pack_rows.argtypes = [c_void_p, c_void_p, c_int, c_int32, c_int32, c_void_p, c_void_p,
+                               c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p,
+                               c_void_p, c_void_p, c_size_t, c_void_p]
     if L.tg_abi_version() != 1:
         raise RuntimeError("libtg_loss ABI mismatch")
     _lib = L

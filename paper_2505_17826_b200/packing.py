@@ -207,3 +207,67 @@ def group_by_task(task_keys: Sequence[int], ready: Sequence[bool], group_size: i
     if k < 0:
         raise ValueError("invalid group_by_task arguments")
     return out[: k * group_size].reshape(k, group_size).tolist()
+
+
+def pack_token_batch(logits: torch.Tensor, input_ids: torch.Tensor, loss_mask: torch.Tensor,
+                     rewards, group_sizes, *, old_logprobs: Optional[torch.Tensor] = None,
+                     ref_logprobs: Optional[torch.Tensor] = None, seq_kind=None,
+                     seq_ref_lp=None, advantage=None) -> PackedBatch:
+    """LLM-layout batch already on the device -> PackedBatch, packed on the GPU
+    (tg_pack_rows): `logits` [B, L, V] (or [B*L, V]) is read in place through
+    row_index with the HF shift (logits at l - 1 score input_ids[l]);
+    `loss_mask` [B, L] marks trainable target positions; `old_logprobs` /
+    `ref_logprobs` are dense [B, L] aligned with `input_ids`.  One 8-byte + 4B
+    byte device->host read sizes the batch."""
+    L_ = N.lib()
+    if input_ids.dim() != 2 or loss_mask.shape != input_ids.shape:
+        raise ValueError("input_ids and loss_mask must be [B, L]")
+    B, Lx = input_ids.shape
+    dev = input_ids.device
+    V = int(logits.shape[-1])
+    flat = logits.reshape(B * Lx, V)
+    if flat.data_ptr() != logits.data_ptr():
+        raise ValueError("logits must be viewable as [B*L, V] without a copy")
+    ids = input_ids.contiguous()
+    if ids.dtype not in (torch.int32, torch.int64):
+        raise ValueError("input_ids must be int32 or int64")
+    mask = loss_mask.to(torch.uint8).contiguous()
+    cap = B * Lx
+    row_index = torch.empty(cap, dtype=torch.int64, device=dev)
+    target = torch.empty(cap, dtype=torch.int32, device=dev)
+    old_out = torch.empty(cap, dtype=torch.float32, device=dev) if old_logprobs is not None else None
+    ref_out = torch.empty(cap, dtype=torch.float32, device=dev) if ref_logprobs is not None else None
+    old_in = None if old_logprobs is None else old_logprobs.float().contiguous()
+    ref_in = None if ref_logprobs is None else ref_logprobs.float().contiguous()
+    seq_off = torch.empty(B + 1, dtype=torch.int32, device=dev)
+    n_rows = torch.empty(1, dtype=torch.int64, device=dev)
+    ws = torch.empty(max(4 * B, 4), dtype=torch.uint8, device=dev)
+
+    def p(t):
+        return None if t is None else t.data_ptr()
+
+    with torch.cuda.device(dev):
+        N.check(L_.tg_pack_rows(mask.data_ptr(), ids.data_ptr(), int(ids.dtype == torch.int64),
+                                B, Lx, p(old_in), p(ref_in), row_index.data_ptr(),
+                                target.data_ptr(), p(old_out), p(ref_out), cap, seq_off.data_ptr(),
+                                n_rows.data_ptr(), ws.data_ptr(), ws.numel(),
+                                torch.cuda.current_stream(dev).cuda_stream))
+    so = seq_off.cpu().numpy().astype(np.int64)
+    T = int(so[-1])
+    seq_lengths = np.diff(so)
+    group_sizes = np.asarray(group_sizes, np.int64)
+    go = offsets_from_lengths(group_sizes)
+    if go[-1] != B:
+        raise AlgorithmError(f"group sizes sum to {go[-1]} but there are {B} sequences")
+    kind = None if seq_kind is None else np.asarray(seq_kind, dtype=np.uint8)
+    rl = np.ones(B, bool) if kind is None else kind == 0
+    return PackedBatch(
+        logits=flat, target=target[:T], seq_offsets=seq_off, group_offsets=_i32(go, dev),
+        reward=_f32(rewards, dev) if not torch.is_tensor(rewards) else rewards.float(),
+        old_lp=None if old_out is None else old_out[:T],
+        ref_lp=None if ref_out is None else ref_out[:T], seq_ref_lp=_f32(seq_ref_lp, dev),
+        advantage=_f32(advantage, dev),
+        seq_kind=None if kind is None else torch.as_tensor(kind, device=dev),
+        row_index=row_index[:T], vocab=V, n_rows=T, n_seqs=B, n_groups=len(group_sizes),
+        n_rl_rows=int(seq_lengths[rl].sum()), n_rl_seqs=int(rl.sum()),
+        n_sft_seqs=int((~rl).sum()), max_rows_per_seq=int(seq_lengths.max()) if B else 0)

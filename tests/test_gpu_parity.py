@@ -21,7 +21,7 @@ from _cases import make_case, oracle_cfg
 from _golden import groups_of, load
 from oracle import rft_oracle as O
 from oracle import toy_policy as TP
-from paper_2505_17826_b200 import AlgorithmError, RFTLoss, RFTLossConfig, logprob_fwd
+from paper_2505_17826_b200 import AlgorithmError, RFTLoss, RFTLossConfig, logprob_fwd, pack_arrays
 from paper_2505_17826_b200 import triad_compat as C
 
 pytestmark = pytest.mark.gpu
@@ -343,3 +343,88 @@ def test_reference_errors_through_compat():
                        C.AlgorithmConfig("OPMD_PAIRWISE", tau=1.0))
     with pytest.raises(AlgorithmError):
         C.loss_sft([], params)
+
+
+# ---------------------------------------------------------------------------
+# BASELINE.json configs[2..4] as parity cases (reduced row counts, full vocab)
+
+
+def test_config3_ppo_k3_entropy_full_vocab_row_sample():
+    """configs[2]: PPO clip + low_var_kl + entropy at Qwen vocabulary.  Per-row
+    results are checked against the oracle on a sample of rows (the oracle is
+    row-separable given the sequence advantages the kernel reports)."""
+    V = 151936
+    lens, gs = [192] * 8, [4, 4]
+    cfg = RFTLossConfig(advantage_fn="grpo", policy_loss_fn="ppo_clip", kl_fn="low_var_kl",
+                        kl_coef=0.001, entropy_loss_fn="default", entropy_coef=0.001,
+                        loss_agg_mode="token-mean", clip_lo=0.2, clip_hi=0.28)
+    batch, packed = make_case(21, V, lens, gs)
+    out = RFTLoss(cfg)(packed)
+    rows = np.random.default_rng(0).choice(batch.n_rows, 48, replace=False)
+    sub = O.Batch(logits=batch.logits[rows], target=batch.target[rows],
+                  seq_offsets=np.arange(len(rows) + 1), group_offsets=np.array([0, len(rows)]),
+                  reward=np.zeros(len(rows)), old_lp=batch.old_lp[rows], ref_lp=batch.ref_lp[rows],
+                  advantage=np.repeat(out.seq_adv.double().cpu().numpy(), 192)[rows])
+    ref = O.general_loss(sub, oracle_cfg(cfg.with_(advantage_fn="given"),
+                                         n_tok_global=batch.n_rows))
+    np.testing.assert_allclose(out.lp.double().cpu().numpy()[rows], ref["lp"], rtol=1e-5,
+                               atol=1e-4)
+    np.testing.assert_allclose(out.entropy.double().cpu().numpy()[rows], ref["entropy"],
+                               rtol=1e-5, atol=1e-4)
+    d = out.dlogits.float().cpu().numpy()[rows].astype(np.float64)
+    r = ref["dz"]
+    assert np.all(np.abs(d - r) <= 2.0 ** -8 * np.abs(r).max() + 1e-2 * np.abs(r))
+    # GRPO advantages are standardised within each group (an all-equal group -> 0)
+    a = out.seq_adv.double().cpu().numpy()
+    for g in range(2):
+        rew = batch.reward[4 * g:4 * g + 4]
+        want = (rew - rew.mean()) / (rew.std(ddof=1) + 1e-6) if rew.std() > 0 else 0 * rew
+        np.testing.assert_allclose(a[4 * g:4 * g + 4], want, rtol=1e-5, atol=1e-6)
+
+
+def test_config4_mixed_grpo_sft_full_vocab():
+    """configs[3]: GRPO loss plus SFT NLL on expert trajectories in one batch,
+    50/50 mix, vocab 151,936 (the reference runs step_groups and step_sft
+    separately; the combined loss is their sum, orchestrator.py:299-315)."""
+    V = 151936
+    lens = [24] * 8
+    kind = [0, 0, 0, 0, 1, 1, 1, 1]
+    cfg = RFTLossConfig(advantage_fn="grpo", policy_loss_fn="ppo_clip",
+                        loss_agg_mode="token-mean", clip_lo=0.2, clip_hi=0.28, sft_weight=1.0)
+    batch, packed = make_case(22, V, lens, [4, 4], seq_kind=kind)
+    out = RFTLoss(cfg)(packed)
+    ref = O.general_loss(batch, oracle_cfg(cfg))
+    compare(out, ref, torch.bfloat16)
+    st = out.stats_dict()
+    assert st["n_sft_seqs"] == 4 and st["n_tok_rl"] == 96
+    # the SFT half equals loss_sft over the expert sequences (algorithms.py:256-274)
+    sft = O.ref_sft(batch, seqs=[4, 5, 6, 7])
+    assert st["sft_loss"] == pytest.approx(sft.loss, rel=1e-4)
+
+
+def test_config5_ragged_multiturn_row_index_gather():
+    """configs[4]: ragged long-CoT responses with interior mask-false spans.
+    The trainable rows are gathered in place from a padded [B*L, V] logits
+    tensor through row_index (no compaction copy); results equal the
+    compacted layout's."""
+    V = 32000
+    rng = np.random.default_rng(23)
+    B, L = 8, 96
+    full = torch.randn((B * L, V), device="cuda", dtype=torch.float32).mul_(2.0).to(torch.bfloat16)
+    mask = rng.uniform(size=(B, L)) < 0.85
+    for b in range(B):  # ragged: responses end early
+        mask[b, int(rng.integers(L // 3, L)):] = False
+    lens = mask.sum(axis=1).tolist()
+    idx = np.concatenate([np.nonzero(mask[b])[0] + b * L for b in range(B)])
+    tgt = rng.integers(0, V, idx.size)
+    reward = rng.integers(0, 2, B).astype(np.float32)
+    cfg = CONFIGS["grpo_ppo_k3_ent"]
+    gathered = pack_arrays(full, tgt, lens, [4, 4], reward, row_index=idx)
+    compact = pack_arrays(full[torch.as_tensor(idx, device="cuda")].contiguous(), tgt, lens,
+                          [4, 4], reward)
+    a = RFTLoss(cfg)(gathered)
+    b = RFTLoss(cfg)(compact)
+    assert torch.equal(a.lp, b.lp) and torch.equal(a.dlogits, b.dlogits)
+    assert torch.equal(a.stats, b.stats)
+    lp, _, _, seq_lp = logprob_fwd(gathered)
+    assert torch.allclose(lp, a.lp, atol=1e-4)
