@@ -66,6 +66,10 @@ def parse():
     p.add_argument("--e2e-groups", type=int, default=8)
     p.add_argument("--cpu-rows", type=int, default=256)
     p.add_argument("--quiet", action="store_true")
+    p.add_argument("--variant", default="grpo",
+                   choices=["grpo", "grpo_two_pass", "opmd_kimi", "opmd_pairwise", "sft"],
+                   help="loss variant (the headline metric is 'grpo'; the others measure the "
+                        "two-pass / sequence-coupled routes)")
     return p.parse_args()
 
 
@@ -254,7 +258,15 @@ def main():
     B = G * K
     cfg = RFTLossConfig(advantage_fn="grpo", policy_loss_fn="ppo_clip", kl_fn="low_var_kl",
                         kl_coef=0.001, loss_agg_mode="token-mean", clip_lo=0.2, clip_hi=0.28)
+    if args.variant == "grpo_two_pass":
+        cfg = cfg.with_(force_two_pass=True)
+    elif args.variant in ("opmd_kimi", "opmd_pairwise"):
+        cfg = RFTLossConfig(policy_loss_fn=args.variant, tau=1.0)
+    elif args.variant == "sft":
+        cfg = RFTLossConfig.from_variant("SFT")
     loss = RFTLoss(cfg)
+    two_pass = args.variant in ("grpo_two_pass", "opmd_kimi", "opmd_pairwise")
+    algo_bytes_row = (6 * V + 24) if two_pass else ALGO_BYTES_PER_ROW
 
     # ---- resident synthetic inputs (outside timing) ----
     gen = torch.Generator(device=dev)
@@ -281,7 +293,8 @@ def main():
         b = pack_arrays(logits, tgt, lens, gsz, rew, old_lp=old, ref_lp=ref)
         batches.append(b)
         outs.append(None)
-    assert loss.route(batches[0]) == 1, "expected the fused TMA route"
+    route = loss.route(batches[0])
+    assert route == (1 if not two_pass else (2 if args.variant == "grpo_two_pass" else 3)), route
     n_tok_g, n_seq_g = world * T, world * B
     stats_all = torch.zeros((n_mb, N.NSTAT), dtype=torch.float64, device=dev)
 
@@ -342,7 +355,7 @@ def main():
     # ---- roofline of the dominant kernel (k_fused_tma) ----
     peak, peak_src = peaks()
     f_ms = statistics.mean(fused_ms)
-    achieved = mb_rows * ALGO_BYTES_PER_ROW / (f_ms / 1000.0) / 1e9
+    achieved = mb_rows * algo_bytes_row / (f_ms / 1000.0) / 1e9
     # DRAM bytes per launch from the committed `ncu --set full` capture of the
     # same kernel at this vocabulary, scaled from its row count to this launch's
     # (the kernel streams rows independently, so bytes / row is size-invariant)
@@ -372,16 +385,20 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "vocab": V, "prompts": G, "repeats": K,
+            "config": {"workload": WORKLOAD if args.variant == "grpo" else
+                       f"{args.variant}_qwen2.5_1.5b_shapes", "vocab": V, "prompts": G,
+                       "repeats": K,
                        "response_len": Lr, "rows_per_gpu_per_step": T,
                        "micro_batches": n_mb, "rows_per_micro_batch": mb_rows,
-                       "loss": "grpo adv + ppo_clip(0.2,0.28) + low_var_kl(0.001) + token-mean",
+                       "loss": "grpo adv + ppo_clip(0.2,0.28) + low_var_kl(0.001) + token-mean"
+                       if args.variant == "grpo" else args.variant,
                        "l2": "inputs larger than L2 (80 GB working set)",
                        "parallelism": f"dp{world} (groups sharded by rank; stats allreduce)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_fused_tma", "kernel_ms": f_ms,
-                         "algorithmic_bytes_per_launch": mb_rows * ALGO_BYTES_PER_ROW,
+                         "kernel": "k_fused_tma" if not two_pass else "k_fwd..k_bwd (two-pass)",
+                         "kernel_ms": f_ms,
+                         "algorithmic_bytes_per_launch": mb_rows * algo_bytes_row,
                          "peak_source": peak_src,
                          "frac_of_8tbs_nominal": achieved / 8000.0},
             "cpu_baseline": cpu,
