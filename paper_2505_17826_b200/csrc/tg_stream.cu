@@ -14,6 +14,7 @@
 // HBM bytes per row: forward 2V (4V with anchor), backward 4V (6V with anchor).
 #include "tg_common.cuh"
 #include "tg_rowcoef.cuh"
+#include "tg_vecmath.cuh"
 
 namespace tg {
 
@@ -307,6 +308,119 @@ __global__ void __launch_bounds__(kStreamThreads) k_bwd(const KParams P) {
 }
 
 // ---------------------------------------------------------------------------
+// fast paths for the common case (no anchor, 16-byte aligned rows): four
+// 128-bit streaming loads in flight per thread, packed fp32x2 math, the lazily
+// rescaled accumulator of tg_vecmath.cuh, target logit read once per row.
+
+constexpr int kFastVec = 4;  // vectors per thread per iteration
+
+template <typename T>
+__global__ void __launch_bounds__(kStreamThreads) k_fwd_fast(const KParams P) {
+  constexpr int EPV = Vec<T>::N;
+  constexpr int ESZ = elem_bytes<T>();
+  __shared__ float4 red[kStreamWarps];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int V = int(P.vocab);
+  const int nvec = (V + EPV - 1) / EPV;
+  const int tail_vec = (V % EPV) ? nvec - 1 : -1;
+  const int tail_valid = V - (nvec - 1) * EPV;
+  for (int64_t row = blockIdx.x; row < P.n_rows; row += gridDim.x) {
+    const int64_t src_row = P.row_index ? P.row_index[row] : row;
+    const char* zrow = reinterpret_cast<const char*>(P.logits) + src_row * P.ld * ESZ;
+    Acc2 acc = {kNegInf, pk2(0.f, 0.f), pk2(0.f, 0.f), pk2(0.f, 0.f)};
+    for (int base = 0; base < nvec; base += kStreamThreads * kFastVec) {
+      uint4 u[kFastVec];
+      bool valid[kFastVec];
+#pragma unroll
+      for (int g = 0; g < kFastVec; ++g) {
+        const int vec = base + g * kStreamThreads + tid;
+        valid[g] = vec < nvec;
+        u[g] = valid[g] ? ld_stream(zrow + int64_t(vec) * 16) : Pk<T>::neutral();
+      }
+#pragma unroll
+      for (int g = 0; g < kFastVec; ++g) {
+        Pk<T>::clamp(u[g]);
+        if (base + g * kStreamThreads + tid == tail_vec) Pk<T>::mask_from(u[g], tail_valid);
+      }
+      const float vmax = group_max<T>(u);
+      if (__any_sync(0xffffffffu, vmax > acc.m + kSlack)) rescale(acc, vmax);
+#pragma unroll
+      for (int g = 0; g < kFastVec; ++g)
+        if (valid[g]) accumulate<T>(acc, u[g]);
+    }
+    Online o;
+    {
+      float s0, s1, t0, t1;
+      upk2(acc.s2, s0, s1);
+      upk2(acc.t2, t0, t1);
+      o = warp_merge(Online{acc.m, s0 + s1, t0 + t1});
+    }
+    if (lane == 0) red[warp] = make_float4(o.m, o.s, o.t, 0.f);
+    __syncthreads();
+    if (tid == 0) {
+      Online a = {kNegInf, 0.f, 0.f};
+      for (int w = 0; w < kStreamWarps; ++w) a = online_merge(a, Online{red[w].x, red[w].y, red[w].z});
+      const int y = P.target[row];
+      const float zy = (y >= 0 && y < V) ? Vec<T>::load1(zrow, y) : kNegInf;
+      const float lse = a.m + logf(a.s);
+      P.lse[row] = lse;
+      P.lp[row] = zy - lse;
+      P.ent[row] = lse - a.t / a.s;
+    }
+    __syncthreads();
+  }
+}
+
+template <typename T, bool kHasH>
+__global__ void __launch_bounds__(kStreamThreads) k_bwd_fast(const KParams P) {
+  constexpr int EPV = Vec<T>::N;
+  constexpr int ESZ = elem_bytes<T>();
+  const int tid = threadIdx.x;
+  const int V = int(P.vocab);
+  const int nvec = (V + EPV - 1) / EPV;
+  const int tail_vec = (V % EPV) ? nvec - 1 : -1;
+  const int tail_valid = V - (nvec - 1) * EPV;
+  for (int64_t row = blockIdx.x; row < P.n_rows; row += gridDim.x) {
+    const int64_t src_row = P.row_index ? P.row_index[row] : row;
+    const char* zrow = reinterpret_cast<const char*>(P.logits) + src_row * P.ld * ESZ;
+    char* drow = reinterpret_cast<char*>(P.dz) + row * P.ld_out * ESZ;
+    const int y = P.target[row];
+    const int vy = (y >= 0 && y < V) ? y / EPV : -1;
+    const int ye = (vy >= 0) ? y - vy * EPV : 0;
+    const float lseL = P.lse[row] * kLog2e;
+    const float a = P.rA[row], hz = P.rHz[row], s = P.rS[row];
+    const uint64_t nl2 = pk2(-lseL, -lseL), av2 = pk2(a, a), hz2 = pk2(hz, hz);
+    for (int base = 0; base < nvec; base += kStreamThreads * kFastVec) {
+      uint4 u[kFastVec];
+#pragma unroll
+      for (int g = 0; g < kFastVec; ++g) {
+        const int vec = base + g * kStreamThreads + tid;
+        u[g] = vec < nvec ? ld_stream(zrow + int64_t(vec) * 16) : Pk<T>::neutral();
+      }
+#pragma unroll
+      for (int g = 0; g < kFastVec; ++g) {
+        const int vec = base + g * kStreamThreads + tid;
+        if (vec >= nvec) continue;
+        float d[EPV];
+        dz_vec<T, kHasH>(u[g], d, nl2, av2, hz2);
+        if (vec == vy) {
+#pragma unroll
+          for (int e = 0; e < EPV; ++e)
+            if (e == ye) d[e] -= s;
+        }
+        if (vec == tail_vec) {
+#pragma unroll
+          for (int e = 0; e < EPV; ++e)
+            if (e < tail_valid) Vec<T>::store1(drow, int64_t(vec) * EPV + e, d[e]);
+        } else {
+          st_stream(drow + int64_t(vec) * 16, Vec<T>::pack(d));
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // launch helpers
 
 template <typename T>
@@ -315,19 +429,25 @@ static void launch_fwd_t(const KParams& P, bool anchor, bool vec, int grid, cuda
     if (vec) k_fwd<T, true, true><<<grid, kStreamThreads, 0, st>>>(P);
     else k_fwd<T, true, false><<<grid, kStreamThreads, 0, st>>>(P);
   } else {
-    if (vec) k_fwd<T, false, true><<<grid, kStreamThreads, 0, st>>>(P);
+    if (vec) k_fwd_fast<T><<<grid, kStreamThreads, 0, st>>>(P);
     else k_fwd<T, false, false><<<grid, kStreamThreads, 0, st>>>(P);
   }
 }
 
+// The backward's entropy coefficient is per row; the kHasH = true variant
+// covers every row (hz = 0 rows just carry a zero coefficient).
 template <typename T>
 static void launch_bwd_t(const KParams& P, bool anchor, bool vec, int grid, cudaStream_t st) {
   if (anchor) {
     if (vec) k_bwd<T, true, true><<<grid, kStreamThreads, 0, st>>>(P);
     else k_bwd<T, true, false><<<grid, kStreamThreads, 0, st>>>(P);
   } else {
-    if (vec) k_bwd<T, false, true><<<grid, kStreamThreads, 0, st>>>(P);
-    else k_bwd<T, false, false><<<grid, kStreamThreads, 0, st>>>(P);
+    if (vec) {
+      if (P.entf != TG_ENT_NONE) k_bwd_fast<T, true><<<grid, kStreamThreads, 0, st>>>(P);
+      else k_bwd_fast<T, false><<<grid, kStreamThreads, 0, st>>>(P);
+    } else {
+      k_bwd<T, false, false><<<grid, kStreamThreads, 0, st>>>(P);
+    }
   }
 }
 
