@@ -31,6 +31,8 @@ cudaError_t launch_fused(const KParams& P, const void* meta, int cl, int n_slots
                          int prefetch_rows,
                          cudaStream_t stream);
 int fused_chunk_bytes();
+cudaError_t launch_fused_l2(const KParams& P, const void* meta, int n_ctas, int prefetch,
+                            cudaStream_t st);
 int fused_max_clusters(int dtype, int cl);
 int fused_max_slots();
 size_t rowmeta_bytes();
@@ -395,11 +397,15 @@ int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspa
   count_launches(1 + (b->n_groups > 0 ? 1 : 0) + (b->n_seqs > 0 ? 1 : 0));
   if (route == 1) {
     const FusedPlan fp = fused_plan(b, o);
-    P.n_partials = fp.n_ctas;
-    if (fp.n_ctas > kMaxPartials) return fail(TG_EUNSUPPORTED, "too many CTAs");
+    // TG_FUSED_IMPL=l2: the L2-reread variant (tg_fused_l2.cu), for A/B
+    const bool l2 = env_int("TG_FUSED_IMPL", 0) == 2;
+    const int l2_ctas = int(b->n_rows < dev_info().sms ? b->n_rows : dev_info().sms);
+    P.n_partials = l2 ? l2_ctas : fp.n_ctas;
+    if (P.n_partials > kMaxPartials) return fail(TG_EUNSUPPORTED, "too many CTAs");
     if (b->n_rows > 0) {
       if (ev_begin) cudaEventRecord(ev_begin, st);
-      cudaError_t e = launch_fused(P, meta, fp.cl, fp.n_slots, fp.n_ctas, fp.prefetch_rows, st);
+      cudaError_t e = l2 ? launch_fused_l2(P, meta, l2_ctas, fp.prefetch_rows, st)
+                         : launch_fused(P, meta, fp.cl, fp.n_slots, fp.n_ctas, fp.prefetch_rows, st);
       if (ev_end) cudaEventRecord(ev_end, st);
       if (e != cudaSuccess) return fail(TG_ECUDA, "fused kernel launch: %s", cudaGetErrorString(e));
       count_launches(1);

@@ -9,7 +9,7 @@ i=0
 for rep in 1 2; do
   for v in ${AB_VARIANTS:-BASE=1}; do
     i=$((i+1))
-    env $v timeout 300 python bench.py --steps 3 --warmup 2 --no-cpu --no-e2e > gpurun_out/ab_${i}_${v}.log 2>&1; echo "bench $v rc=$?" >> gpurun_out/status.txt
+    env ${v//,/ } timeout 300 python bench.py --steps 3 --warmup 2 --no-cpu --no-e2e > gpurun_out/ab_${i}_${v}.log 2>&1; echo "bench $v rc=$?" >> gpurun_out/status.txt
   done
 done
 if [[ " $* " == *" ncu "* ]]; then
