@@ -33,6 +33,7 @@ cudaError_t launch_fused(const KParams& P, const void* meta, int cl, int n_slots
 int fused_chunk_bytes();
 cudaError_t launch_fused_l2(const KParams& P, const void* meta, int n_ctas, int prefetch,
                             cudaStream_t st);
+int l2_threads();
 int fused_max_clusters(int dtype, int cl);
 int fused_max_slots();
 size_t rowmeta_bytes();
@@ -399,7 +400,8 @@ int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspa
     const FusedPlan fp = fused_plan(b, o);
     // TG_FUSED_IMPL=l2: the L2-reread variant (tg_fused_l2.cu), for A/B
     const bool l2 = env_int("TG_FUSED_IMPL", 0) == 2;
-    const int l2_ctas = int(b->n_rows < dev_info().sms ? b->n_rows : dev_info().sms);
+    const int64_t l2_slots = int64_t(dev_info().sms) * (1024 / l2_threads());
+    const int l2_ctas = int(b->n_rows < l2_slots ? b->n_rows : l2_slots);
     P.n_partials = l2 ? l2_ctas : fp.n_ctas;
     if (P.n_partials > kMaxPartials) return fail(TG_EUNSUPPORTED, "too many CTAs");
     if (b->n_rows > 0) {

@@ -9,14 +9,14 @@
 // well inside the 126 MB L2) -- with L2::evict_first and writes dz with
 // streaming stores.  HBM traffic stays 4V bytes per row when the re-read
 // hits; there is no cluster exchange, no ring and no per-chunk barrier.
+#include <stdlib.h>
+
 #include "tg_common.cuh"
 #include "tg_rowcoef.cuh"
 #include "tg_vecmath.cuh"
 
 namespace tg {
 
-constexpr int kL2Threads = 1024;
-constexpr int kL2Warps = kL2Threads / 32;
 constexpr int kL2Vec = 4;  // vectors per thread per iteration
 
 __device__ __forceinline__ uint64_t policy_evict_last() {
@@ -33,11 +33,12 @@ __device__ __forceinline__ uint4 ld_hint(const void* p, uint64_t pol) {
   return r;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kL2Threads, 1)
+template <typename T, int kL2Threads>
+__global__ void __launch_bounds__(kL2Threads, 1024 / kL2Threads)
     k_fused_l2(const KParams P, const RowMeta* __restrict__ meta, int prefetch) {
   constexpr int EPV = Vec<T>::N;
   constexpr int ESZ = elem_bytes<T>();
+  constexpr int kL2Warps = kL2Threads / 32;
   __shared__ float4 red[kL2Warps];
   __shared__ float4 bc;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -97,7 +98,7 @@ __global__ void __launch_bounds__(kL2Threads, 1)
     if (lane == 0) red[warp] = make_float4(o.m, o.s, o.t, 0.f);
     __syncthreads();
     if (warp == 0) {
-      const float4 v = red[lane];
+      const float4 v = lane < kL2Warps ? red[lane] : make_float4(kNegInf, 0.f, 0.f, 0.f);
       const Online tot = warp_merge(Online{v.x, v.y, v.z});
       if (lane == 0) {
         const int y = cur.y;
@@ -197,13 +198,30 @@ __global__ void __launch_bounds__(kL2Threads, 1)
   }
 }
 
+// threads per CTA (TG_L2_THREADS = 256 / 512 / 1024); CTAs per SM = 1024 / threads
+int l2_threads() {
+  const char* e = getenv("TG_L2_THREADS");
+  const int t = e ? atoi(e) : 1024;
+  return (t == 256 || t == 512) ? t : 1024;
+}
+
 cudaError_t launch_fused_l2(const KParams& P, const void* meta, int n_ctas, int prefetch,
                             cudaStream_t st) {
   const RowMeta* m = reinterpret_cast<const RowMeta*>(meta);
-  if (P.dtype == TG_DTYPE_BF16)
-    k_fused_l2<bf16_t><<<n_ctas, kL2Threads, 0, st>>>(P, m, prefetch);
-  else
-    k_fused_l2<float><<<n_ctas, kL2Threads, 0, st>>>(P, m, prefetch);
+  const bool b16 = P.dtype == TG_DTYPE_BF16;
+  switch (l2_threads()) {
+    case 256:
+      if (b16) k_fused_l2<bf16_t, 256><<<n_ctas, 256, 0, st>>>(P, m, prefetch);
+      else k_fused_l2<float, 256><<<n_ctas, 256, 0, st>>>(P, m, prefetch);
+      break;
+    case 512:
+      if (b16) k_fused_l2<bf16_t, 512><<<n_ctas, 512, 0, st>>>(P, m, prefetch);
+      else k_fused_l2<float, 512><<<n_ctas, 512, 0, st>>>(P, m, prefetch);
+      break;
+    default:
+      if (b16) k_fused_l2<bf16_t, 1024><<<n_ctas, 1024, 0, st>>>(P, m, prefetch);
+      else k_fused_l2<float, 1024><<<n_ctas, 1024, 0, st>>>(P, m, prefetch);
+  }
   return cudaGetLastError();
 }
 
