@@ -54,31 +54,44 @@ def _stale(target: Path, deps) -> bool:
     return any(Path(d).stat().st_mtime > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = False) -> Path:
-    OBJDIR.mkdir(parents=True, exist_ok=True)
+# instrumented builds for kernel studies (never the product library):
+#   prof -> libtg_loss_prof.so with per-CTA cycle accounting in k_fused_tma
+VARIANTS = {"prof": ["-DTG_FUSED_PROF"]}
+
+
+def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = False,
+          variant: str | None = None) -> Path:
+    objdir, lib_out, defines = OBJDIR, LIB, []
+    if variant:
+        objdir = ROOT / "build" / f"obj_{variant}"
+        lib_out = LIBDIR / f"libtg_loss_{variant}.so"
+        defines = VARIANTS[variant]
+    OBJDIR_, LIB_ = objdir, lib_out
+    OBJDIR_.mkdir(parents=True, exist_ok=True)
     LIBDIR.mkdir(parents=True, exist_ok=True)
     headers = list(CSRC.glob("*.cuh")) + [ROOT / "include" / "tg_loss.h"]
     objs = []
     for src in CU_SOURCES:
-        obj = OBJDIR / (src + ".o")
+        obj = OBJDIR_ / (src + ".o")
         objs.append(obj)
         if force or _stale(obj, [CSRC / src, *headers]):
             extra = ["-Xptxas", "-v"] if ptxas_verbose else []
-            _run([nvcc(), *ARCH, *NVCC_FLAGS, *extra, "-c", str(CSRC / src), "-o", str(obj)],
+            _run([nvcc(), *ARCH, *NVCC_FLAGS, *defines, *extra, "-c", str(CSRC / src), "-o",
+                  str(obj)],
                  verbose or ptxas_verbose)
     for src in CPP_SOURCES:
-        obj = OBJDIR / (src + ".o")
+        obj = OBJDIR_ / (src + ".o")
         objs.append(obj)
         if force or _stale(obj, [CSRC / src, *headers]):
             _run(["g++", "-O2", "-std=c++17", "-fPIC", "-I", str(ROOT / "include"), "-c",
                   str(CSRC / src), "-o", str(obj)], verbose)
-    if force or _stale(LIB, objs):
-        _run([nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs)],
+    if force or _stale(LIB_, objs):
+        _run([nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(LIB_), *map(str, objs)],
              verbose)
-    return LIB
+    return LIB_
 
 
 if __name__ == "__main__":
-    build(verbose="--verbose" in sys.argv, force="--force" in sys.argv,
-          ptxas_verbose="--ptxas" in sys.argv)
-    print(LIB)
+    var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), None)
+    print(build(verbose="--verbose" in sys.argv, force="--force" in sys.argv,
+                ptxas_verbose="--ptxas" in sys.argv, variant=var))

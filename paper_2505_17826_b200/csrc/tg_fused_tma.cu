@@ -64,7 +64,35 @@ struct FusedSmemTail {
   float4 wpart[2][kConsumerWarps];
   float4 bcast[2];  // (a, h, lse, s) of a row, from the epilogue warp
   double stats[16];
+#ifdef TG_FUSED_PROF
+  unsigned long long prof[8];
+#endif
 };
+
+// ---- optional cycle accounting (profiling build only: -DTG_FUSED_PROF) -------
+// prof[0] consumer cycles waiting for ring data (summed over consumer warps)
+// prof[1] consumer cycles waiting for the epilogue broadcast (summed over warps)
+// prof[2] consumer busy span (warp 0: first wait -> last store)
+// prof[3] producer cycles waiting for a free slot
+// prof[4] epilogue cycles waiting for the consumer partials
+// prof[5] epilogue cycles waiting for the cluster exchange
+// prof[6] rows processed by the CTA
+#ifdef TG_FUSED_PROF
+__device__ unsigned long long g_fused_prof[1024][8];
+__device__ __forceinline__ FusedSmemTail* prof_tail() {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  return reinterpret_cast<FusedSmemTail*>(smem + size_t(kSlots) * kChunk);
+}
+#define TG_PROF_T0() const long long _tp0 = clock64()
+#define TG_PROF_ADD(tail, i)                                                     \
+  do {                                                                           \
+    if ((threadIdx.x & 31) == 0)                                                 \
+      atomicAdd(&(tail)->prof[i], (unsigned long long)(clock64() - _tp0));       \
+  } while (0)
+#else
+#define TG_PROF_T0() (void)0
+#define TG_PROF_ADD(tail, i) (void)0
+#endif
 
 // ---- shared-memory / barrier primitives on 32-bit shared addresses ----------
 
@@ -124,7 +152,11 @@ __device__ __forceinline__ void phase1_chunk(Acc2& acc, RingIt& it, const RingBa
                                              int vbase, const Slice& sl, int tid) {
   uint4 u[kVecPerThread];
   bool valid[kVecPerThread];
-  wait_full(it.full(rb), it.phase());
+  {
+    TG_PROF_T0();
+    wait_full(it.full(rb), it.phase());
+    TG_PROF_ADD(prof_tail(), 0);
+  }
   const uint32_t a = it.addr(rb) + tid * 16;
 #pragma unroll
   for (int g = 0; g < kVecPerThread; ++g) {
@@ -269,11 +301,17 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       mbar_init(&tail->bbar[i], 1);
     }
     fence_mbar_init();
+#ifdef TG_FUSED_PROF
+    for (int i = 0; i < 8; ++i) tail->prof[i] = 0ull;
+#endif
   }
   if (CL > 1)
     cluster_sync_all();
   else
     __syncthreads();
+#ifdef TG_FUSED_PROF
+  const long long t_start = clock64();
+#endif
 
   if (warp == kProducerWarp) {
     // ===================== producer warp: bulk TMA into the ring =====================
@@ -296,7 +334,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         }
         const char* src = slice_ptr(row);
         for (int j = 0; j < sl.nchunk; ++j) {
-          mbar_wait_u32(it.empty(rb), it.phase() ^ 1u);
+          {
+            TG_PROF_T0();
+            mbar_wait_u32(it.empty(rb), it.phase() ^ 1u);
+            TG_PROF_ADD(tail, 3);
+          }
           const uint32_t off = uint32_t(j) * kChunk;
           const uint32_t bytes = min(uint32_t(kChunk), slice_bytes - off);
           asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
@@ -331,7 +373,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       const int y = __ldg(&meta[row].y);
       const int vy = (y >= 0 && y < V) ? (y / EPV) : -1;
       const int ye = (vy >= 0) ? y - vy * EPV : 0;
-      mbar_wait_u32(smem_u32(&tail->pbar[par]), parity);
+      {
+        TG_PROF_T0();
+        mbar_wait_u32(smem_u32(&tail->pbar[par]), parity);
+        TG_PROF_ADD(tail, 4);
+      }
       const float4 v = (lane < kConsumerWarps) ? tail->wpart[par][lane]
                                                : make_float4(kNegInf, 0.f, 0.f, 0.f);
       const Online cta = warp_merge(Online{v.x, v.y, v.z});
@@ -356,7 +402,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
             st_async_v4(map_to_rank(my_slot, r), cta.m, cta.s, cta.t, czy, map_to_rank(bar, r));
           }
         }
-        mbar_wait_cluster(&tail->xbar[par], parity);
+        {
+          TG_PROF_T0();
+          mbar_wait_cluster(&tail->xbar[par], parity);
+          TG_PROF_ADD(tail, 5);
+        }
         tot = {kNegInf, 0.f, 0.f};
         tzy = kNegInf;
 #pragma unroll
@@ -461,7 +511,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       if (nrow < NR) phase1_range<T>(acc, npos, rb, sl, 0, pre, tid);
 
       // ---------------- phase 2: dz from the resident slice ----------------
-      mbar_wait_u32(smem_u32(&tail->bbar[par]), uint32_t((k >> 1) & 1));
+      {
+        TG_PROF_T0();
+        mbar_wait_u32(smem_u32(&tail->bbar[par]), uint32_t((k >> 1) & 1));
+        TG_PROF_ADD(tail, 1);
+      }
       const float4 bc = tail->bcast[par];
       const float a = bc.x, hz = bc.y, s_t = bc.w;
       const float lseL = bc.z * kLog2e;
@@ -473,10 +527,20 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         phase2_row<T, true>(sl, pos0, rb, dzrow, vy, ye, s_t, nl2, av2, hz2, tid, lane);
       pos0 = npos;
       y_cur = y_next;
+#ifdef TG_FUSED_PROF
+      if (tid == 0) tail->prof[6] += 1;
+#endif
     }
+#ifdef TG_FUSED_PROF
+    if (tid == 0) tail->prof[2] = (unsigned long long)(clock64() - t_start);
+#endif
   }
   if (CL > 1)
     cluster_sync_all();  // no CTA leaves while a peer may still st.async into it
+#ifdef TG_FUSED_PROF
+  __syncthreads();
+  if (tid < 8) g_fused_prof[blockIdx.x][tid] = tail->prof[tid];
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -579,6 +643,14 @@ int fused_max_clusters(int dtype, int cl) {
   }
   return cache[dev][di][cl];
 }
+
+#ifdef TG_FUSED_PROF
+// profiling build: per-CTA counters of the last fused launch (see prof[] above)
+extern "C" int tg_debug_fused_prof(unsigned long long* out, int n_ctas) {
+  if (n_ctas > 1024) n_ctas = 1024;
+  return int(cudaMemcpyFromSymbol(out, g_fused_prof, size_t(n_ctas) * 8 * sizeof(unsigned long long)));
+}
+#endif
 
 int fused_chunk_bytes() { return kChunk; }
 int fused_max_slots() { return kSlots; }

@@ -1,0 +1,20 @@
+"""Summarise the per-CTA cycle accounting of the instrumented fused kernel
+(libtg_loss_prof.so, bench.py with TG_FUSED_PROF_OUT=file.npy)."""
+import sys
+
+import numpy as np
+
+NCW = 14  # consumer warps
+for f in sys.argv[1:]:
+    a = np.load(f).astype(np.float64)
+    a = a[a[:, 2] > 0]
+    span = a[:, 2]
+    print(f"{f}: {len(a)} CTAs, rows/CTA {a[:, 6].mean():.1f}, span {span.mean() / 1e6:.2f} Mcyc")
+    names = ["consumer data wait", "consumer bcast wait", None, "producer slot wait",
+             "epilogue partial wait", "epilogue cluster wait"]
+    for i, n in enumerate(names):
+        if n is None:
+            continue
+        per = a[:, i] / (NCW if i < 2 else 1)
+        print(f"  {n:24s} {100 * (per / span).mean():6.2f} % of span "
+              f"(min {100 * (per / span).min():.1f}, max {100 * (per / span).max():.1f})")
