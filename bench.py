@@ -346,9 +346,9 @@ def main():
     prof_out = os.environ.get("TG_FUSED_PROF_OUT")
     if prof_out and hasattr(L, "tg_debug_fused_prof"):  # instrumented library only
         import ctypes
-        buf = (ctypes.c_ulonglong * (1024 * 8))()
+        buf = (ctypes.c_ulonglong * (1024 * 16))()
         L.tg_debug_fused_prof(buf, 1024)
-        arr = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 8)
+        arr = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 16)
         np.save(prof_out, arr[:int((arr[:, 6] > 0).sum()) or 1024])
     ms = t_start.elapsed_time(t_end)
     fused_ms = [a.elapsed_time(b_) for a, b_ in evs]

@@ -60,12 +60,13 @@ VARIANTS = {"prof": ["-DTG_FUSED_PROF"]}
 
 
 def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = False,
-          variant: str | None = None) -> Path:
-    objdir, lib_out, defines = OBJDIR, LIB, []
+          variant: str | None = None, defines: list | None = None) -> Path:
+    objdir, lib_out = OBJDIR, LIB
+    defines = list(defines or [])
     if variant:
         objdir = ROOT / "build" / f"obj_{variant}"
         lib_out = LIBDIR / f"libtg_loss_{variant}.so"
-        defines = VARIANTS[variant]
+        defines = VARIANTS.get(variant, []) + defines
     OBJDIR_, LIB_ = objdir, lib_out
     OBJDIR_.mkdir(parents=True, exist_ok=True)
     LIBDIR.mkdir(parents=True, exist_ok=True)
@@ -93,5 +94,6 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
 
 if __name__ == "__main__":
     var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), None)
+    defs = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--define=")]
     print(build(verbose="--verbose" in sys.argv, force="--force" in sys.argv,
-                ptxas_verbose="--ptxas" in sys.argv, variant=var))
+                ptxas_verbose="--ptxas" in sys.argv, variant=var, defines=defs))

@@ -105,6 +105,23 @@ __device__ __forceinline__ Online warp_merge(Online o) {
   return o;
 }
 
+// merge of the partials held by lanes [0, N) (the others hold the neutral
+// element): log2(next_pow2(N)) butterfly levels instead of five; lane 0 gets the total
+template <int N>
+__device__ __forceinline__ Online warp_merge_first(Online o) {
+  constexpr int top = N > 16 ? 16 : N > 8 ? 8 : N > 4 ? 4 : N > 2 ? 2 : 1;
+#pragma unroll
+  for (int d = top; d >= 1; d >>= 1) {
+    if (d >= N && d > 1) continue;
+    Online x;
+    x.m = __shfl_xor_sync(0xffffffffu, o.m, d);
+    x.s = __shfl_xor_sync(0xffffffffu, o.s, d);
+    x.t = __shfl_xor_sync(0xffffffffu, o.t, d);
+    o = online_merge(o, x);
+  }
+  return o;
+}
+
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
   for (int d = 16; d >= 1; d >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, d));
@@ -270,6 +287,13 @@ __device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t addr, uint32_t pa
       : "r"(addr), "r"(parity)
       : "memory");
   return ok != 0;
+}
+
+template <int kSleep>
+__device__ __forceinline__ void mbar_wait_cluster_sleep(uint32_t addr, uint32_t parity) {
+  while (!mbar_try_wait_cluster(addr, parity)) {
+    if constexpr (kSleep > 0) __nanosleep(kSleep);
+  }
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {

@@ -39,33 +39,45 @@
 
 namespace tg {
 
-// 14 consumer warps + 1 epilogue warp + 1 producer warp = 16 warps: with the
-// 4-warp register allocation granularity this leaves 128 registers per thread
-// (17 warps would cap it at 96 and spill).
-constexpr int kConsumerWarps = 14;
+// Geometry (overridable at build time for A/B studies):
+//   TG_CONSUMER_WARPS consumer warps + 1 epilogue warp + 1 producer warp,
+//   TG_VEC_PER_THREAD 16-byte vectors per consumer thread per chunk,
+//   TG_SLOTS ring slots of one chunk each (<= 227 KB of opt-in SMEM).
+// Measured on B200 (V = 151,936, CL = 2): 16 x 4 x 7 (32 KB chunks, 4 consumer
+// warps on every SM sub-partition) beats 14 x 4 x 8 by ~1.5 %; more warps with
+// fewer vectors each, or smaller chunks, lose (scripts/gpu_libab.sh).
+#ifndef TG_CONSUMER_WARPS
+#define TG_CONSUMER_WARPS 16
+#endif
+#ifndef TG_VEC_PER_THREAD
+#define TG_VEC_PER_THREAD 4
+#endif
+#ifndef TG_SLOTS
+#define TG_SLOTS 7
+#endif
+constexpr int kConsumerWarps = TG_CONSUMER_WARPS;
 constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kEpilogueWarp = kConsumerWarps;
 constexpr int kProducerWarp = kConsumerWarps + 1;
 constexpr int kFusedThreads = kConsumers + 64;
-constexpr int kVecPerThread = 4;                  // 16-byte vectors per consumer thread per chunk
+constexpr int kVecPerThread = TG_VEC_PER_THREAD;  // 16-byte vectors per consumer thread per chunk
 constexpr int kVecPerChunk = kConsumers * kVecPerThread;
-constexpr int kChunk = kVecPerChunk * 16;         // 28 KB per TMA bulk copy / ring slot
-constexpr int kSlots = 8;                          // ring: 224 KB of the 227 KB opt-in SMEM
+constexpr int kChunk = kVecPerChunk * 16;         // bytes per TMA bulk copy / ring slot
+constexpr int kSlots = TG_SLOTS;
+static_assert(kConsumerWarps <= 32, "one partial per epilogue lane");
 constexpr int kMaxPrefixChunks = 8;  // next-row phase-1 chunks run before this row's phase 2
 constexpr uint32_t kPrefetchPiece = 65536;  // bytes per L2 prefetch instruction
 
 struct FusedSmemTail {
   uint64_t full[kSlots];
   uint64_t empty[kSlots];
-  uint64_t xbar[2];   // cluster exchange (DSMEM tx bytes from the peers)
   uint64_t pbar[2];   // consumers -> epilogue warp: per-warp partials written
   uint64_t bbar[2];   // epilogue warp -> consumers: (a, h, lse, s) written
-  float4 xdata[2][4];
-  float4 wpart[2][kConsumerWarps];
+  float4 wpart[2][4 * kConsumerWarps];  // [rank * warps + warp]: every CTA's partials
   float4 bcast[2];  // (a, h, lse, s) of a row, from the epilogue warp
   double stats[16];
 #ifdef TG_FUSED_PROF
-  unsigned long long prof[8];
+  unsigned long long prof[16];
 #endif
 };
 
@@ -77,8 +89,10 @@ struct FusedSmemTail {
 // prof[4] epilogue cycles waiting for the consumer partials
 // prof[5] epilogue cycles waiting for the cluster exchange
 // prof[6] rows processed by the CTA
+// prof[7] epilogue critical path: partials complete -> broadcast
+// prof[8] epilogue: cluster exchange complete -> broadcast
 #ifdef TG_FUSED_PROF
-__device__ unsigned long long g_fused_prof[1024][8];
+__device__ unsigned long long g_fused_prof[1024][16];
 __device__ __forceinline__ FusedSmemTail* prof_tail() {
   extern __shared__ __align__(1024) unsigned char smem[];
   return reinterpret_cast<FusedSmemTail*>(smem + size_t(kSlots) * kChunk);
@@ -119,10 +133,10 @@ struct RingBase {
 };
 
 // Ring position as a running chunk counter: slot = c mod kSlots, mbarrier phase
-// parity = (c / kSlots) & 1 (kSlots is a power of two, so both are one op).
+// parity = (c / kSlots) & 1 (compile-time divisor: a multiply-shift at most).
 struct RingIt {
   uint32_t c;
-  __device__ __forceinline__ uint32_t slot() const { return c & (kSlots - 1); }
+  __device__ __forceinline__ uint32_t slot() const { return c % uint32_t(kSlots); }
   __device__ __forceinline__ uint32_t phase() const { return (c / kSlots) & 1u; }
   __device__ __forceinline__ uint32_t addr(const RingBase& rb) const { return rb.ring + slot() * kChunk; }
   __device__ __forceinline__ uint32_t full(const RingBase& rb) const { return rb.full + slot() * 8u; }
@@ -145,10 +159,49 @@ struct Slice {
 
 // ---- phase 1: one chunk (kVecPerThread vectors per consumer thread) ---------
 // kPartial: the chunk may run past the slice end (lanes there use a neutral
-// -1e30 vector and skip the sums, but still vote, so the lazy-rescale test is
+// -1e30 vector and skip the sums, but still vote, so the rescale test is
 // always a full-warp vote).  kMaskTail: the chunk holds the tail padding.
+//
+// Speculative fast path (full chunks): the sums are taken straight away with
+// the lane's current reference max m -- no -inf clamp, no vector max, no
+// pre-vote -- and accepted when they are safe: finite, s <= 2^32 (no term near
+// overflow) and, for the first chunk of a row (m carried over from the
+// previous row), s >= 2^-20 (no significant term lost to underflow).  Otherwise
+// (a -inf logit gives 0 * -inf = NaN in the sum of p z, a new maximum more
+// than ~22 above m, the first rows) the warp redoes the chunk on the checked
+// path: clamp, vector max, rescale, sums.  The checked path is what partial
+// and tail chunks always take.
+struct Acc1 {
+  Acc2 a;
+  bool fresh;  // no chunk of the current row accumulated yet by this lane
+};
+
 template <typename T, bool kPartial, bool kMaskTail>
-__device__ __forceinline__ void phase1_chunk(Acc2& acc, RingIt& it, const RingBase& rb,
+__device__ __forceinline__ void phase1_checked(Acc1& acc, uint4 (&u)[kVecPerThread],
+                                               const bool (&valid)[kVecPerThread], int vbase,
+                                               const Slice& sl, int tid) {
+#pragma unroll
+  for (int g = 0; g < kVecPerThread; ++g) {
+    const int vec = vbase + g * kConsumers + tid;
+    Pk<T>::clamp(u[g]);
+    if (kMaskTail && vec == sl.tail_vec) Pk<T>::mask_from(u[g], sl.tail_valid);
+  }
+  const float vmax = group_max<T>(u);
+  if (acc.fresh) {  // empty sums: take this chunk's max as the reference
+    acc.a.m = vmax;
+    const float nmL = -vmax * kLog2e;
+    acc.a.nm2 = pk2(nmL, nmL);
+  } else {
+    rescale(acc.a, vmax);
+  }
+#pragma unroll
+  for (int g = 0; g < kVecPerThread; ++g)
+    if (!kPartial || valid[g]) accumulate<T>(acc.a, u[g]);
+  acc.fresh = false;
+}
+
+template <typename T, bool kPartial, bool kMaskTail>
+__device__ __forceinline__ void phase1_chunk(Acc1& acc, RingIt& it, const RingBase& rb,
                                              int vbase, const Slice& sl, int tid) {
   uint4 u[kVecPerThread];
   bool valid[kVecPerThread];
@@ -163,15 +216,35 @@ __device__ __forceinline__ void phase1_chunk(Acc2& acc, RingIt& it, const RingBa
     const int vec = vbase + g * kConsumers + tid;
     valid[g] = !kPartial || vec < sl.v1;
     u[g] = valid[g] ? lds128(a + g * kConsumers * 16) : Pk<T>::neutral();
-    Pk<T>::clamp(u[g]);
-    if (kMaskTail && vec == sl.tail_vec) Pk<T>::mask_from(u[g], sl.tail_valid);
   }
   it.next();
-  const float vmax = group_max<T>(u);
-  if (__any_sync(0xffffffffu, vmax > acc.m + kSlack)) rescale(acc, vmax);
+  if constexpr (!kPartial && !kMaskTail) {
+    const uint64_t l2e2 = pk2(kLog2e, kLog2e);
+    uint64_t s2 = pk2(0.f, 0.f), t2 = pk2(0.f, 0.f);
 #pragma unroll
-  for (int g = 0; g < kVecPerThread; ++g)
-    if (!kPartial || valid[g]) accumulate<T>(acc, u[g]);
+    for (int g = 0; g < kVecPerThread; ++g) {
+#pragma unroll
+      for (int w = 0; w < Vec<T>::N / 2; ++w) {
+        const uint64_t x = pair<T>(u[g], w);
+        const uint64_t p = ex2x2(fma2(x, l2e2, acc.a.nm2));
+        s2 = add2(s2, p);
+        t2 = fma2(p, x, t2);
+      }
+    }
+    float s0, s1, t0, t1;
+    upk2(s2, s0, s1);
+    upk2(t2, t0, t1);
+    const float sc = s0 + s1, tc = t0 + t1;
+    const bool ok = sc <= 4294967296.0f && fabsf(tc) <= 3.0e38f &&
+                    (!acc.fresh || sc >= 9.5367431640625e-07f);
+    if (__all_sync(0xffffffffu, ok)) {
+      acc.a.s2 = add2(acc.a.s2, s2);
+      acc.a.t2 = add2(acc.a.t2, t2);
+      acc.fresh = false;
+      return;
+    }
+  }
+  phase1_checked<T, kPartial, kMaskTail>(acc, u, valid, vbase, sl, tid);
 }
 
 // ---- phase 2: dz for one chunk ------------------------------------------------
@@ -179,7 +252,7 @@ template <typename T, bool kHasH, bool kCheck>
 __device__ __forceinline__ void phase2_chunk(const RingIt& it, const RingBase& rb, int vbase,
                                              const Slice& sl, char* dzrow, int vy, int ye,
                                              float s_t, uint64_t nl2, uint64_t av2, uint64_t hz2,
-                                             int tid) {
+                                             uint32_t pf2, int tid) {
   constexpr int EPV = Vec<T>::N;
   char* dst = dzrow + int64_t(vbase + tid) * 16;
   const uint32_t a = it.addr(rb) + tid * 16;
@@ -188,7 +261,7 @@ __device__ __forceinline__ void phase2_chunk(const RingIt& it, const RingBase& r
     const int vec = vbase + g * kConsumers + tid;
     if (!kCheck || vec < sl.v1) {
       float d[EPV];
-      dz_vec<T, kHasH>(lds128(a + g * kConsumers * 16), d, nl2, av2, hz2);
+      dz_vec<T, kHasH>(lds128(a + g * kConsumers * 16), d, nl2, av2, hz2, pf2);
       bool done = false;
       if (kCheck) {
         if (vec == vy) {
@@ -203,7 +276,11 @@ __device__ __forceinline__ void phase2_chunk(const RingIt& it, const RingBase& r
           done = true;
         }
       }
+#ifdef TG_NULL_MATH
+      if (!done) st_stream(dst + g * kConsumers * 16, lds128(a + g * kConsumers * 16));
+#else
       if (!done) st_stream(dst + g * kConsumers * 16, Vec<T>::pack(d));
+#endif
     }
   }
 }
@@ -213,16 +290,17 @@ __device__ __forceinline__ void phase2_chunk(const RingIt& it, const RingBase& r
 template <typename T, bool kHasH>
 __device__ __forceinline__ void phase2_row(const Slice& sl, RingIt it, const RingBase& rb,
                                            char* dzrow, int vy, int ye, float s_t, uint64_t nl2,
-                                           uint64_t av2, uint64_t hz2, int tid, int lane) {
+                                           uint64_t av2, uint64_t hz2, uint32_t pf2, int tid,
+                                           int lane) {
   int vbase = sl.v0;
   for (int j = 0; j < sl.nchunk; ++j) {
     const int vend = vbase + kVecPerChunk;
     const bool check = (vend > sl.v1) || (sl.tail_vec >= vbase && sl.tail_vec < vend) ||
                        (vy >= vbase && vy < vend);
     if (check)
-      phase2_chunk<T, kHasH, true>(it, rb, vbase, sl, dzrow, vy, ye, s_t, nl2, av2, hz2, tid);
+      phase2_chunk<T, kHasH, true>(it, rb, vbase, sl, dzrow, vy, ye, s_t, nl2, av2, hz2, pf2, tid);
     else
-      phase2_chunk<T, kHasH, false>(it, rb, vbase, sl, dzrow, vy, ye, s_t, nl2, av2, hz2, tid);
+      phase2_chunk<T, kHasH, false>(it, rb, vbase, sl, dzrow, vy, ye, s_t, nl2, av2, hz2, pf2, tid);
     __syncwarp();
     if (lane == 0) arrive_u32(it.empty(rb));
     it.next();
@@ -232,7 +310,7 @@ __device__ __forceinline__ void phase2_row(const Slice& sl, RingIt it, const Rin
 
 // phase 1 over chunks [c0, c1) of a row whose first chunk is at `row_it`
 template <typename T>
-__device__ __forceinline__ void phase1_range(Acc2& acc, RingIt row_it, const RingBase& rb,
+__device__ __forceinline__ void phase1_range(Acc1& acc, RingIt row_it, const RingBase& rb,
                                              const Slice& sl, int c0, int c1, int tid) {
   RingIt it = row_it;
   it.advance(c0);
@@ -250,14 +328,47 @@ __device__ __forceinline__ void phase1_range(Acc2& acc, RingIt row_it, const Rin
   }
 }
 
-__device__ __forceinline__ Acc2 acc_init() {
-  return Acc2{kNegInf, pk2(0.f, 0.f), pk2(0.f, 0.f), pk2(0.f, 0.f)};  // nm2 set on first use
+// new row: empty sums; the reference max carries over from the previous row
+// (the fast path's bet that consecutive rows have similar maxima)
+__device__ __forceinline__ void acc_new_row(Acc1& acc) {
+  acc.a.s2 = pk2(0.f, 0.f);
+  acc.a.t2 = pk2(0.f, 0.f);
+  acc.fresh = true;
+}
+
+__device__ __forceinline__ Acc1 acc_init() {
+  Acc1 acc;
+  acc.a.m = 0.f;
+  acc.a.nm2 = pk2(0.f, 0.f);
+  acc_new_row(acc);
+  return acc;
 }
 
 // waits of the producer / epilogue warps back off with nanosleep so their
 // polling does not steal issue slots from the consumer warps on the same SMSP
+// Back-off (ns) of the producer's slot waits, the epilogue's partial waits and
+// the consumers' broadcast waits; a negative value selects a try_wait with a
+// suspend-time hint (the warp sleeps until the phase completes).
+#ifndef TG_SLEEP_PROD
+#define TG_SLEEP_PROD 64
+#endif
+#ifndef TG_SLEEP_EPI
+#define TG_SLEEP_EPI 64
+#endif
+#ifndef TG_SLEEP_BCAST
+#define TG_SLEEP_BCAST 64
+#endif
+template <int kSleep>
 __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) __nanosleep(64);
+  if constexpr (kSleep < 0) {
+    while (!mbar_try_wait_sleep(bar, parity)) {
+    }
+  } else if constexpr (kSleep == 0) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+  } else {
+    while (!mbar_try_wait(bar, parity)) __nanosleep(kSleep);
+  }
 }
 
 template <typename T, int CL>
@@ -296,13 +407,12 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       mbar_init(&tail->empty[i], kConsumerWarps);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&tail->xbar[i], 1);
-      mbar_init(&tail->pbar[i], kConsumerWarps);
+      mbar_init(&tail->pbar[i], kConsumerWarps + (CL > 1 ? 1 : 0));  // + epilogue expect_tx
       mbar_init(&tail->bbar[i], 1);
     }
     fence_mbar_init();
 #ifdef TG_FUSED_PROF
-    for (int i = 0; i < 8; ++i) tail->prof[i] = 0ull;
+    for (int i = 0; i < 16; ++i) tail->prof[i] = 0ull;
 #endif
   }
   if (CL > 1)
@@ -336,7 +446,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         for (int j = 0; j < sl.nchunk; ++j) {
           {
             TG_PROF_T0();
-            mbar_wait_u32(it.empty(rb), it.phase() ^ 1u);
+            mbar_wait_u32<TG_SLEEP_PROD>(it.empty(rb), it.phase() ^ 1u);
             TG_PROF_ADD(tail, 3);
           }
           const uint32_t off = uint32_t(j) * kChunk;
@@ -363,63 +473,50 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     double sd[15];
 #pragma unroll
     for (int i = 0; i < 15; ++i) sd[i] = 0.0;
-    RingIt pos0 = {0u};
     int64_t k = 0;
     for (int64_t row = cid; row < NR; row += ncl, ++k) {
       const int par = int(k & 1);
       const uint32_t parity = uint32_t((k >> 1) & 1);
       RowMeta cur;
-      if (lane == 0) cur = load_meta(meta, row);
-      const int y = __ldg(&meta[row].y);
-      const int vy = (y >= 0 && y < V) ? (y / EPV) : -1;
-      const int ye = (vy >= 0) ? y - vy * EPV : 0;
+      float tzy = kNegInf;  // the target logit, read ahead of the wait (raw, unclamped)
+      if (lane == 0) {
+        cur = load_meta(meta, row);
+        const int y = cur.y;
+        if (y >= 0 && y < V) {
+          const int64_t src_row = P.row_index ? P.row_index[row] : row;
+          tzy = Vec<T>::load1(reinterpret_cast<const char*>(P.logits) + src_row * P.ld * ESZ, y);
+        }
+        if constexpr (CL > 1)
+          mbar_arrive_expect_tx(&tail->pbar[par], (CL - 1) * kConsumerWarps * 16);
+      }
       {
         TG_PROF_T0();
-        mbar_wait_u32(smem_u32(&tail->pbar[par]), parity);
+        if constexpr (CL > 1)
+          mbar_wait_cluster_sleep<TG_SLEEP_EPI>(smem_u32(&tail->pbar[par]), parity);
+        else
+          mbar_wait_u32<TG_SLEEP_EPI>(smem_u32(&tail->pbar[par]), parity);
         TG_PROF_ADD(tail, 4);
       }
-      const float4 v = (lane < kConsumerWarps) ? tail->wpart[par][lane]
-                                               : make_float4(kNegInf, 0.f, 0.f, 0.f);
-      const Online cta = warp_merge(Online{v.x, v.y, v.z});
-      // the target logit, read straight from the still-resident chunk (raw, unclamped)
-      float czy = kNegInf;
-      if (vy >= sl.v0 && vy < sl.v1) {
-        const int off = vy - sl.v0;
-        RingIt at = pos0;
-        at.advance(off / kVecPerChunk);
-        czy = Pk<T>::elem(lds128(at.addr(rb) + uint32_t(off % kVecPerChunk) * 16), ye);
-      }
-      Online tot = cta;
-      float tzy = czy;
-      if constexpr (CL > 1) {
-        if (lane == 0) {
-          mbar_arrive_expect_tx(&tail->xbar[par], (CL - 1) * 16);
-          const uint32_t my_slot = smem_u32(&tail->xdata[par][rank]);
-          const uint32_t bar = smem_u32(&tail->xbar[par]);
+#ifdef TG_FUSED_PROF
+      const long long t_crit = clock64();
+      const long long t_xdone = t_crit;
+#endif
+      // all CL x warps partials, merged in a fixed lane order: lane 0 holds the
+      // same bits on every CTA of the cluster
+      constexpr int NP = CL * kConsumerWarps;
+      Online acc_p = {kNegInf, 0.f, 0.f};
 #pragma unroll
-          for (int r = 0; r < CL; ++r) {
-            if (r == int(rank)) continue;
-            st_async_v4(map_to_rank(my_slot, r), cta.m, cta.s, cta.t, czy, map_to_rank(bar, r));
-          }
-        }
-        {
-          TG_PROF_T0();
-          mbar_wait_cluster(&tail->xbar[par], parity);
-          TG_PROF_ADD(tail, 5);
-        }
-        tot = {kNegInf, 0.f, 0.f};
-        tzy = kNegInf;
-#pragma unroll
-        for (int r = 0; r < CL; ++r) {  // fixed rank order: identical result on every CTA
-          const float4 w = (r == int(rank)) ? make_float4(cta.m, cta.s, cta.t, czy)
-                                            : tail->xdata[par][r];
-          tot = online_merge(tot, Online{w.x, w.y, w.z});
-          tzy = fmaxf(tzy, w.w);
+      for (int i = 0; i < (NP + 31) / 32; ++i) {
+        const int j = lane + 32 * i;
+        if (j < NP) {
+          const float4 v = tail->wpart[par][j];
+          acc_p = online_merge(acc_p, Online{v.x, v.y, v.z});
         }
       }
+      const Online tot = warp_merge_first<(NP < 32 ? NP : 32)>(acc_p);
       if (lane == 0) {
-        const float lse = tot.m + logf(tot.s);
-        const float H = lse - tot.t / tot.s;
+        const float lse = tot.m + __logf(tot.s);
+        const float H = lse - __fdividef(tot.t, tot.s);
         const bool bad_target = (cur.flags & 2u) != 0;
         const float lp = tzy - lse;
         RowTerms o = meta_terms(P, cur, lp, H);
@@ -429,6 +526,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         }
         tail->bcast[par] = make_float4(o.s + o.h * (H - lse), o.h, lse, o.s);
         arrive_u32(smem_u32(&tail->bbar[par]));
+#ifdef TG_FUSED_PROF
+        tail->prof[7] += (unsigned long long)(clock64() - t_crit);
+        tail->prof[8] += (unsigned long long)(clock64() - t_xdone);
+#endif
         if (rank == 0) {  // outputs + statistics, after the broadcast
           P.lp[row] = lp;
           P.ent[row] = H;
@@ -454,7 +555,6 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
           sd[14] += 1.0;
         }
       }
-      pos0.advance(sl.nchunk);
     }
     // rank 0 of each cluster accumulated its rows; other ranks store zeros
     if (lane == 0) {
@@ -479,7 +579,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   } else {
     // ===================== consumer warps =====================
     RingIt pos0 = {0u};  // the current row's first chunk
-    Acc2 acc = acc_init();
+    Acc1 acc = acc_init();
     if (cid < NR) phase1_range<T>(acc, pos0, rb, sl, 0, pre, tid);  // first row's prefix
     int y_cur = (cid < NR) ? __ldg(&meta[cid].y) : 0;
     int64_t k = 0;
@@ -496,35 +596,49 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       Online o;
       {
         float s0, s1, t0, t1;
-        upk2(acc.s2, s0, s1);
-        upk2(acc.t2, t0, t1);
-        o = warp_merge(Online{acc.m, s0 + s1, t0 + t1});
+        upk2(acc.a.s2, s0, s1);
+        upk2(acc.a.t2, t0, t1);
+        const float sl_s = s0 + s1;
+        // a lane that saw no element of the row carries a stale m: neutral
+        o = warp_merge(Online{sl_s > 0.f ? acc.a.m : kNegInf, sl_s, t0 + t1});
       }
       if (lane == 0) {
-        tail->wpart[par][warp] = make_float4(o.m, o.s, o.t, 0.f);
+        // the warp partial goes to every CTA of the cluster (peers: DSMEM st.async
+        // completing tx bytes on their partials barrier), so each epilogue merges
+        // all CL x warps partials after a single wait
+        const int slot = int(rank) * kConsumerWarps + warp;
+        tail->wpart[par][slot] = make_float4(o.m, o.s, o.t, 0.f);
+        if constexpr (CL > 1) {
+          const uint32_t la = smem_u32(&tail->wpart[par][slot]);
+          const uint32_t lb = smem_u32(&tail->pbar[par]);
+#pragma unroll
+          for (int r = 0; r < CL; ++r)
+            if (r != int(rank)) st_async_v4(map_to_rank(la, r), o.m, o.s, o.t, 0.f, map_to_rank(lb, r));
+        }
         arrive_u32(smem_u32(&tail->pbar[par]));
       }
       // ---------------- phase 1 prefix of the next row (hides the epilogue) ----------
       RingIt npos = pos0;
       npos.advance(sl.nchunk);
-      acc = acc_init();
+      acc_new_row(acc);
       if (nrow < NR) phase1_range<T>(acc, npos, rb, sl, 0, pre, tid);
 
       // ---------------- phase 2: dz from the resident slice ----------------
       {
         TG_PROF_T0();
-        mbar_wait_u32(smem_u32(&tail->bbar[par]), uint32_t((k >> 1) & 1));
+        mbar_wait_u32<TG_SLEEP_BCAST>(smem_u32(&tail->bbar[par]), uint32_t((k >> 1) & 1));
         TG_PROF_ADD(tail, 1);
       }
       const float4 bc = tail->bcast[par];
       const float a = bc.x, hz = bc.y, s_t = bc.w;
       const float lseL = bc.z * kLog2e;
       const uint64_t nl2 = pk2(-lseL, -lseL), av2 = pk2(a, a), hz2 = pk2(hz, hz);
+      const uint32_t pf2 = TG_POLY2_MASK ? poly_floor2(bc.z) : 0u;
       char* dzrow = reinterpret_cast<char*>(P.dz) + row * P.ld_out * ESZ;
       if (hz == 0.f)
-        phase2_row<T, false>(sl, pos0, rb, dzrow, vy, ye, s_t, nl2, av2, hz2, tid, lane);
+        phase2_row<T, false>(sl, pos0, rb, dzrow, vy, ye, s_t, nl2, av2, hz2, pf2, tid, lane);
       else
-        phase2_row<T, true>(sl, pos0, rb, dzrow, vy, ye, s_t, nl2, av2, hz2, tid, lane);
+        phase2_row<T, true>(sl, pos0, rb, dzrow, vy, ye, s_t, nl2, av2, hz2, pf2, tid, lane);
       pos0 = npos;
       y_cur = y_next;
 #ifdef TG_FUSED_PROF
@@ -539,7 +653,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     cluster_sync_all();  // no CTA leaves while a peer may still st.async into it
 #ifdef TG_FUSED_PROF
   __syncthreads();
-  if (tid < 8) g_fused_prof[blockIdx.x][tid] = tail->prof[tid];
+  if (tid < 16) g_fused_prof[blockIdx.x][tid] = tail->prof[tid];
 #endif
 }
 
@@ -648,7 +762,7 @@ int fused_max_clusters(int dtype, int cl) {
 // profiling build: per-CTA counters of the last fused launch (see prof[] above)
 extern "C" int tg_debug_fused_prof(unsigned long long* out, int n_ctas) {
   if (n_ctas > 1024) n_ctas = 1024;
-  return int(cudaMemcpyFromSymbol(out, g_fused_prof, size_t(n_ctas) * 8 * sizeof(unsigned long long)));
+  return int(cudaMemcpyFromSymbol(out, g_fused_prof, size_t(n_ctas) * 16 * sizeof(unsigned long long)));
 }
 #endif
 

@@ -15,6 +15,10 @@
 
 namespace tg {
 
+// fast exp (ex2.approx based, ~2 ulp at |x| <= 20): on the fused epilogue's
+// latency-critical path
+#define TG_EXPF __expf
+
 struct RowTerms {
   float s, h;                     // gradient coefficients
   float l_pg, l_kl, l_ent, l_sft;  // weighted loss contributions
@@ -64,7 +68,7 @@ __device__ __forceinline__ RowTerms meta_terms(const KParams& P, const RowMeta& 
   if (P.pg == TG_PG_PPO_CLIP) {
     const float old = P.old_lp ? m.old : lp;
     const float logr = fminf(fmaxf(lp - old, -20.f), 20.f);
-    const float rho = expf(logr);
+    const float rho = TG_EXPF(logr);
     const float l1 = -A * rho;
     const float l2 = -A * fminf(fmaxf(rho, 1.f - P.clip_lo), 1.f + P.clip_hi);
     pg = fmaxf(l1, l2);
@@ -103,7 +107,7 @@ __device__ __forceinline__ RowTerms meta_terms(const KParams& P, const RowMeta& 
     } else if (P.kl == TG_KL_K3) {
       const float delta = ref - lp;
       const float dcl = fminf(fmaxf(delta, -20.f), 20.f);
-      const float ratio = expf(dcl);
+      const float ratio = TG_EXPF(dcl);
       const float raw = ratio - dcl - 1.f;
       klv = fminf(fmaxf(raw, -10.f), 10.f);
       dkl = (delta == dcl && raw == klv) ? 1.f - ratio : 0.f;

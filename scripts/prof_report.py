@@ -4,7 +4,9 @@ import sys
 
 import numpy as np
 
-NCW = 14  # consumer warps
+NCW = int(sys.argv[1]) if sys.argv[1].isdigit() else 14  # consumer warps
+if sys.argv[1].isdigit():
+    sys.argv.pop(1)
 for f in sys.argv[1:]:
     a = np.load(f).astype(np.float64)
     a = a[a[:, 2] > 0]
@@ -18,3 +20,6 @@ for f in sys.argv[1:]:
         per = a[:, i] / (NCW if i < 2 else 1)
         print(f"  {n:24s} {100 * (per / span).mean():6.2f} % of span "
               f"(min {100 * (per / span).min():.1f}, max {100 * (per / span).max():.1f})")
+    rows = a[:, 6]
+    print(f"  per row: span {(span / rows).mean():.0f} cyc, epilogue critical path "
+          f"{(a[:, 7] / rows).mean():.0f} cyc, of which after the exchange {(a[:, 8] / rows).mean():.0f}")
