@@ -78,6 +78,8 @@ struct FusedSmemTail {
   double stats[16];
 #ifdef TG_FUSED_PROF
   unsigned long long prof[16];
+  unsigned long long post_first[2], post_last[2];
+  unsigned long long post_t[2][kConsumerWarps];
 #endif
 };
 
@@ -91,6 +93,10 @@ struct FusedSmemTail {
 // prof[6] rows processed by the CTA
 // prof[7] epilogue critical path: partials complete -> broadcast
 // prof[8] epilogue: cluster exchange complete -> broadcast
+// prof[9] first local warp partial posted -> epilogue wakes (all partials in)
+// prof[10] first -> last local warp partial posted (intra-CTA skew)
+// prof[11..14] post lag behind the first local post, summed over the consumer
+//              warps of SM sub-partition 0..3 (warp % 4)
 #ifdef TG_FUSED_PROF
 __device__ unsigned long long g_fused_prof[1024][16];
 __device__ __forceinline__ FusedSmemTail* prof_tail() {
@@ -252,7 +258,7 @@ template <typename T, bool kHasH, bool kCheck>
 __device__ __forceinline__ void phase2_chunk(const RingIt& it, const RingBase& rb, int vbase,
                                              const Slice& sl, char* dzrow, int vy, int ye,
                                              float s_t, uint64_t nl2, uint64_t av2, uint64_t hz2,
-                                             uint32_t pf2, int tid) {
+                                             int tid) {
   constexpr int EPV = Vec<T>::N;
   char* dst = dzrow + int64_t(vbase + tid) * 16;
   const uint32_t a = it.addr(rb) + tid * 16;
@@ -261,7 +267,7 @@ __device__ __forceinline__ void phase2_chunk(const RingIt& it, const RingBase& r
     const int vec = vbase + g * kConsumers + tid;
     if (!kCheck || vec < sl.v1) {
       float d[EPV];
-      dz_vec<T, kHasH>(lds128(a + g * kConsumers * 16), d, nl2, av2, hz2, pf2);
+      dz_vec<T, kHasH>(lds128(a + g * kConsumers * 16), d, nl2, av2, hz2);
       bool done = false;
       if (kCheck) {
         if (vec == vy) {
@@ -290,17 +296,18 @@ __device__ __forceinline__ void phase2_chunk(const RingIt& it, const RingBase& r
 template <typename T, bool kHasH>
 __device__ __forceinline__ void phase2_row(const Slice& sl, RingIt it, const RingBase& rb,
                                            char* dzrow, int vy, int ye, float s_t, uint64_t nl2,
-                                           uint64_t av2, uint64_t hz2, uint32_t pf2, int tid,
-                                           int lane) {
+                                           uint64_t av2, uint64_t hz2, int tid, int lane) {
   int vbase = sl.v0;
   for (int j = 0; j < sl.nchunk; ++j) {
     const int vend = vbase + kVecPerChunk;
     const bool check = (vend > sl.v1) || (sl.tail_vec >= vbase && sl.tail_vec < vend) ||
                        (vy >= vbase && vy < vend);
     if (check)
-      phase2_chunk<T, kHasH, true>(it, rb, vbase, sl, dzrow, vy, ye, s_t, nl2, av2, hz2, pf2, tid);
+      phase2_chunk<T, kHasH, true>(it, rb, vbase, sl, dzrow, vy, ye, s_t, nl2, av2, hz2,
+                                               tid);
     else
-      phase2_chunk<T, kHasH, false>(it, rb, vbase, sl, dzrow, vy, ye, s_t, nl2, av2, hz2, pf2, tid);
+      phase2_chunk<T, kHasH, false>(it, rb, vbase, sl, dzrow, vy, ye, s_t, nl2, av2, hz2,
+                                                tid);
     __syncwarp();
     if (lane == 0) arrive_u32(it.empty(rb));
     it.next();
@@ -413,6 +420,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     fence_mbar_init();
 #ifdef TG_FUSED_PROF
     for (int i = 0; i < 16; ++i) tail->prof[i] = 0ull;
+    for (int i = 0; i < 2; ++i) {
+      tail->post_first[i] = ~0ull;
+      tail->post_last[i] = 0ull;
+    }
 #endif
   }
   if (CL > 1)
@@ -500,6 +511,14 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
 #ifdef TG_FUSED_PROF
       const long long t_crit = clock64();
       const long long t_xdone = t_crit;
+      if (lane == 0) {
+        tail->prof[9] += (unsigned long long)t_crit - tail->post_first[par];
+        tail->prof[10] += tail->post_last[par] - tail->post_first[par];
+        for (int w = 0; w < kConsumerWarps; ++w)
+          tail->prof[11 + (w & 3)] += tail->post_t[par][w] - tail->post_first[par];
+        tail->post_first[par] = ~0ull;
+        tail->post_last[par] = 0ull;
+      }
 #endif
       // all CL x warps partials, merged in a fixed lane order: lane 0 holds the
       // same bits on every CTA of the cluster
@@ -607,6 +626,12 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         // completing tx bytes on their partials barrier), so each epilogue merges
         // all CL x warps partials after a single wait
         const int slot = int(rank) * kConsumerWarps + warp;
+#ifdef TG_FUSED_PROF
+        const unsigned long long tpost = clock64();
+        atomicMin(&tail->post_first[par], tpost);
+        atomicMax(&tail->post_last[par], tpost);
+        tail->post_t[par][warp] = tpost;
+#endif
         tail->wpart[par][slot] = make_float4(o.m, o.s, o.t, 0.f);
         if constexpr (CL > 1) {
           const uint32_t la = smem_u32(&tail->wpart[par][slot]);
@@ -633,12 +658,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       const float a = bc.x, hz = bc.y, s_t = bc.w;
       const float lseL = bc.z * kLog2e;
       const uint64_t nl2 = pk2(-lseL, -lseL), av2 = pk2(a, a), hz2 = pk2(hz, hz);
-      const uint32_t pf2 = TG_POLY2_MASK ? poly_floor2(bc.z) : 0u;
       char* dzrow = reinterpret_cast<char*>(P.dz) + row * P.ld_out * ESZ;
       if (hz == 0.f)
-        phase2_row<T, false>(sl, pos0, rb, dzrow, vy, ye, s_t, nl2, av2, hz2, pf2, tid, lane);
+        phase2_row<T, false>(sl, pos0, rb, dzrow, vy, ye, s_t, nl2, av2, hz2, tid, lane);
       else
-        phase2_row<T, true>(sl, pos0, rb, dzrow, vy, ye, s_t, nl2, av2, hz2, pf2, tid, lane);
+        phase2_row<T, true>(sl, pos0, rb, dzrow, vy, ye, s_t, nl2, av2, hz2, tid, lane);
       pos0 = npos;
       y_cur = y_next;
 #ifdef TG_FUSED_PROF

@@ -184,64 +184,19 @@ __device__ __forceinline__ void accumulate(Acc2& acc, const uint4& u) {
   }
 }
 
-// 2^x of an fp32x2 pair on the FMA pipe (no MUFU), to take part of the ex2
-// load off the SFU: x = j + f with j = rint(x) (magic-number add), 2^f by a
-// degree-3 minimax polynomial on [-0.5, 0.5] (max relative error 7.5e-5, far
-// below the bf16 rounding of dz), 2^j added into the exponent field.
-// Valid for x in [-125, 127]: callers clamp the logits first.
-__device__ __forceinline__ uint64_t ex2x2_poly3(uint64_t x) {
-  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
-  const uint64_t t = add2(x, pk2(kMagic, kMagic));
-  const uint64_t j = add2(t, pk2(-kMagic, -kMagic));
-  const uint64_t f = fma2(j, pk2(-1.f, -1.f), x);
-  uint64_t p = fma2(pk2(0.0551716648042202f, 0.0551716648042202f), f,
-                    pk2(0.2426111251115799f, 0.2426111251115799f));
-  p = fma2(p, f, pk2(0.6932609677314758f, 0.6932609677314758f));
-  p = fma2(p, f, pk2(0.9999280571937561f, 0.9999280571937561f));
-  float t0, t1, p0, p1;
-  upk2(t, t0, t1);
-  upk2(p, p0, p1);
-  return pk2(__uint_as_float(__float_as_uint(p0) + (__float_as_uint(t0) << 23)),
-             __uint_as_float(__float_as_uint(p1) + (__float_as_uint(t1) << 23)));
-}
-
-// Words of each 16-byte bf16 vector whose phase-2 exponentials run on the FMA
-// pipe (bit w = 32-bit word w); the rest use MUFU ex2.
-#ifndef TG_POLY2_MASK
-#define TG_POLY2_MASK 0
-#endif
-
-// packed bf16x2 lower bound for the polynomial words: lse - 80, rounded up, so
-// that (z - lse) log2e >= -116 > -125 for every clamped logit (e^-80 ~ 2e-35:
-// the clamp changes nothing visible in a bf16 dz)
-__device__ __forceinline__ uint32_t poly_floor2(float lse) {
-  const uint32_t b = __float_as_uint(lse - 80.0f);
-  uint32_t h = b >> 16;                         // truncation toward zero
-  if (!(b & 0x80000000u) && (b & 0xffffu)) ++h;  // positive: round up
-  return h | (h << 16);
-}
-
 // dz of one vector: p * (a + hz * z), p = 2^(z log2e - lse log2e).  Without the
 // entropy term (kHasH = false) -inf logits need no clamp: p = 0 exactly.
 template <typename T, bool kHasH>
 __device__ __forceinline__ void dz_vec(uint4 u, float (&d)[Vec<T>::N], uint64_t nl2, uint64_t av2,
-                                       uint64_t hz2, uint32_t pfloor2 = 0u) {
+                                       uint64_t hz2) {
   const uint64_t l2e2 = pk2(kLog2e, kLog2e);
   if (kHasH) Pk<T>::clamp(u);
 #pragma unroll
   for (int w = 0; w < Vec<T>::N / 2; ++w) {
-    constexpr bool kBf = sizeof(T) == 2;
-    const bool poly = kBf && ((TG_POLY2_MASK >> w) & 1);
-    uint64_t p;
-    if (poly) {
-      uint32_t* uw = reinterpret_cast<uint32_t*>(&u);
-      uw[w] = bmax2(uw[w], pfloor2);
-      p = ex2x2_poly3(fma2(pair<T>(u, w), l2e2, nl2));
-    } else {
-      p = ex2x2(fma2(pair<T>(u, w), l2e2, nl2));
-    }
     const uint64_t x = pair<T>(u, w);
-    upk2(kHasH ? mul2(p, fma2(hz2, x, av2)) : mul2(p, av2), d[2 * w], d[2 * w + 1]);
+    const uint64_t p = ex2x2(fma2(x, l2e2, nl2));
+    const uint64_t r = kHasH ? mul2(p, fma2(hz2, x, av2)) : mul2(p, av2);
+    upk2(r, d[2 * w], d[2 * w + 1]);
   }
 }
 

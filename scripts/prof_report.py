@@ -22,4 +22,7 @@ for f in sys.argv[1:]:
               f"(min {100 * (per / span).min():.1f}, max {100 * (per / span).max():.1f})")
     rows = a[:, 6]
     print(f"  per row: span {(span / rows).mean():.0f} cyc, epilogue critical path "
-          f"{(a[:, 7] / rows).mean():.0f} cyc, of which after the exchange {(a[:, 8] / rows).mean():.0f}")
+          f"{(a[:, 7] / rows).mean():.0f} cyc; first local partial -> epilogue wake "
+          f"{(a[:, 9] / rows).mean():.0f} cyc, intra-CTA post skew {(a[:, 10] / rows).mean():.0f} cyc")
+    lag = [(a[:, 11 + q] / rows / (NCW / 4)).mean() for q in range(4)]
+    print("  mean post lag by SM sub-partition (warp % 4): " + ", ".join(f"{x:.0f}" for x in lag))
