@@ -14,6 +14,7 @@
  *   algorithms.loss_dpo             algorithms.py:277-315                   TG_PG_DPO
  *   algorithms.combine_reports      algorithms.py:368-379                   stats[] (sums + group count)
  *   algorithms.experience_logprob   algorithms.py:81-85                     tg_logprob_fwd
+ *   (hidden states, no logits)      policy.py:194-212 behind an LM head     tg_lmhead_logprob_fwd
  *   policy.logprob / grad_logprob   policy.py:194-212, 253-270              (fused into both)
  *   policy.scored_states            policy.py:181-191 (toy-table adapter)   tg_scored_states (host)
  *   ExperienceBuffer.sample_batch   buffer.py:240-264 (group indexing)      tg_group_by_task (host)
@@ -184,6 +185,22 @@ int tg_loss_fwd_bwd(const TgBatch* batch, const TgConfig* cfg, TgOut* out,
    (algorithms.py:81-85) for old / ref logprob recompute.  stats may be NULL. */
 int tg_logprob_fwd(const TgBatch* batch, TgOut* out, void* workspace,
                    size_t workspace_bytes, void* stream);
+
+/* Fused LM-head + log-softmax forward on the tensor cores:
+   z = hidden [n_rows, dim] x weight [vocab, dim]^T (bf16, row-major, pitches
+   ld_hidden / ld_weight elements, multiples of 8; dim a multiple of 64) is
+   folded tile by tile into per-row lse / entropy and lp = z[target] - lse
+   without writing the logits.  Replaces policy.logprob (policy.py:194-212)
+   when the caller holds hidden states instead of logits.  lp / target may be
+   NULL (entropy / lse only).  fp32 accumulation.  When the row blocks alone
+   cannot fill the SMs the vocabulary is split across CTAs and merged in a
+   fixed order: the workspace (tg_lmhead_workspace_size bytes, 16-byte
+   aligned; 0 bytes for large n_rows) holds the per-split partials. */
+size_t tg_lmhead_workspace_size(int64_t n_rows, int64_t vocab);
+int tg_lmhead_logprob_fwd(const void* hidden, int64_t ld_hidden, const void* weight,
+                          int64_t ld_weight, int64_t n_rows, int64_t vocab, int64_t dim,
+                          const int32_t* target, float* lp, float* entropy, float* lse,
+                          void* workspace, size_t workspace_bytes, void* stream);
 
 /* Which kernel route tg_loss_fwd_bwd takes for this input: 1 = fused single
    pass (4V bytes/row), 2 = forward + backward streaming (6V), 3 = coupled. */

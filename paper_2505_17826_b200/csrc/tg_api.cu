@@ -31,6 +31,13 @@ cudaError_t launch_fused(const KParams& P, const void* meta, int cl, int n_slots
                          int prefetch_rows,
                          cudaStream_t stream);
 int fused_chunk_bytes();
+cudaError_t launch_lmhead_logprob(const void* hidden, int64_t ld_hidden, const void* weight,
+                                  int64_t ld_weight, int64_t n_rows, int64_t vocab, int64_t dim,
+                                  const int32_t* target, float* lp, float* ent, float* lse,
+                                  void* workspace, size_t workspace_bytes, int n_sms,
+                                  cudaStream_t stream);
+size_t lm_workspace_bytes(int64_t n_rows, int64_t vocab, int n_sms);
+int lm_split(int64_t n_rows, int64_t vocab, int n_sms);
 cudaError_t launch_fused_l2(const KParams& P, const void* meta, int n_ctas, int prefetch,
                             cudaStream_t st);
 int l2_threads();
@@ -477,6 +484,51 @@ int tg_logprob_fwd(const TgBatch* b, TgOut* o, void* workspace, size_t workspace
     count_launches(1);
   }
   return check_cuda("tg_logprob_fwd");
+}
+
+int tg_lmhead_logprob_fwd(const void* hidden, int64_t ld_hidden, const void* weight,
+                          int64_t ld_weight, int64_t n_rows, int64_t vocab, int64_t dim,
+                          const int32_t* target, float* lp, float* entropy, float* lse,
+                          void* workspace, size_t workspace_bytes, void* stream) {
+  if (n_rows < 0 || vocab < 1 || dim < 1)
+    return fail(TG_EINVAL, "bad sizes (rows %lld, vocab %lld, dim %lld)", (long long)n_rows,
+                (long long)vocab, (long long)dim);
+  if (dim % 64 != 0) return fail(TG_EINVAL, "dim must be a multiple of 64, got %lld", (long long)dim);
+  if (ld_hidden < dim || ld_weight < dim)
+    return fail(TG_EINVAL, "row pitch below dim (ld_hidden %lld, ld_weight %lld)",
+                (long long)ld_hidden, (long long)ld_weight);
+  if (ld_hidden % 8 != 0 || ld_weight % 8 != 0)
+    return fail(TG_EINVAL, "row pitches must be multiples of 8 elements (16 bytes)");
+  if (vocab > (int64_t(1) << 31) - 256 || n_rows > (int64_t(1) << 31) - 128)
+    return fail(TG_EINVAL, "vocab / rows too large");
+  if (n_rows == 0) return TG_OK;
+  if (!hidden || !weight || !lse || !entropy)
+    return fail(TG_EINVAL, "hidden, weight, entropy and lse are required");
+  if (!aligned16(hidden) || !aligned16(weight))
+    return fail(TG_EINVAL, "hidden and weight must be 16-byte aligned");
+  if (lp && !target) return fail(TG_EINVAL, "lp requires target");
+  const DevInfo d = dev_info();
+  const int sms = d.sms > 0 ? d.sms : 148;
+  const size_t need = lm_workspace_bytes(n_rows, vocab, sms);
+  if (need > 0 && (!workspace || workspace_bytes < need))
+    return fail(TG_EWORKSPACE, "workspace too small: need %zu bytes, got %zu", need,
+                workspace_bytes);
+  if (need > 0 && !aligned16(workspace)) return fail(TG_EINVAL, "workspace must be 16-byte aligned");
+  cudaGetLastError();
+  cudaError_t e = launch_lmhead_logprob(hidden, ld_hidden, weight, ld_weight, n_rows, vocab, dim,
+                                        target, lp, entropy, lse, workspace, workspace_bytes, sms,
+                                        reinterpret_cast<cudaStream_t>(stream));
+  if (e == cudaErrorNotSupported)
+    return fail(TG_EUNSUPPORTED, "cuTensorMapEncodeTiled is unavailable (driver too old)");
+  count_launches(lm_split(n_rows, vocab, sms) > 1 ? 2 : 1);
+  if (e != cudaSuccess) return fail(TG_ECUDA, "tg_lmhead_logprob_fwd: %s", cudaGetErrorString(e));
+  return TG_OK;
+}
+
+size_t tg_lmhead_workspace_size(int64_t n_rows, int64_t vocab) {
+  if (n_rows <= 0 || vocab <= 0) return 0;
+  const DevInfo d = dev_info();
+  return lm_workspace_bytes(n_rows, vocab, d.sms > 0 ? d.sms : 148);
 }
 
 const char* tg_strerror(int code) {

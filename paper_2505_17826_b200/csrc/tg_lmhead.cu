@@ -1,0 +1,473 @@
+// tg_lmhead.cu -- K7: fused LM-head + log-softmax forward on the 5th-gen tensor cores.
+//
+// the logits "producer".  For hidden states X [T, d] and the
+// LM-head W [V, d] (both bf16, K-contiguous) it computes per row
+//     lse_t = log sum_v exp(z_tv),  lp_t = z_{t,y_t} - lse_t,  H_t = lse_t - sum_v p_tv z_tv
+// with z = X W^T, without ever writing the [T, V] logits to HBM: the logits of a
+// 128 x 256 tile live only in TMEM and are folded into per-row online
+// (max, sum e, sum e z) state by the epilogue warps.  This is the forward-only
+// logprob service of §8(f-3) (policy.logprob, policy.py:194-212, for old / ref
+// logprob recompute) moved in front of the GEMM.
+//
+// Design (sm_100a, one CTA per SM, persistent over 128-row blocks):
+//  * warp 0, one lane: TMA producer.  For every (row block, vocab tile, k-block)
+//    it loads the X tile [128 x 64] and the W tile [256 x 64] (128-byte swizzle)
+//    into a 4-stage shared-memory ring (48 KB per stage), full / empty mbarriers.
+//  * warp 1, one lane: MMA issuer.  tcgen05.mma.cta_group::1.kind::f16
+//    (M = 128, N = 256, K = 16, bf16 x bf16 -> fp32) into one of two TMEM
+//    accumulators (2 x 256 columns); tcgen05.commit frees ring slots and
+//    signals the epilogue when a tile's accumulation is complete.
+//  * warp 2: TMEM allocation / deallocation (512 columns).
+//  * warps 4..7: epilogue.  Warp q reads TMEM lanes [32q, 32q + 32) (row = lane)
+//    with tcgen05.ld.32x32b.x32, updates its row's online state in packed fp32x2
+//    arithmetic, gathers the target logit, and hands the accumulator back; the
+//    next tile's MMAs already run into the other accumulator.
+//  Rows past T and vocabulary columns past V come in as TMA zero fill and are
+//  masked in the epilogue.
+#include "tg_common.cuh"
+#include "tg_vecmath.cuh"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+namespace tg {
+
+constexpr int LM_BM = 128;                       // rows per tile (UMMA M)
+constexpr int LM_BN = 256;                       // vocabulary columns per tile (UMMA N)
+constexpr int LM_BK = 64;                        // K per stage: 64 bf16 = one 128-byte swizzle row
+constexpr int LM_UK = 16;                        // K per tcgen05.mma (kind::f16)
+constexpr int LM_STAGES = 4;
+constexpr int LM_A_BYTES = LM_BM * LM_BK * 2;    // 16 KB
+constexpr int LM_B_BYTES = LM_BN * LM_BK * 2;    // 32 KB
+constexpr int LM_STAGE_BYTES = LM_A_BYTES + LM_B_BYTES;
+constexpr int LM_THREADS = 256;                  // 8 warps
+constexpr int LM_EPI_WARP0 = 4;
+constexpr uint32_t LM_TMEM_COLS = 512;           // 2 accumulators x 256 fp32 columns
+
+struct LmParams {
+  int64_t n_rows, vocab, dim;
+  int n_split;            // vocabulary splits per row block (> 1: partials + merge kernel)
+  float4* partial;        // [n_split, T] (m, sum e, sum e z, z_target) when n_split > 1
+  const int32_t* target;  // [T] (may be null: lp not produced)
+  float* lp;              // [T]
+  float* ent;             // [T]
+  float* lse;             // [T]
+};
+
+struct LmSmemTail {
+  uint64_t full[LM_STAGES];
+  uint64_t empty[LM_STAGES];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint32_t tmem_base;
+};
+
+size_t lm_smem_bytes() { return size_t(LM_STAGES) * LM_STAGE_BYTES + sizeof(LmSmemTail) + 1024; }
+
+// ---- PTX wrappers -------------------------------------------------------------
+
+__device__ __forceinline__ void lm_tma_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                          uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void lm_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void lm_wait(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+__device__ __forceinline__ void lm_wait_sleep(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) __nanosleep(32);
+}
+
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+// K-major operand tile with 128-byte swizzle: rows of 128 B, 8-row groups 1 KB
+// apart (SBO = 1024 B), LBO unused (1), descriptor version 1, layout type 2.
+__device__ __forceinline__ uint64_t lm_sw128_desc(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= uint64_t((smem_addr >> 4) & 0x3FFFu);
+  d |= uint64_t(1u) << 16;             // leading byte offset (unused for swizzled K-major)
+  d |= uint64_t(1024u >> 4) << 32;     // stride byte offset: 8 rows x 128 B
+  d |= uint64_t(1u) << 46;             // descriptor version (sm_100)
+  d |= uint64_t(2u) << 61;             // SWIZZLE_128B
+  return d;
+}
+
+// instruction descriptor: bf16 x bf16 -> fp32, both K-major, M = 128, N = 256
+constexpr uint32_t lm_idesc() {
+  return (1u << 4)                      // D format fp32
+         | (1u << 7)                    // A format bf16
+         | (1u << 10)                   // B format bf16
+         | (uint32_t(LM_BN >> 3) << 17)  // N
+         | (uint32_t(LM_BM >> 4) << 24);  // M
+}
+
+__device__ __forceinline__ void lm_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void lm_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+
+// 32 consecutive fp32 columns of this thread's TMEM lane
+__device__ __forceinline__ void lm_tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ---- the kernel -----------------------------------------------------------------
+
+__global__ void __launch_bounds__(LM_THREADS, 1)
+    k_lmhead_logprob(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                     const LmParams P) {
+  extern __shared__ __align__(1024) unsigned char lm_smem_raw[];
+  // 1 KB alignment for the 128-byte swizzle atoms
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(lm_smem_raw) + 1023) & ~uintptr_t(1023));
+  LmSmemTail* tail = reinterpret_cast<LmSmemTail*>(smem + size_t(LM_STAGES) * LM_STAGE_BYTES);
+  const uint32_t ring = smem_u32(smem);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t T = P.n_rows;
+  const int V = int(P.vocab);
+  const int n_mb = int((T + LM_BM - 1) / LM_BM);
+  const int n_nt = (V + LM_BN - 1) / LM_BN;
+  // work unit u = (row block u / n_split, vocabulary split u % n_split)
+  const int n_split = P.n_split;
+  const int n_units = n_mb * n_split;
+  auto unit_tiles = [&](int u, int& mb, int& nt0, int& nt1) {
+    mb = u / n_split;
+    const int sp = u - mb * n_split;
+    nt0 = int((int64_t(sp) * n_nt) / n_split);
+    nt1 = int((int64_t(sp + 1) * n_nt) / n_split);
+  };
+  const int n_kb = int(P.dim / LM_BK);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < LM_STAGES; ++i) {
+      mbar_init(&tail->full[i], 1);
+      mbar_init(&tail->empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tail->tfull[i], 1);
+      mbar_init(&tail->tempty[i], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tail->tmem_base)),
+                 "r"(LM_TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tail->tmem_base;
+
+  if (warp == 0) {
+    // ============================ TMA producer ============================
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
+      uint32_t stage = 0, phase = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        int mb, nt0, nt1;
+        unit_tiles(u, mb, nt0, nt1);
+        for (int nt = nt0; nt < nt1; ++nt) {
+          for (int kb = 0; kb < n_kb; ++kb) {
+            lm_wait(smem_u32(&tail->empty[stage]), phase ^ 1u);
+            const uint32_t fb = smem_u32(&tail->full[stage]);
+            lm_expect_tx(fb, LM_STAGE_BYTES);
+            const uint32_t a = ring + stage * LM_STAGE_BYTES;
+            lm_tma_2d(a, &tmX, kb * LM_BK, mb * LM_BM, fb);
+            lm_tma_2d(a + LM_A_BYTES, &tmW, kb * LM_BK, nt * LM_BN, fb);
+            if (++stage == LM_STAGES) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ============================ MMA issuer ============================
+    if (lane == 0) {
+      constexpr uint32_t idesc = lm_idesc();
+      uint32_t stage = 0, phase = 0, tile = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        int mb, nt0, nt1;
+        unit_tiles(u, mb, nt0, nt1);
+        for (int nt = nt0; nt < nt1; ++nt, ++tile) {
+          const uint32_t acc = tile & 1u, acc_phase = (tile >> 1) & 1u;
+          lm_wait(smem_u32(&tail->tempty[acc]), acc_phase ^ 1u);
+          tc_fence_after();
+          const uint32_t d = tmem + acc * LM_BN;
+          for (int kb = 0; kb < n_kb; ++kb) {
+            lm_wait(smem_u32(&tail->full[stage]), phase);
+            tc_fence_after();
+            const uint32_t a = ring + stage * LM_STAGE_BYTES;
+            const uint64_t ad = lm_sw128_desc(a), bd = lm_sw128_desc(a + LM_A_BYTES);
+#pragma unroll
+            for (int k = 0; k < LM_BK / LM_UK; ++k)  // +32 bytes along K per step
+              lm_mma(d, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc, (kb | k) != 0);
+            lm_commit(smem_u32(&tail->empty[stage]));
+            if (++stage == LM_STAGES) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+          lm_commit(smem_u32(&tail->tfull[acc]));
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= LM_EPI_WARP0) {
+    // ============================ epilogue ============================
+    const int q = warp & 3;  // TMEM lane quadrant of this warp
+    const uint32_t lane_base = uint32_t(32 * q) << 16;
+    const uint64_t l2e2 = pk2(kLog2e, kLog2e);
+    uint32_t tile = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      int mb, nt0, nt1;
+      unit_tiles(u, mb, nt0, nt1);
+      const int64_t row = int64_t(mb) * LM_BM + 32 * q + lane;
+      const int y = (row < T && P.target) ? P.target[row] : -1;
+      float m = -1.0e30f, zy = kNegInf;
+      uint64_t s2 = pk2(0.f, 0.f), t2 = pk2(0.f, 0.f);
+      for (int nt = nt0; nt < nt1; ++nt, ++tile) {
+        const uint32_t acc = tile & 1u, acc_phase = (tile >> 1) & 1u;
+        lm_wait_sleep(smem_u32(&tail->tfull[acc]), acc_phase);
+        tc_fence_after();
+        const int col_tile = nt * LM_BN;
+        // two-level sums (32-column chunk, then tile) keep the fp32 rounding of
+        // the ~V/2 terms per lane near (32 + 8 + V/256) ulp instead of V/2 ulp
+        uint64_t ts2 = pk2(0.f, 0.f), tt2 = pk2(0.f, 0.f);
+#pragma unroll 1
+        for (int c = 0; c < LM_BN; c += 32) {
+          float v[32];
+          lm_tmem_ld32(tmem + lane_base + acc * LM_BN + uint32_t(c), v);
+          const int col0 = col_tile + c;
+          if (col0 + 32 > V) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (col0 + i >= V) v[i] = -1.0e30f;
+          }
+          if (y >= col0 && y < col0 + 32) {
+            // predicated selects (an indexed read would push v[] to local memory)
+            const int yo = y - col0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              asm("{\n\t.reg .pred p;\n\tsetp.eq.s32 p, %1, %2;\n\tselp.f32 %0, %3, %0, p;\n\t}"
+                  : "+f"(zy)
+                  : "r"(yo), "r"(i), "f"(v[i]));
+          }
+          float cm = v[0];
+#pragma unroll
+          for (int i = 1; i < 32; ++i) cm = fmaxf(cm, v[i]);
+          if (cm > m) {  // exact running max (rescale the sums)
+            const float sc = ex2((m - cm) * kLog2e);
+            const uint64_t sc2 = pk2(sc, sc);
+            s2 = mul2(s2, sc2);
+            t2 = mul2(t2, sc2);
+            ts2 = mul2(ts2, sc2);
+            tt2 = mul2(tt2, sc2);
+            m = cm;
+          }
+          const float nmL = -m * kLog2e;
+          const uint64_t nm2 = pk2(nmL, nmL);
+          uint64_t cs2, ct2;
+          {
+            const uint64_t x = pk2(v[0], v[1]);
+            cs2 = ex2x2(fma2(x, l2e2, nm2));
+            ct2 = mul2(cs2, x);
+          }
+#pragma unroll
+          for (int i = 2; i < 32; i += 2) {
+            const uint64_t x = pk2(v[i], v[i + 1]);
+            const uint64_t p = ex2x2(fma2(x, l2e2, nm2));
+            cs2 = add2(cs2, p);
+            ct2 = fma2(p, x, ct2);
+          }
+          ts2 = add2(ts2, cs2);
+          tt2 = add2(tt2, ct2);
+        }
+        s2 = add2(s2, ts2);
+        t2 = add2(t2, tt2);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tail->tempty[acc]);
+      }
+      if (row < T) {
+        float s0, s1, t0, t1;
+        upk2(s2, s0, s1);
+        upk2(t2, t0, t1);
+        const float s = s0 + s1, t = t0 + t1;
+        if (n_split > 1) {
+          P.partial[int64_t(u - mb * n_split) * T + row] = make_float4(m, s, t, zy);
+        } else {
+          const float l = m + logf(s);
+          P.lse[row] = l;
+          P.ent[row] = l - t / s;
+          if (P.lp) P.lp[row] = (y >= 0 && y < V) ? zy - l : kNegInf;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(LM_TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// fixed-order merge of the vocabulary-split partials of each row
+__global__ void k_lmhead_merge(const LmParams P) {
+  const int64_t row = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (row >= P.n_rows) return;
+  Online o = {kNegInf, 0.f, 0.f};
+  float zy = kNegInf;
+  for (int sp = 0; sp < P.n_split; ++sp) {
+    const float4 w = P.partial[int64_t(sp) * P.n_rows + row];
+    o = online_merge(o, Online{w.x, w.y, w.z});
+    zy = fmaxf(zy, w.w);
+  }
+  const float l = o.m + logf(o.s);
+  P.lse[row] = l;
+  P.ent[row] = l - o.t / o.s;
+  if (P.lp) {
+    const int y = P.target[row];
+    P.lp[row] = (y >= 0 && y < P.vocab) ? zy - l : kNegInf;
+  }
+}
+
+// Vocabulary splits per 128-row block: enough work units to fill the SMs in
+// whole waves (small row counts would otherwise leave SMs idle).
+int lm_split(int64_t n_rows, int64_t vocab, int n_sms) {
+  const int64_t n_mb = (n_rows + LM_BM - 1) / LM_BM;
+  const int64_t n_nt = (vocab + LM_BN - 1) / LM_BN;
+  int best = 1;
+  double best_eff = 0.0;
+  for (int sp = 1; sp <= 16 && sp <= n_nt; ++sp) {
+    const int64_t units = n_mb * sp;
+    const int64_t waves = (units + n_sms - 1) / n_sms;
+    const double eff = double(units) / double(waves * n_sms);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = sp;
+    }
+  }
+  return best;
+}
+
+size_t lm_workspace_bytes(int64_t n_rows, int64_t vocab, int n_sms) {
+  const int sp = lm_split(n_rows, vocab, n_sms);
+  return sp > 1 ? size_t(sp) * size_t(n_rows) * sizeof(float4) : 0;
+}
+
+// ---- host side --------------------------------------------------------------------
+
+static PFN_cuTensorMapEncodeTiled_v12000 lm_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// bf16 [rows, ld] row-major, box [box_rows, 64] with the 128-byte swizzle
+static bool lm_make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld,
+                        uint32_t box_rows) {
+  auto enc = lm_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+  cuuint64_t strides[1] = {cuuint64_t(ld) * 2};
+  cuuint32_t box[2] = {cuuint32_t(LM_BK), box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// returns a cudaError_t; cudaErrorNotSupported when the driver entry point is missing
+cudaError_t launch_lmhead_logprob(const void* hidden, int64_t ld_hidden, const void* weight,
+                                  int64_t ld_weight, int64_t n_rows, int64_t vocab, int64_t dim,
+                                  const int32_t* target, float* lp, float* ent, float* lse,
+                                  void* workspace, size_t workspace_bytes, int n_sms,
+                                  cudaStream_t stream) {
+  CUtensorMap mx, mw;
+  if (!lm_make_map(&mx, hidden, n_rows, dim, ld_hidden, LM_BM)) return cudaErrorNotSupported;
+  if (!lm_make_map(&mw, weight, vocab, dim, ld_weight, LM_BN)) return cudaErrorNotSupported;
+  LmParams P;
+  P.n_rows = n_rows;
+  P.vocab = vocab;
+  P.dim = dim;
+  P.target = target;
+  P.lp = lp;
+  P.ent = ent;
+  P.lse = lse;
+  P.n_split = lm_split(n_rows, vocab, n_sms);
+  P.partial = reinterpret_cast<float4*>(workspace);
+  if (P.n_split > 1 && (!workspace || workspace_bytes < lm_workspace_bytes(n_rows, vocab, n_sms)))
+    return cudaErrorInvalidValue;
+  const size_t smem = lm_smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(k_lmhead_logprob,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  const int64_t units = ((n_rows + LM_BM - 1) / LM_BM) * P.n_split;
+  const int grid = int(units < n_sms ? units : n_sms);
+  k_lmhead_logprob<<<grid, LM_THREADS, smem, stream>>>(mx, mw, P);
+  if (P.n_split > 1) k_lmhead_merge<<<int((n_rows + 255) / 256), 256, 0, stream>>>(P);
+  return cudaGetLastError();
+}
+
+}  // namespace tg

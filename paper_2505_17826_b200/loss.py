@@ -222,3 +222,44 @@ def logprob_fwd(batch: PackedBatch, stream: Optional[torch.cuda.Stream] = None):
         N.check(L.tg_logprob_fwd(ctypes.byref(cb), ctypes.byref(co), ws.data_ptr(), ws.numel(),
                                  s.cuda_stream))
     return lp, ent, lse, seq_lp
+
+
+def lmhead_logprob_fwd(hidden: torch.Tensor, weight: torch.Tensor,
+                       target: Optional[torch.Tensor] = None,
+                       stream: Optional[torch.cuda.Stream] = None):
+    """Fused LM-head + log-softmax forward on the tensor cores
+    (``tg_lmhead_logprob_fwd``): for hidden [T, d] and weight [V, d] (bf16,
+    d a multiple of 64) returns per-row ``(lp, entropy, lse)`` of
+    ``z = hidden @ weight.T`` without materialising the [T, V] logits
+    (policy.logprob, policy.py:194-212, behind an LM head).  ``lp`` is None
+    when no target is given."""
+    if hidden.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
+        raise TypeError("hidden and weight must be bfloat16")
+    if hidden.dim() != 2 or weight.dim() != 2 or hidden.shape[1] != weight.shape[1]:
+        raise ValueError(f"shape mismatch: hidden {tuple(hidden.shape)}, weight "
+                         f"{tuple(weight.shape)}")
+    if not hidden.is_cuda or hidden.device != weight.device:
+        raise ValueError("hidden and weight must be on the same CUDA device")
+    if hidden.stride(1) != 1 or weight.stride(1) != 1:
+        raise ValueError("hidden and weight need unit stride along d")
+    L = N.lib()
+    dev = hidden.device
+    T, d = hidden.shape
+    V = weight.shape[0]
+    f32 = dict(dtype=torch.float32, device=dev)
+    ent, lse = torch.empty(T, **f32), torch.empty(T, **f32)
+    lp = tgt = None
+    if target is not None:
+        tgt = target.to(device=dev, dtype=torch.int32).contiguous()
+        if tgt.shape != (T,):
+            raise ValueError(f"target must have shape ({T},)")
+        lp = torch.empty(T, **f32)
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    with torch.cuda.device(dev):
+        nbytes = L.tg_lmhead_workspace_size(T, V)
+        ws = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
+        N.check(L.tg_lmhead_logprob_fwd(
+            hidden.data_ptr(), hidden.stride(0), weight.data_ptr(), weight.stride(0), T, V, d,
+            tgt.data_ptr() if tgt is not None else None, lp.data_ptr() if lp is not None else None,
+            ent.data_ptr(), lse.data_ptr(), ws.data_ptr(), ws.numel(), s.cuda_stream))
+    return lp, ent, lse

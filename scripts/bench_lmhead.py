@@ -1,0 +1,73 @@
+"""Throughput of the fused LM-head logprob forward (tg_lmhead_logprob_fwd) at
+Qwen2.5 shapes: TFLOP/s of the logits GEMM (2 T V d) against the measured bf16
+peak, with cuBLAS (torch.matmul into materialised logits) timed beside it.
+
+    python scripts/bench_lmhead.py [--rows 16384] [--dim 1536] [--vocab 151936]
+"""
+import argparse
+import json
+import sys
+from pathlib import Path
+
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+from paper_2505_17826_b200 import lmhead_logprob_fwd, logprob_fwd, pack_arrays  # noqa: E402
+
+
+def timed(fn, reps=10):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--rows", type=int, default=16384)
+    p.add_argument("--dim", type=int, default=1536)
+    p.add_argument("--vocab", type=int, default=151936)
+    a = p.parse_args()
+    T, d, V = a.rows, a.dim, a.vocab
+    h = torch.randn(T, d, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(V, d, device="cuda") / d ** 0.5).to(torch.bfloat16)
+    y = torch.randint(0, V, (T,), device="cuda", dtype=torch.int32)
+    flops = 2.0 * T * V * d
+    ms = timed(lambda: lmhead_logprob_fwd(h, w, y))
+    ms_cublas = timed(lambda: torch.matmul(h, w.T))
+    # unfused baseline: cuBLAS writes the bf16 logits, the streaming logprob kernel reads them
+    logits = torch.matmul(h, w.T)
+    import numpy as np
+    batch = pack_arrays(logits, y.cpu().numpy(), [T], [1], np.zeros(1, np.float32))
+
+    def unfused():
+        torch.matmul(h, w.T, out=logits)
+        logprob_fwd(batch)
+    ms_unfused = timed(unfused)
+    lp_f, _, lse_f = lmhead_logprob_fwd(h, w, y)
+    lp_u, _, lse_u, _ = logprob_fwd(batch)
+    dlse = float((lse_f - lse_u).abs().max())
+    peak = None
+    try:
+        peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["bf16_tflops"]
+    except Exception:
+        pass
+    out = {"kernel": "k_lmhead_logprob", "rows": T, "dim": d, "vocab": V, "ms": ms,
+           "tflops": flops / ms / 1e9, "peak_tflops": peak,
+           "frac": (flops / ms / 1e9 / peak) if peak else None,
+           "cublas_gemm_only_ms": ms_cublas, "cublas_tflops": flops / ms_cublas / 1e9,
+           "tokens_per_s": T / ms * 1e3, "unfused_cublas_plus_logprob_ms": ms_unfused,
+           "speedup_vs_unfused": ms_unfused / ms,
+           "max_abs_lse_diff_vs_unfused_bf16_logits": dlse}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
