@@ -49,6 +49,18 @@ V = 151936
 BUMP = 13.5
 ALGO_BYTES_PER_ROW = 4 * V + 24  # 2V read + 2V write + 24 B side data
 WORKLOAD = "grpo_ppo_clip_k3_token_mean_qwen2.5_1.5b_shapes"
+VARIANT_WORKLOAD = {
+    "grpo": WORKLOAD,
+    "c3": "configs[2] per-GPU shard: ppo_clip_k3_entropy, 16 prompts x 8 x 4096 tokens "
+          "(128 x 8 over 8 GPUs)",
+    "c4": "configs[3]: mixed GRPO + SFT NLL (50/50 sequences) at configs[1] shapes",
+    "c5": "configs[4] per-GPU shard: long-CoT 32 groups x 16 ragged responses <= 8192, "
+          "10 % interior mask-false spans, row_index gather (256 x 16 over 8 GPUs)",
+}
+_BASE_LOSS = "grpo adv + ppo_clip(0.2,0.28) + low_var_kl(0.001) + token-mean"
+VARIANT_LOSS = {"grpo": _BASE_LOSS, "c3": _BASE_LOSS + " + entropy(0.001)",
+                "c4": _BASE_LOSS + " on RL seqs + SFT NLL (weight 1) on expert seqs",
+                "c5": _BASE_LOSS}
 
 
 def parse():
@@ -67,10 +79,18 @@ def parse():
     p.add_argument("--cpu-rows", type=int, default=256)
     p.add_argument("--quiet", action="store_true")
     p.add_argument("--variant", default="grpo",
-                   choices=["grpo", "grpo_two_pass", "opmd_kimi", "opmd_pairwise", "sft"],
-                   help="loss variant (the headline metric is 'grpo'; the others measure the "
-                        "two-pass / sequence-coupled routes)")
-    return p.parse_args()
+                   choices=["grpo", "grpo_two_pass", "opmd_kimi", "opmd_pairwise", "sft",
+                            "c3", "c4", "c5"],
+                   help="loss variant (the headline metric is 'grpo' = configs[1]; c3 / c4 / c5 "
+                        "are the per-GPU shards of BASELINE configs[2..4]; the others measure "
+                        "the two-pass / sequence-coupled routes)")
+    a = p.parse_args()
+    # per-GPU shards of the multi-GPU configs (weak scaling: fixed work per GPU)
+    if a.variant == "c3":    # configs[2]: 128 x 8 rollouts x 4096 tokens over 8 GPUs
+        a.groups, a.group_size, a.resp_len, a.mb_groups = 16, 8, 4096, 4
+    elif a.variant == "c5":  # configs[4]: 256 x 16 rollouts, <= 8192 ragged tokens, 8 GPUs
+        a.groups, a.group_size, a.resp_len, a.mb_groups = 32, 16, 8192, 2
+    return a
 
 
 def log(*a):
@@ -253,8 +273,7 @@ def main():
     G, K, Lr = args.groups, args.group_size, args.resp_len
     mbg = min(args.mb_groups, G)
     n_mb = G // mbg
-    mb_rows = mbg * K * Lr
-    T = n_mb * mb_rows
+    mb_rows = mbg * K * Lr  # logits buffer rows (c5: padded layout of the ragged batch)
     B = G * K
     cfg = RFTLossConfig(advantage_fn="grpo", policy_loss_fn="ppo_clip", kl_fn="low_var_kl",
                         kl_coef=0.001, loss_agg_mode="token-mean", clip_lo=0.2, clip_hi=0.28)
@@ -264,6 +283,10 @@ def main():
         cfg = RFTLossConfig(policy_loss_fn=args.variant, tau=1.0)
     elif args.variant == "sft":
         cfg = RFTLossConfig.from_variant("SFT")
+    elif args.variant == "c3":  # PPO clip + low_var_kl + entropy bonus
+        cfg = cfg.with_(entropy_loss_fn="default", entropy_coef=0.001)
+    elif args.variant == "c4":  # GRPO + SFT NLL on expert sequences in the same batch
+        cfg = cfg.with_(sft_weight=1.0)
     loss = RFTLoss(cfg)
     two_pass = args.variant in ("grpo_two_pass", "opmd_kimi", "opmd_pairwise")
     algo_bytes_row = (6 * V + 24) if two_pass else ALGO_BYTES_PER_ROW
@@ -283,16 +306,48 @@ def main():
     gsz = [K] * mbg
     probe = pack_arrays(logits, tgt, lens, gsz, np.zeros(mbg * K, np.float32))
     lp_true = logprob_fwd(probe)[0].cpu().numpy().astype(np.float64)
+
+    def mb_layout(m):
+        """(lens, row_index, seq_kind) of micro-batch m.  c5: ragged long-CoT
+        responses (lognormal lengths, 64..8192) with ~10 % of rows in interior
+        mask-false spans of 8..64 rows, read in place from the padded buffer
+        through row_index; c4: the second half of the groups are SFT sequences."""
+        if args.variant == "c5":
+            lrng = np.random.default_rng(1236 + 1000 * rank + m)
+            L = np.clip(np.exp(lrng.normal(np.log(3000.0), 0.8, mbg * K)), 64, Lr).astype(int)
+            keep = []
+            off = 0
+            for n in L:
+                mask = np.ones(n, bool)
+                masked = 0
+                while masked < 0.1 * n:
+                    run = int(lrng.integers(8, 65))
+                    start = int(lrng.integers(0, max(1, n - run)))
+                    masked += int(mask[start:start + run].sum())
+                    mask[start:start + run] = False
+                keep.append(np.nonzero(mask)[0] + off)
+                off += n
+            return [len(k) for k in keep], np.concatenate(keep), None
+        kind = None
+        if args.variant == "c4":
+            kind = np.repeat((np.arange(mbg) >= mbg // 2).astype(np.uint8), K)
+        return lens, None, kind
+
     batches, outs = [], []
+    T = 0
     for m in range(n_mb):
         rew = rng.integers(0, 2, mbg * K).astype(np.float32)
         if m == 0:
             rew[:K] = 1.0  # an all-equal group (A = 0, std = 0)
-        old = (lp_true + rng.normal(0, 0.05, mb_rows)).astype(np.float32)
-        ref = (lp_true + rng.normal(0, 0.1, mb_rows)).astype(np.float32)
-        b = pack_arrays(logits, tgt, lens, gsz, rew, old_lp=old, ref_lp=ref)
+        lens_m, ridx, kind = mb_layout(m)
+        rows = np.arange(mb_rows) if ridx is None else ridx
+        old = (lp_true[rows] + rng.normal(0, 0.05, rows.size)).astype(np.float32)
+        ref = (lp_true[rows] + rng.normal(0, 0.1, rows.size)).astype(np.float32)
+        b = pack_arrays(logits, tgt[rows], lens_m, gsz, rew, old_lp=old, ref_lp=ref,
+                        seq_kind=kind, row_index=ridx)
         batches.append(b)
         outs.append(None)
+        T += int(rows.size)
     route = loss.route(batches[0])
     assert route == (1 if not two_pass else (2 if args.variant == "grpo_two_pass" else 3)), route
     n_tok_g, n_seq_g = world * T, world * B
@@ -362,7 +417,8 @@ def main():
     # ---- roofline of the dominant kernel (k_fused_tma) ----
     peak, peak_src = peaks()
     f_ms = statistics.mean(fused_ms)
-    achieved = mb_rows * algo_bytes_row / (f_ms / 1000.0) / 1e9
+    rows_per_launch = T / n_mb
+    achieved = rows_per_launch * algo_bytes_row / (f_ms / 1000.0) / 1e9
     # DRAM bytes per launch from the committed `ncu --set full` capture of the
     # same kernel at this vocabulary, scaled from its row count to this launch's
     # (the kernel streams rows independently, so bytes / row is size-invariant)
@@ -372,7 +428,7 @@ def main():
         try:
             d = json.loads(tf.read_text())
             if int(d.get("vocab", 0)) == V:
-                traffic = float(d["dram_bytes_per_row"]) * mb_rows
+                traffic = float(d["dram_bytes_per_row"]) * rows_per_launch
         except Exception:
             traffic = None
 
@@ -392,20 +448,20 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": WORKLOAD if args.variant == "grpo" else
-                       f"{args.variant}_qwen2.5_1.5b_shapes", "vocab": V, "prompts": G,
-                       "repeats": K,
-                       "response_len": Lr, "rows_per_gpu_per_step": T,
-                       "micro_batches": n_mb, "rows_per_micro_batch": mb_rows,
-                       "loss": "grpo adv + ppo_clip(0.2,0.28) + low_var_kl(0.001) + token-mean"
-                       if args.variant == "grpo" else args.variant,
+            "config": {"workload": VARIANT_WORKLOAD.get(args.variant,
+                                                        f"{args.variant}_qwen2.5_1.5b_shapes"),
+                       "vocab": V, "prompts": G, "repeats": K,
+                       "response_len": Lr if args.variant != "c5" else f"ragged <= {Lr}",
+                       "rows_per_gpu_per_step": T,
+                       "micro_batches": n_mb, "rows_per_micro_batch": T // n_mb,
+                       "loss": VARIANT_LOSS.get(args.variant, args.variant),
                        "l2": "inputs larger than L2 (80 GB working set)",
                        "parallelism": f"dp{world} (groups sharded by rank; stats allreduce)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "k_fused_tma" if not two_pass else "k_fwd..k_bwd (two-pass)",
                          "kernel_ms": f_ms,
-                         "algorithmic_bytes_per_launch": mb_rows * algo_bytes_row,
+                         "algorithmic_bytes_per_launch": rows_per_launch * algo_bytes_row,
                          "peak_source": peak_src,
                          "frac_of_8tbs_nominal": achieved / 8000.0},
             "cpu_baseline": cpu,
