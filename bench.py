@@ -334,7 +334,7 @@ def main():
         return lens, None, kind
 
     batches, outs = [], []
-    T = 0
+    T = n_sft = 0
     for m in range(n_mb):
         rew = rng.integers(0, 2, mbg * K).astype(np.float32)
         if m == 0:
@@ -348,15 +348,16 @@ def main():
         batches.append(b)
         outs.append(None)
         T += int(rows.size)
+        n_sft += 0 if kind is None else int(kind.sum())
     route = loss.route(batches[0])
     assert route == (1 if not two_pass else (2 if args.variant == "grpo_two_pass" else 3)), route
-    n_tok_g, n_seq_g = world * T, world * B
+    n_tok_g, n_seq_g, n_sft_g = world * T, world * B, world * n_sft
     stats_all = torch.zeros((n_mb, N.NSTAT), dtype=torch.float64, device=dev)
 
     def step():
         for m in range(n_mb):
             outs[m] = loss(batches[m], dlogits=dz, n_tok_global=n_tok_g, n_seq_global=n_seq_g,
-                           out=outs[m])
+                           n_sft_seq_global=n_sft_g, out=outs[m])
         st = torch.stack([o.stats for o in outs]).sum(0)
         return allreduce_stats(st)
 
@@ -390,7 +391,7 @@ def main():
             L.tg_set_timing_events(evs[k][0].cuda_event, evs[k][1].cuda_event)
             k += 1
             outs[m] = loss(batches[m], dlogits=dz, n_tok_global=n_tok_g, n_seq_global=n_seq_g,
-                           out=outs[m])
+                           n_sft_seq_global=n_sft_g, out=outs[m])
         st = allreduce_stats(torch.stack([o.stats for o in outs]).sum(0))
     t_end.record()
     torch.cuda.synchronize()

@@ -18,6 +18,7 @@
  *   policy.logprob / grad_logprob   policy.py:194-212, 253-270              (fused into both)
  *   policy.scored_states            policy.py:181-191 (toy-table adapter)   tg_scored_states (host)
  *   ExperienceBuffer.sample_batch   buffer.py:240-264 (group indexing)      tg_group_by_task (host)
+ *   algorithms.apply_update         algorithms.py:329-348 (SGD step)        tg_apply_update
  *
  * plus the north_star registry pieces the reference does not have (GRPO std
  * advantage, RLOO, PPO clip / dual clip, k1/k2/k3(low_var_kl)/abs KL,
@@ -201,6 +202,21 @@ int tg_lmhead_logprob_fwd(const void* hidden, int64_t ld_hidden, const void* wei
                           int64_t ld_weight, int64_t n_rows, int64_t vocab, int64_t dim,
                           const int32_t* target, float* lp, float* entropy, float* lse,
                           void* workspace, size_t workspace_bytes, void* stream);
+
+/* Optimizer step: algorithms.apply_update (algorithms.py:329-348) on the
+   device.  table [n_states, ld_table] fp32 (updated in place) gets
+   table[s] -= learning_rate * sum of the gradient rows of state s, where the
+   gradient rows are dlogits rows [*, ld_grad] (dtype TG_DTYPE_*) grouped by
+   state in CSR form: state_ids[n_touched], state_offsets[n_touched + 1] into
+   row_order[n_rows] (rows in row order within a state).  Per-state sums are
+   f64 in row order (deterministic).  *status (device int32) becomes 0, or 1
+   when any gradient element is non-finite, 2 when a state is outside
+   [0, n_states) -- and then nothing is written (the reference refuses
+   before it updates).  Stream-ordered; the caller reads status when it syncs. */
+int tg_apply_update(float* table, int64_t ld_table, int64_t n_states, int64_t vocab,
+                    const void* grad, int dtype, int64_t ld_grad, const int64_t* state_ids,
+                    const int64_t* state_offsets, const int64_t* row_order, int64_t n_touched,
+                    int64_t n_rows, double learning_rate, int32_t* status, void* stream);
 
 /* Which kernel route tg_loss_fwd_bwd takes for this input: 1 = fused single
    pass (4V bytes/row), 2 = forward + backward streaming (6V), 3 = coupled. */

@@ -72,7 +72,7 @@ EXPORTED = [
     "tg_workspace_size", "tg_loss_fwd_bwd", "tg_logprob_fwd", "tg_route", "tg_strerror",
     "tg_last_error", "tg_abi_version", "tg_scored_states", "tg_group_by_task",
     "tg_set_timing_events", "tg_launch_count", "tg_pack_rows", "tg_lmhead_logprob_fwd",
-    "tg_lmhead_workspace_size",
+    "tg_lmhead_workspace_size", "tg_apply_update",
 ]
 
 _lib = None
@@ -133,6 +133,10 @@ def lib() -> ctypes.CDLL:
     L.tg_lmhead_logprob_fwd.argtypes = [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64,
                                         c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                         c_size_t, c_void_p]
+    L.tg_apply_update.restype = c_int
+    L.tg_apply_update.argtypes = [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int, c_int64,
+                                  c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_double,
+                                  c_void_p, c_void_p]
     L.tg_lmhead_workspace_size.restype = c_size_t
     L.tg_lmhead_workspace_size.argtypes = [c_int64, c_int64]
     if L.tg_abi_version() != 1:

@@ -37,6 +37,11 @@ cudaError_t launch_lmhead_logprob(const void* hidden, int64_t ld_hidden, const v
                                   void* workspace, size_t workspace_bytes, int n_sms,
                                   cudaStream_t stream);
 size_t lm_workspace_bytes(int64_t n_rows, int64_t vocab, int n_sms);
+cudaError_t launch_update(float* table, int64_t ld_table, int64_t n_states, int64_t vocab,
+                          const void* grad, int dtype, int64_t ld_grad, const int64_t* state_ids,
+                          const int64_t* state_offsets, const int64_t* row_order,
+                          int64_t n_touched, int64_t n_rows, double lr, int32_t* status,
+                          cudaStream_t stream);
 int lm_split(int64_t n_rows, int64_t vocab, int n_sms);
 cudaError_t launch_fused_l2(const KParams& P, const void* meta, int n_ctas, int prefetch,
                             cudaStream_t st);
@@ -522,6 +527,34 @@ int tg_lmhead_logprob_fwd(const void* hidden, int64_t ld_hidden, const void* wei
     return fail(TG_EUNSUPPORTED, "cuTensorMapEncodeTiled is unavailable (driver too old)");
   count_launches(lm_split(n_rows, vocab, sms) > 1 ? 2 : 1);
   if (e != cudaSuccess) return fail(TG_ECUDA, "tg_lmhead_logprob_fwd: %s", cudaGetErrorString(e));
+  return TG_OK;
+}
+
+int tg_apply_update(float* table, int64_t ld_table, int64_t n_states, int64_t vocab,
+                    const void* grad, int dtype, int64_t ld_grad, const int64_t* state_ids,
+                    const int64_t* state_offsets, const int64_t* row_order, int64_t n_touched,
+                    int64_t n_rows, double learning_rate, int32_t* status, void* stream) {
+  if (dtype != TG_DTYPE_BF16 && dtype != TG_DTYPE_F32)
+    return fail(TG_EINVAL, "unknown dtype %d", dtype);
+  if (n_states < 1 || vocab < 1 || n_touched < 0 || n_rows < 0)
+    return fail(TG_EINVAL, "bad sizes (states %lld, vocab %lld, touched %lld, rows %lld)",
+                (long long)n_states, (long long)vocab, (long long)n_touched, (long long)n_rows);
+  if (n_touched > 65535) return fail(TG_EINVAL, "at most 65535 touched states per call");
+  if (ld_table < vocab || ld_grad < vocab)
+    return fail(TG_EINVAL, "row pitch below vocab (ld_table %lld, ld_grad %lld)",
+                (long long)ld_table, (long long)ld_grad);
+  if (!(learning_rate > 0)) return fail(TG_EINVAL, "learning_rate must be > 0, got %g",
+                                        learning_rate);
+  if (!table || !status || (n_touched > 0 && (!grad || !state_ids || !state_offsets ||
+                                              !row_order)))
+    return fail(TG_EINVAL, "table, status, grad, state_ids, state_offsets and row_order are "
+                           "required");
+  cudaGetLastError();
+  cudaError_t e = launch_update(table, ld_table, n_states, vocab, grad, dtype, ld_grad, state_ids,
+                                state_offsets, row_order, n_touched, n_rows, learning_rate,
+                                status, reinterpret_cast<cudaStream_t>(stream));
+  count_launches(n_touched > 0 ? 2 : 0);
+  if (e != cudaSuccess) return fail(TG_ECUDA, "tg_apply_update: %s", cudaGetErrorString(e));
   return TG_OK;
 }
 

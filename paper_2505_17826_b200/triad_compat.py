@@ -146,13 +146,14 @@ def _scatter(dz: torch.Tensor, states: np.ndarray, S: int) -> SparseGrad:
 
 
 def _run(groups, params, cfg: RFTLossConfig, *, anchor=None, seq_ref_override=None,
-         seq_kind=None, metrics_override=None) -> LossReport:
+         seq_kind=None, metrics_override=None, table=None, keep_rows=False):
     dev = _device()
     h = flatten_groups(groups)
     S, V = int(params.num_buckets), int(params.vocab.size)
     states, target = scored_states(h, S)
     _check_vocab(h, target, V)
-    table = _table(params, dev)
+    if table is None:
+        table = _table(params, dev)
     seq_ref = h.seq_ref_lp if seq_ref_override is None else seq_ref_override
     anchor_rows = None
     if anchor is not None:
@@ -172,7 +173,10 @@ def _run(groups, params, cfg: RFTLossConfig, *, anchor=None, seq_ref_override=No
     metrics = {k: m[k] for k in ("mean_reward", "baseline", "kl_estimate", "group_size")}
     if metrics_override:
         metrics.update(metrics_override(st))
-    return LossReport(loss=float(st["loss"]), gradient=grad, metrics=metrics)
+    report = LossReport(loss=float(st["loss"]), gradient=grad, metrics=metrics)
+    if keep_rows:
+        return report, out.dlogits, states
+    return report
 
 
 def group_losses(groups: Sequence, params, config: AlgorithmConfig,
@@ -288,6 +292,46 @@ def apply_update(params, gradient: SparseGrad, learning_rate: float):
                         num_buckets=params.num_buckets)
 
 
+def apply_update_rows(table: torch.Tensor, dlogits: torch.Tensor, states: np.ndarray,
+                      learning_rate: float) -> None:
+    """algorithms.apply_update (algorithms.py:329-348) on the device, straight
+    from the loss kernels' per-token gradient rows: ``table[s] -= lr * sum of
+    the dlogits rows scored by state s`` (``tg_apply_update``; per-state f64
+    sums in row order).  ``table`` is the fp32 [S, V] device table, updated in
+    place.  Raises AlgorithmError like the reference -- non-finite gradient,
+    state outside the table -- and then the table is unchanged."""
+    from . import _native as N
+
+    states = np.asarray(states, dtype=np.int64)
+    dev = table.device
+    if table.dtype != torch.float32 or table.dim() != 2 or table.stride(1) != 1:
+        raise ValueError("table must be a 2-D fp32 tensor with unit column stride")
+    if dlogits.dim() != 2 or dlogits.shape[0] != states.size or dlogits.stride(1) != 1:
+        raise ValueError("dlogits must hold one row per state entry")
+    order = np.argsort(states, kind="stable")  # rows grouped by state, row order kept
+    uniq, starts = np.unique(states[order], return_index=True)
+    offsets = np.append(starts, states.size).astype(np.int64)
+    i64 = dict(dtype=torch.int64, device=dev)
+    ids_d = torch.as_tensor(uniq, **i64)
+    off_d = torch.as_tensor(offsets, **i64)
+    ord_d = torch.as_tensor(order.astype(np.int64), **i64)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    dtype = N.TG_DTYPE_BF16 if dlogits.dtype == torch.bfloat16 else N.TG_DTYPE_F32
+    L = N.lib()
+    with torch.cuda.device(dev):
+        N.check(L.tg_apply_update(table.data_ptr(), table.stride(0), table.shape[0],
+                                  table.shape[1], dlogits.data_ptr(), dtype, dlogits.stride(0),
+                                  ids_d.data_ptr(), off_d.data_ptr(), ord_d.data_ptr(),
+                                  uniq.size, states.size, float(learning_rate),
+                                  status.data_ptr(), torch.cuda.current_stream(dev).cuda_stream))
+    code = int(status.item())
+    if code & 2:
+        bad = int(uniq[(uniq < 0) | (uniq >= table.shape[0])][0])
+        raise AlgorithmError(f"gradient row {bad} outside the logits table")
+    if code & 1:
+        raise AlgorithmError("refusing to apply a non-finite gradient")
+
+
 class Trainer:
     """orchestrator.Trainer (orchestrator.py:288-322) on the CUDA loss path."""
 
@@ -309,4 +353,39 @@ class Trainer:
     def step_dpo(self, pairs) -> LossReport:
         report = loss_dpo(pairs, self.params, self.anchor, self.algo.dpo_beta)
         self.params = apply_update(self.params, report.gradient, self.algo.learning_rate)
+        return report
+
+
+class DeviceTrainer:
+    """``Trainer.step_groups`` with the policy table resident on the GPU: the
+    loss kernels read it in place (row_index) and the SGD step runs on the
+    device from the per-token gradient rows (``tg_apply_update``), so only the
+    LossReport crosses PCIe.  ``params`` materialises the host table on access
+    (version counted like apply_update, algorithms.py:343-348)."""
+
+    def __init__(self, params, algo: AlgorithmConfig) -> None:
+        self._host = params
+        self.algo = algo
+        self.anchor = params
+        self.table = _table(params, _device())
+        self.version = int(getattr(params, "version", 0))
+
+    @property
+    def params(self):
+        p = self._host
+        return type(p)(logits=self.table.double().cpu().numpy(), version=self.version,
+                       vocab=p.vocab, num_buckets=p.num_buckets)
+
+    def step_groups(self, groups) -> LossReport:
+        config = self.algo
+        if config.variant not in (Variant.OPMD_KIMI, Variant.OPMD_PAIRWISE, Variant.OPMD_SIMPLE):
+            raise AlgorithmError(f"{config.variant.value} is not a group-based loss")
+        if not groups:
+            raise AlgorithmError("cannot combine an empty report list")
+        cfg = RFTLossConfig.from_variant(config.variant, config.tau, config.beta, config.dpo_beta)
+        anchor = self.anchor if (config.variant == Variant.OPMD_SIMPLE and config.beta > 0) else None
+        report, dz, states = _run(groups, self._host, cfg, anchor=anchor, table=self.table,
+                                  keep_rows=True)
+        apply_update_rows(self.table, dz, states, config.learning_rate)
+        self.version += 1
         return report
