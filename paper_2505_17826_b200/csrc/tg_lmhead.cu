@@ -54,15 +54,26 @@ struct LmParams {
   float* lse;             // [T]
 };
 
+constexpr int LM_MAX_STAGES = 6;
+
 struct LmSmemTail {
-  uint64_t full[LM_STAGES];
-  uint64_t empty[LM_STAGES];
+  uint64_t full[LM_MAX_STAGES];
+  uint64_t empty[LM_MAX_STAGES];
   uint64_t tfull[2];
   uint64_t tempty[2];
   uint32_t tmem_base;
 };
 
-size_t lm_smem_bytes() { return size_t(LM_STAGES) * LM_STAGE_BYTES + sizeof(LmSmemTail) + 1024; }
+// per-CTA stage: X tile 16 KB + W tile 32 KB (single) or 16 KB (pair: half of it);
+// the pair variant affords 6 stages in the same shared memory
+template <bool kPair>
+constexpr int lm_stages() { return kPair ? 6 : LM_STAGES; }
+template <bool kPair>
+constexpr int lm_stage_bytes() { return LM_A_BYTES + (kPair ? LM_BN / 2 : LM_BN) * LM_BK * 2; }
+template <bool kPair>
+size_t lm_smem_bytes() {
+  return size_t(lm_stages<kPair>()) * lm_stage_bytes<kPair>() + sizeof(LmSmemTail) + 1024;
+}
 
 // ---- PTX wrappers -------------------------------------------------------------
 
@@ -152,22 +163,83 @@ __device__ __forceinline__ void lm_tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// ---- the kernel -----------------------------------------------------------------
+// ---- cluster-pair helpers (kPair: cta_group::2, M = 256 across two SMs) ----------
 
+__device__ __forceinline__ uint32_t lm_peer0(uint32_t smem_addr) {  // same offset in CTA rank 0
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_addr));
+  return r;
+}
+
+__device__ __forceinline__ void lm_tma_2d_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                               uint32_t leader_bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(leader_bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void lm_mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// arrive on the same barrier of both CTAs of the pair when the MMAs complete
+__device__ __forceinline__ void lm_commit_pair(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], m;\n\t}" ::"r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void lm_arrive_cluster(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar)
+               : "memory");
+}
+
+template <bool kPair>
+constexpr uint32_t lm_idesc_t() {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(LM_BN >> 3) << 17) |
+         (uint32_t((kPair ? 2 * LM_BM : LM_BM) >> 4) << 24);
+}
+
+// ---- the kernel -----------------------------------------------------------------
+// kPair = false: one CTA per 128-row block, tcgen05.mma.cta_group::1 (M 128, N 256).
+// kPair = true : a 2-CTA cluster per 256-row block; each CTA stages its own 128 X
+//   rows and half of the 256-row W tile, the leader (rank 0) issues
+//   tcgen05.mma.cta_group::2 (M 256, N 256) reading both CTAs' shared memory, and
+//   each CTA's TMEM receives its 128 rows: per SM the W-tile traffic halves.
+
+template <bool kPair>
 __global__ void __launch_bounds__(LM_THREADS, 1)
     k_lmhead_logprob(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                      const LmParams P) {
+  constexpr int B_ROWS = kPair ? LM_BN / 2 : LM_BN;      // W rows staged per CTA
+  constexpr int STAGE = lm_stage_bytes<kPair>();
+  constexpr int NST = lm_stages<kPair>();
+  constexpr int ROWS_PER_UNIT = kPair ? 2 * LM_BM : LM_BM;
   extern __shared__ __align__(1024) unsigned char lm_smem_raw[];
   // 1 KB alignment for the 128-byte swizzle atoms
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(lm_smem_raw) + 1023) & ~uintptr_t(1023));
-  LmSmemTail* tail = reinterpret_cast<LmSmemTail*>(smem + size_t(LM_STAGES) * LM_STAGE_BYTES);
+  LmSmemTail* tail = reinterpret_cast<LmSmemTail*>(smem + size_t(NST) * STAGE);
   const uint32_t ring = smem_u32(smem);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = kPair ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  const int unit0 = kPair ? int(cluster_id_x()) : int(blockIdx.x);
+  const int unit_stride = kPair ? int(n_clusters_x()) : int(gridDim.x);
   const int64_t T = P.n_rows;
   const int V = int(P.vocab);
-  const int n_mb = int((T + LM_BM - 1) / LM_BM);
+  const int n_mb = int((T + ROWS_PER_UNIT - 1) / ROWS_PER_UNIT);
   const int n_nt = (V + LM_BN - 1) / LM_BN;
   // work unit u = (row block u / n_split, vocabulary split u % n_split)
   const int n_split = P.n_split;
@@ -181,25 +253,36 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
   const int n_kb = int(P.dim / LM_BK);
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < LM_STAGES; ++i) {
+    for (int i = 0; i < NST; ++i) {
       mbar_init(&tail->full[i], 1);
       mbar_init(&tail->empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tail->tfull[i], 1);
-      mbar_init(&tail->tempty[i], 4);
+      mbar_init(&tail->tempty[i], kPair ? 8 : 4);  // epilogue warps of the pair / of the CTA
     }
     fence_mbar_init();
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&tail->tmem_base)),
-                 "r"(LM_TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (kPair) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(&tail->tmem_base)),
+                   "r"(LM_TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(&tail->tmem_base)),
+                   "r"(LM_TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair)
+    cluster_sync_all();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tail->tmem_base;
 
@@ -209,18 +292,28 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
       uint32_t stage = 0, phase = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      for (int u = unit0; u < n_units; u += unit_stride) {
         int mb, nt0, nt1;
         unit_tiles(u, mb, nt0, nt1);
+        const int xrow = mb * ROWS_PER_UNIT + int(rank) * LM_BM;
         for (int nt = nt0; nt < nt1; ++nt) {
+          const int wrow = nt * LM_BN + int(rank) * B_ROWS;
           for (int kb = 0; kb < n_kb; ++kb) {
             lm_wait(smem_u32(&tail->empty[stage]), phase ^ 1u);
             const uint32_t fb = smem_u32(&tail->full[stage]);
-            lm_expect_tx(fb, LM_STAGE_BYTES);
-            const uint32_t a = ring + stage * LM_STAGE_BYTES;
-            lm_tma_2d(a, &tmX, kb * LM_BK, mb * LM_BM, fb);
-            lm_tma_2d(a + LM_A_BYTES, &tmW, kb * LM_BK, nt * LM_BN, fb);
-            if (++stage == LM_STAGES) {
+            const uint32_t a = ring + stage * STAGE;
+            if constexpr (kPair) {
+              // both CTAs' bytes complete on the leader's full barrier
+              if (leader) lm_expect_tx(fb, 2 * STAGE);
+              const uint32_t lfb = lm_peer0(fb);
+              lm_tma_2d_pair(a, &tmX, kb * LM_BK, xrow, lfb);
+              lm_tma_2d_pair(a + LM_A_BYTES, &tmW, kb * LM_BK, wrow, lfb);
+            } else {
+              lm_expect_tx(fb, STAGE);
+              lm_tma_2d(a, &tmX, kb * LM_BK, xrow, fb);
+              lm_tma_2d(a + LM_A_BYTES, &tmW, kb * LM_BK, wrow, fb);
+            }
+            if (++stage == uint32_t(NST)) {
               stage = 0;
               phase ^= 1u;
             }
@@ -230,33 +323,48 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    // ============================ MMA issuer ============================
-    if (lane == 0) {
-      constexpr uint32_t idesc = lm_idesc();
+    // ============================ MMA issuer (leader) ============================
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = lm_idesc_t<kPair>();
       uint32_t stage = 0, phase = 0, tile = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      for (int u = unit0; u < n_units; u += unit_stride) {
         int mb, nt0, nt1;
         unit_tiles(u, mb, nt0, nt1);
         for (int nt = nt0; nt < nt1; ++nt, ++tile) {
           const uint32_t acc = tile & 1u, acc_phase = (tile >> 1) & 1u;
-          lm_wait(smem_u32(&tail->tempty[acc]), acc_phase ^ 1u);
+          if constexpr (kPair) {
+            while (!mbar_try_wait_cluster(smem_u32(&tail->tempty[acc]), acc_phase ^ 1u)) {
+            }
+          } else {
+            lm_wait(smem_u32(&tail->tempty[acc]), acc_phase ^ 1u);
+          }
           tc_fence_after();
           const uint32_t d = tmem + acc * LM_BN;
           for (int kb = 0; kb < n_kb; ++kb) {
             lm_wait(smem_u32(&tail->full[stage]), phase);
             tc_fence_after();
-            const uint32_t a = ring + stage * LM_STAGE_BYTES;
+            const uint32_t a = ring + stage * STAGE;
             const uint64_t ad = lm_sw128_desc(a), bd = lm_sw128_desc(a + LM_A_BYTES);
 #pragma unroll
-            for (int k = 0; k < LM_BK / LM_UK; ++k)  // +32 bytes along K per step
-              lm_mma(d, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc, (kb | k) != 0);
-            lm_commit(smem_u32(&tail->empty[stage]));
-            if (++stage == LM_STAGES) {
+            for (int k = 0; k < LM_BK / LM_UK; ++k) {  // +32 bytes along K per step
+              if constexpr (kPair)
+                lm_mma_pair(d, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc, (kb | k) != 0);
+              else
+                lm_mma(d, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc, (kb | k) != 0);
+            }
+            if constexpr (kPair)
+              lm_commit_pair(smem_u32(&tail->empty[stage]));
+            else
+              lm_commit(smem_u32(&tail->empty[stage]));
+            if (++stage == uint32_t(NST)) {
               stage = 0;
               phase ^= 1u;
             }
           }
-          lm_commit(smem_u32(&tail->tfull[acc]));
+          if constexpr (kPair)
+            lm_commit_pair(smem_u32(&tail->tfull[acc]));
+          else
+            lm_commit(smem_u32(&tail->tfull[acc]));
         }
       }
     }
@@ -267,10 +375,10 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
     const uint32_t lane_base = uint32_t(32 * q) << 16;
     const uint64_t l2e2 = pk2(kLog2e, kLog2e);
     uint32_t tile = 0;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+    for (int u = unit0; u < n_units; u += unit_stride) {
       int mb, nt0, nt1;
       unit_tiles(u, mb, nt0, nt1);
-      const int64_t row = int64_t(mb) * LM_BM + 32 * q + lane;
+      const int64_t row = int64_t(mb) * ROWS_PER_UNIT + int64_t(rank) * LM_BM + 32 * q + lane;
       const int y = (row < T && P.target) ? P.target[row] : -1;
       float m = -1.0e30f, zy = kNegInf;
       uint64_t s2 = pk2(0.f, 0.f), t2 = pk2(0.f, 0.f);
@@ -335,7 +443,12 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
         t2 = add2(t2, tt2);
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tail->tempty[acc]);
+        if (lane == 0) {
+          if constexpr (kPair)
+            lm_arrive_cluster(lm_peer0(smem_u32(&tail->tempty[acc])));
+          else
+            mbar_arrive(&tail->tempty[acc]);
+        }
       }
       if (row < T) {
         float s0, s1, t0, t1;
@@ -354,12 +467,20 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair)
+    cluster_sync_all();  // the peer's MMAs and remote arrivals are done
+  else
+    __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(LM_TMEM_COLS)
-                 : "memory");
+    if constexpr (kPair)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "r"(LM_TMEM_COLS)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "r"(LM_TMEM_COLS)
+                   : "memory");
   }
 }
 
@@ -383,17 +504,32 @@ __global__ void k_lmhead_merge(const LmParams P) {
   }
 }
 
-// Vocabulary splits per 128-row block: enough work units to fill the SMs in
-// whole waves (small row counts would otherwise leave SMs idle).
+// Single CTAs by default; TG_LMHEAD_PAIR=1 selects the 2-CTA (cta_group::2)
+// variant.  A/B on B200 (profiles/r01_lmhead_ab.txt): pairs +1 % at d = 1536,
+// -6 % at d = 3584, so the simpler single-CTA kernel stays the default.
+static bool lm_pair_mode() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* v = getenv("TG_LMHEAD_PAIR");
+    mode = (v && *v) ? (atoi(v) != 0) : 0;
+  }
+  return mode != 0;
+}
+
+// Vocabulary splits per row block: enough work units to fill the SMs (or SM
+// pairs) in whole waves -- small row counts would otherwise leave SMs idle.
 int lm_split(int64_t n_rows, int64_t vocab, int n_sms) {
-  const int64_t n_mb = (n_rows + LM_BM - 1) / LM_BM;
+  const bool pair = lm_pair_mode();
+  const int64_t rows_per_unit = pair ? 2 * LM_BM : LM_BM;
+  const int64_t slots = pair ? n_sms / 2 : n_sms;
+  const int64_t n_mb = (n_rows + rows_per_unit - 1) / rows_per_unit;
   const int64_t n_nt = (vocab + LM_BN - 1) / LM_BN;
   int best = 1;
   double best_eff = 0.0;
   for (int sp = 1; sp <= 16 && sp <= n_nt; ++sp) {
     const int64_t units = n_mb * sp;
-    const int64_t waves = (units + n_sms - 1) / n_sms;
-    const double eff = double(units) / double(waves * n_sms);
+    const int64_t waves = (units + slots - 1) / slots;
+    const double eff = double(units) / double(waves * slots);
     if (eff > best_eff + 0.02) {
       best_eff = eff;
       best = sp;
@@ -444,9 +580,11 @@ cudaError_t launch_lmhead_logprob(const void* hidden, int64_t ld_hidden, const v
                                   const int32_t* target, float* lp, float* ent, float* lse,
                                   void* workspace, size_t workspace_bytes, int n_sms,
                                   cudaStream_t stream) {
+  const bool pair = lm_pair_mode();
   CUtensorMap mx, mw;
   if (!lm_make_map(&mx, hidden, n_rows, dim, ld_hidden, LM_BM)) return cudaErrorNotSupported;
-  if (!lm_make_map(&mw, weight, vocab, dim, ld_weight, LM_BN)) return cudaErrorNotSupported;
+  if (!lm_make_map(&mw, weight, vocab, dim, ld_weight, pair ? LM_BN / 2 : LM_BN))
+    return cudaErrorNotSupported;
   LmParams P;
   P.n_rows = n_rows;
   P.vocab = vocab;
@@ -459,13 +597,37 @@ cudaError_t launch_lmhead_logprob(const void* hidden, int64_t ld_hidden, const v
   P.partial = reinterpret_cast<float4*>(workspace);
   if (P.n_split > 1 && (!workspace || workspace_bytes < lm_workspace_bytes(n_rows, vocab, n_sms)))
     return cudaErrorInvalidValue;
-  const size_t smem = lm_smem_bytes();
-  cudaError_t e = cudaFuncSetAttribute(k_lmhead_logprob,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return e;
-  const int64_t units = ((n_rows + LM_BM - 1) / LM_BM) * P.n_split;
-  const int grid = int(units < n_sms ? units : n_sms);
-  k_lmhead_logprob<<<grid, LM_THREADS, smem, stream>>>(mx, mw, P);
+  cudaError_t e;
+  if (pair) {
+    const size_t smem = lm_smem_bytes<true>();
+    e = cudaFuncSetAttribute(k_lmhead_logprob<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem));
+    if (e != cudaSuccess) return e;
+    const int64_t units = ((n_rows + 2 * LM_BM - 1) / (2 * LM_BM)) * P.n_split;
+    const int64_t pairs = units < n_sms / 2 ? units : n_sms / 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(2 * pairs));
+    cfg.blockDim = dim3(LM_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, k_lmhead_logprob<true>, mx, mw, P);
+    if (e != cudaSuccess) return e;
+  } else {
+    const size_t smem = lm_smem_bytes<false>();
+    e = cudaFuncSetAttribute(k_lmhead_logprob<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem));
+    if (e != cudaSuccess) return e;
+    const int64_t units = ((n_rows + LM_BM - 1) / LM_BM) * P.n_split;
+    const int grid = int(units < n_sms ? units : n_sms);
+    k_lmhead_logprob<false><<<grid, LM_THREADS, smem, stream>>>(mx, mw, P);
+  }
   if (P.n_split > 1) k_lmhead_merge<<<int((n_rows + 255) / 256), 256, 0, stream>>>(P);
   return cudaGetLastError();
 }
