@@ -1,0 +1,28 @@
+"""The environment-selected alternative kernels (kept for A/B) stay
+parity-green: the L2-reread fused loss kernel (TG_FUSED_IMPL=2) against the
+oracle, the 2-CTA LM-head kernel (TG_LMHEAD_PAIR=1) against torch fp32.  Each
+runs in a subprocess because the selection is read once per process."""
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+HERE = Path(__file__).resolve().parent
+
+
+@pytest.mark.parametrize("what,env", [("fused", {"TG_FUSED_IMPL": "2"}),
+                                      ("lmhead", {"TG_LMHEAD_PAIR": "1"})])
+def test_alternative_kernel_parity(what, env):
+    r = subprocess.run([sys.executable, str(HERE / "_alt_paths.py"), what],
+                       env={**os.environ, **env}, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.strip().endswith("ok")
