@@ -51,6 +51,8 @@ ALGO_BYTES_PER_ROW = 4 * V + 24  # 2V read + 2V write + 24 B sid
 WORKLOAD = "grpo_ppo_clip_k3_token_mean_qwen2.5_1.5b_shapes"
 VARIANT_WORKLOAD = {
     "grpo": WORKLOAD,
+    "c1": "configs[0]: GRPO loss, 8 prompts x 8 x 512 tokens, vocab 32,000 (the CPU "
+          "reference's case) on 1 GPU",
     "c3": "configs[2] per-GPU shard: ppo_clip_k3_entropy, 16 prompts x 8 x 4096 tokens "
           "(128 x 8 over 8 GPUs)",
     "c4": "configs[3]: mixed GRPO + SFT NLL (50/50 sequences) at configs[1] shapes",
@@ -58,7 +60,7 @@ VARIANT_WORKLOAD = {
           "10 % interior mask-false spans, row_index gather (256 x 16 over 8 GPUs)",
 }
 _BASE_LOSS = "grpo adv + ppo_clip(0.2,0.28) + low_var_kl(0.001) + token-mean"
-VARIANT_LOSS = {"grpo": _BASE_LOSS, "c3": _BASE_LOSS + " + entropy(0.001)",
+VARIANT_LOSS = {"grpo": _BASE_LOSS, "c1": _BASE_LOSS, "c3": _BASE_LOSS + " + entropy(0.001)",
                 "c4": _BASE_LOSS + " on RL seqs + SFT NLL (weight 1) on expert seqs",
                 "c5": _BASE_LOSS}
 
@@ -80,13 +82,18 @@ def parse():
     p.add_argument("--quiet", action="store_true")
     p.add_argument("--variant", default="grpo",
                    choices=["grpo", "grpo_two_pass", "opmd_kimi", "opmd_pairwise", "sft",
-                            "c3", "c4", "c5"],
+                            "c1", "c3", "c4", "c5"],
                    help="loss variant (the headline metric is 'grpo' = configs[1]; c3 / c4 / c5 "
                         "are the per-GPU shards of BASELINE configs[2..4]; the others measure "
                         "the two-pass / sequence-coupled routes)")
     a = p.parse_args()
+    global V, BUMP, ALGO_BYTES_PER_ROW
     # per-GPU shards of the multi-GPU configs (weak scaling: fixed work per GPU)
-    if a.variant == "c3":    # configs[2]: 128 x 8 rollouts x 4096 tokens over 8 GPUs
+    if a.variant == "c1":    # configs[0]: the CPU oracle's case, 8 x 8 x 512 at V = 32,000
+        V, BUMP = 32000, 12.0
+        ALGO_BYTES_PER_ROW = 4 * V + 24
+        a.groups, a.group_size, a.resp_len, a.mb_groups = 8, 8, 512, 8
+    elif a.variant == "c3":    # configs[2]: 128 x 8 rollouts x 4096 tokens over 8 GPUs
         a.groups, a.group_size, a.resp_len, a.mb_groups = 16, 8, 4096, 4
     elif a.variant == "c5":  # configs[4]: 256 x 16 rollouts, <= 8192 ragged tokens, 8 GPUs
         a.groups, a.group_size, a.resp_len, a.mb_groups = 32, 16, 8192, 2
@@ -456,7 +463,8 @@ def main():
                        "rows_per_gpu_per_step": T,
                        "micro_batches": n_mb, "rows_per_micro_batch": T // n_mb,
                        "loss": VARIANT_LOSS.get(args.variant, args.variant),
-                       "l2": "inputs larger than L2 (80 GB working set)",
+                       "l2": f"inputs larger than L2 ({2 * mb_rows * V * 2 / 1e9:.1f} GB "
+                             "working set)",
                        "parallelism": f"dp{world} (groups sharded by rank; stats allreduce)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
