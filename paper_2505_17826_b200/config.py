@@ -6,7 +6,6 @@ from __future__ import annotations
 import enum
 import math
 from dataclasses import dataclass, replace
-from typing import Optional
 
 from . import _native as N
 from .registry import (ADVANTAGE_FNS, ENTROPY_LOSS_FNS, KL_FNS, LOSS_AGG_MODES,

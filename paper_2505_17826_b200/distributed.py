@@ -15,7 +15,7 @@ rank holds, so no pre-kernel collective is needed.
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import List, Optional, Sequence, Tuple
+from typing import List, Sequence, Tuple
 
 import numpy as np
 

@@ -20,7 +20,6 @@ import torch
 from _cases import make_case, oracle_cfg
 from _golden import groups_of, load
 from oracle import rft_oracle as O
-from oracle import toy_policy as TP
 from paper_2505_17826_b200 import AlgorithmError, RFTLoss, RFTLossConfig, logprob_fwd, pack_arrays
 from paper_2505_17826_b200 import triad_compat as C
 
