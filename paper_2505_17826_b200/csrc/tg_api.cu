@@ -50,6 +50,8 @@ int fused_max_clusters(int dtype, int cl);
 int fused_max_slots();
 size_t rowmeta_bytes();
 void launch_fwd(const KParams& P, bool anchor, bool vec, int grid, cudaStream_t st);
+cudaError_t launch_fwd_tma(const KParams& P, int n_sms, cudaStream_t stream);
+size_t fwd_tma_smem_bytes();
 void launch_bwd(const KParams& P, bool anchor, bool vec, int grid, cudaStream_t st);
 void launch_rowcoef(const KParams& P, const void* meta, bool coupled, bool anchor, int grid,
                     cudaStream_t st);
@@ -328,6 +330,22 @@ FusedPlan fused_plan(const TgBatch* b, const TgOut* o) {
   return fp;
 }
 
+// Forward pass of the two-pass / coupled routes and tg_logprob_fwd: the TMA
+// streaming kernel (k_fwd_tma) for 16-byte-aligned rows without an anchor, the
+// grid-stride kernels otherwise.  TG_FWD_TMA=0 forces the latter (A/B).
+void run_forward(const KParams& P, const TgBatch* b, bool anchor, bool vin, int grid,
+                 cudaStream_t st) {
+  const int esz = esz_of(b->dtype);
+  const int epv = 16 / esz;
+  const int64_t nvec = (b->vocab + epv - 1) / epv;
+  const DevInfo d = dev_info();
+  const bool tma = !anchor && vin && env_int("TG_FWD_TMA", 1) != 0 && b->ld >= nvec * epv &&
+                   d.sms > 0 && size_t(d.smem_optin) >= fwd_tma_smem_bytes();
+  if (tma && launch_fwd_tma(P, d.sms, st) == cudaSuccess) return;
+  cudaGetLastError();
+  launch_fwd(P, anchor, vin, grid, st);
+}
+
 int route_of(const TgBatch* b, const TgConfig* c, const TgOut* o) {
   if (coupled_pg(c->policy_loss_fn)) return 3;
   if (c->anchor_beta > 0) return 2;
@@ -434,7 +452,7 @@ int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspa
     const int grid = stream_grid(b->n_rows);
     if (ev_begin) cudaEventRecord(ev_begin, st);
     if (b->n_rows > 0) {
-      launch_fwd(P, anchor, vin, grid, st);
+      run_forward(P, b, anchor, vin, grid, st);
       count_launches(1);
     }
     if (coupled) {
@@ -481,7 +499,7 @@ int tg_logprob_fwd(const TgBatch* b, TgOut* o, void* workspace, size_t workspace
   cudaGetLastError();
   const int esz = esz_of(b->dtype);
   if (b->n_rows > 0) {
-    launch_fwd(P, false, vec_ok(b->logits, b->ld, esz), stream_grid(b->n_rows), st);
+    run_forward(P, b, false, vec_ok(b->logits, b->ld, esz), stream_grid(b->n_rows), st);
     count_launches(1);
   }
   if (o->seq_lp && b->n_seqs > 0) {

@@ -682,6 +682,183 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
+// k_fwd_tma: forward-only streaming logprob (tg_logprob_fwd, and the forward
+// pass of the two-pass / sequence-coupled routes).  Same warp roles and ring
+// as k_fused_tma, but nothing has to stay resident: each chunk is released as
+// soon as its phase-1 sums are taken, so the whole 224 KB ring is read-ahead,
+// one CTA owns whole rows (no cluster), and the consumers never wait for the
+// epilogue -- it only merges the warp partials, reads the target logit and
+// writes lse / lp / entropy.  2V bytes read per row.
+
+constexpr int kFwdPar = 4;  // row-partial buffers between the consumers and the epilogue
+
+struct FwdSmemTail {
+  uint64_t full[kSlots];
+  uint64_t empty[kSlots];
+  uint64_t pbar[kFwdPar];  // consumers -> epilogue: partials of a row written
+  uint64_t ebar[kFwdPar];  // epilogue -> consumers: partial buffer free again
+  float4 wpart[kFwdPar][kConsumerWarps];
+};
+
+template <typename T>
+__device__ __forceinline__ void phase1_stream_row(Acc1& acc, RingIt& it, const RingBase& rb,
+                                                  const Slice& sl, int tid, int lane) {
+  int vbase = sl.v0;
+  for (int c = 0; c < sl.nchunk; ++c) {
+    const uint32_t empty = it.empty(rb);
+    const int vend = vbase + kVecPerChunk;
+    const bool has_tail = sl.tail_vec >= vbase && sl.tail_vec < vend;
+    if (vend <= sl.v1 && !has_tail)
+      phase1_chunk<T, false, false>(acc, it, rb, vbase, sl, tid);
+    else if (!has_tail)
+      phase1_chunk<T, true, false>(acc, it, rb, vbase, sl, tid);
+    else
+      phase1_chunk<T, true, true>(acc, it, rb, vbase, sl, tid);
+    __syncwarp();
+    if (lane == 0) arrive_u32(empty);  // the chunk's data is in registers: slot free
+    vbase = vend;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kFusedThreads, 1) k_fwd_tma(const KParams P) {
+  constexpr int EPV = Vec<T>::N;
+  constexpr int ESZ = elem_bytes<T>();
+  extern __shared__ __align__(1024) unsigned char smem[];
+  FwdSmemTail* tail = reinterpret_cast<FwdSmemTail*>(smem + size_t(kSlots) * kChunk);
+  const RingBase rb = {smem_u32(smem), smem_u32(&tail->full[0]), smem_u32(&tail->empty[0])};
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t NR = P.n_rows;
+  const int V = int(P.vocab);
+  Slice sl;
+  const int nvec = (V + EPV - 1) / EPV;
+  sl.v0 = 0;
+  sl.v1 = nvec;
+  const uint32_t row_bytes = uint32_t(nvec) * 16u;
+  sl.nchunk = int((row_bytes + kChunk - 1) / kChunk);
+  sl.tail_vec = (V % EPV) ? nvec - 1 : -1;
+  sl.tail_valid = V - (nvec - 1) * EPV;
+
+  if (tid == 0) {
+    for (int i = 0; i < kSlots; ++i) {
+      mbar_init(&tail->full[i], 1);
+      mbar_init(&tail->empty[i], kConsumerWarps);
+    }
+    for (int i = 0; i < kFwdPar; ++i) {
+      mbar_init(&tail->pbar[i], kConsumerWarps);
+      mbar_init(&tail->ebar[i], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == kProducerWarp) {
+    if (lane == 0 && sl.nchunk > 0) {
+      const uint64_t pol = policy_evict_first();
+      const char* base = reinterpret_cast<const char*>(P.logits);
+      RingIt it = {0u};
+      for (int64_t row = blockIdx.x; row < NR; row += gridDim.x) {
+        const int64_t src_row = P.row_index ? P.row_index[row] : row;
+        const char* src = base + src_row * P.ld * ESZ;
+        for (int j = 0; j < sl.nchunk; ++j) {
+          mbar_wait_u32<TG_SLEEP_PROD>(it.empty(rb), it.phase() ^ 1u);
+          const uint32_t off = uint32_t(j) * kChunk;
+          const uint32_t bytes = min(uint32_t(kChunk), row_bytes - off);
+          asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                           it.full(rb)),
+                       "r"(bytes)
+                       : "memory");
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+              " [%0], [%1], %2, [%3], %4;" ::"r"(it.addr(rb)),
+              "l"(src + off), "r"(bytes), "r"(it.full(rb)), "l"(pol)
+              : "memory");
+          it.next();
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == kEpilogueWarp) {
+    int64_t k = 0;
+    for (int64_t row = blockIdx.x; row < NR; row += gridDim.x, ++k) {
+      const int slot = int(k % kFwdPar);
+      const uint32_t parity = uint32_t((k / kFwdPar) & 1);
+      float zy = kNegInf;  // target logit, read ahead of the wait
+      if (lane == 0) {
+        const int y = P.target[row];
+        if (y >= 0 && y < V) {
+          const int64_t src_row = P.row_index ? P.row_index[row] : row;
+          zy = Vec<T>::load1(reinterpret_cast<const char*>(P.logits) + src_row * P.ld * ESZ, y);
+        }
+      }
+      mbar_wait_u32<TG_SLEEP_EPI>(smem_u32(&tail->pbar[slot]), parity);
+      Online acc_p = {kNegInf, 0.f, 0.f};
+      if (lane < kConsumerWarps) {
+        const float4 v = tail->wpart[slot][lane];
+        acc_p = Online{v.x, v.y, v.z};
+      }
+      __syncwarp();
+      if (lane == 0) arrive_u32(smem_u32(&tail->ebar[slot]));
+      const Online tot = warp_merge_first<kConsumerWarps>(acc_p);
+      if (lane == 0) {  // off the consumers' path: full-precision log and divide
+        const float lse = tot.m + logf(tot.s);
+        P.lse[row] = lse;
+        P.lp[row] = zy - lse;
+        P.ent[row] = lse - tot.t / tot.s;
+      }
+    }
+  } else {
+    RingIt it = {0u};
+    Acc1 acc = acc_init();
+    int64_t k = 0;
+    for (int64_t row = blockIdx.x; row < NR; row += gridDim.x, ++k) {
+      acc_new_row(acc);
+      phase1_stream_row<T>(acc, it, rb, sl, tid, lane);
+      Online o;
+      {
+        float s0, s1, t0, t1;
+        upk2(acc.a.s2, s0, s1);
+        upk2(acc.a.t2, t0, t1);
+        const float sl_s = s0 + s1;
+        o = warp_merge(Online{sl_s > 0.f ? acc.a.m : kNegInf, sl_s, t0 + t1});
+      }
+      const int slot = int(k % kFwdPar);
+      if (lane == 0) {
+        if (k >= kFwdPar)  // the epilogue has read this buffer's previous row
+          mbar_wait_u32<TG_SLEEP_BCAST>(smem_u32(&tail->ebar[slot]),
+                                        uint32_t(((k / kFwdPar) - 1) & 1));
+        tail->wpart[slot][warp] = make_float4(o.m, o.s, o.t, 0.f);
+        arrive_u32(smem_u32(&tail->pbar[slot]));
+      }
+    }
+  }
+}
+
+size_t fwd_tma_smem_bytes() { return size_t(kSlots) * kChunk + sizeof(FwdSmemTail); }
+
+cudaError_t launch_fwd_tma(const KParams& P, int n_sms, cudaStream_t stream) {
+#ifdef TG_FUSED_PROF
+  return cudaErrorNotSupported;  // the profiling counters assume k_fused_tma's layout
+#endif
+  const size_t smem = fwd_tma_smem_bytes();
+  const int64_t grid64 = P.n_rows < n_sms ? P.n_rows : n_sms;
+  if (grid64 <= 0) return cudaSuccess;
+  cudaError_t e;
+  if (P.dtype == TG_DTYPE_BF16) {
+    e = cudaFuncSetAttribute(k_fwd_tma<bf16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem));
+    if (e != cudaSuccess) return e;
+    k_fwd_tma<bf16_t><<<int(grid64), kFusedThreads, smem, stream>>>(P);
+  } else {
+    e = cudaFuncSetAttribute(k_fwd_tma<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem));
+    if (e != cudaSuccess) return e;
+    k_fwd_tma<float><<<int(grid64), kFusedThreads, smem, stream>>>(P);
+  }
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // host-side launch helper (called from tg_api.cu)
 
 size_t fused_smem_bytes(int n_slots) { return size_t(n_slots) * kChunk + sizeof(FusedSmemTail); }
