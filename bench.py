@@ -271,10 +271,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; TG_BENCH_BACKEND=gloo lets a multi-rank smoke run share
+    # a single GPU (NCCL refuses two ranks on one device) -- plumbing only
+    backend = os.environ.get("TG_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     L = N.lib()
 
     G, K, Lr = args.groups, args.group_size, args.resp_len
