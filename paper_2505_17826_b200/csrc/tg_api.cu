@@ -48,6 +48,7 @@ cudaError_t launch_fused_l2(const KParams& P, const void* meta, int n_ctas, int 
 int l2_threads();
 int fused_max_clusters(int dtype, int cl);
 int fused_max_slots();
+int fused_resident_chunks();
 size_t rowmeta_bytes();
 void launch_fwd(const KParams& P, bool anchor, bool vec, int grid, cudaStream_t st);
 cudaError_t launch_fwd_tma(const KParams& P, int n_sms, cudaStream_t stream);
@@ -316,7 +317,7 @@ FusedPlan fused_plan(const TgBatch* b, const TgOut* o) {
     if (force_cl ? cl != force_cl : cl == 3) continue;  // CL = 3 only on request
     const int64_t slice_vec = (nvec + cl - 1) / cl;
     const int64_t nchunk = (slice_vec * 16 + fused_chunk_bytes() - 1) / fused_chunk_bytes();
-    if (nchunk + 2 <= n_slots) {
+    if (nchunk + 2 <= fused_resident_chunks()) {
       // persistent grid: as many clusters as can be co-resident, at most one per row
       int64_t clusters_max = fused_max_clusters(b->dtype, cl);
       if (clusters_max <= 0) clusters_max = d.sms / cl;

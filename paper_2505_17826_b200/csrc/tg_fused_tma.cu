@@ -75,6 +75,7 @@ struct FusedSmemTail {
   uint64_t bbar[2];   // epilogue warp -> consumers: (a, h, lse, s) written
   float4 wpart[2][4 * kConsumerWarps];  // [rank * warps + warp]: every CTA's partials
   float4 bcast[2];  // (a, h, lse, s) of a row, from the epilogue warp
+  uint32_t tmem_base;  // TG_TMEM_STASH: 512 TMEM columns of this CTA
   double stats[16];
 #ifdef TG_FUSED_PROF
   unsigned long long prof[16];
@@ -136,7 +137,50 @@ __device__ __forceinline__ void arrive_u32(uint32_t bar) {
 
 struct RingBase {
   uint32_t ring, full, empty;  // shared addresses of slot 0's data / full / empty barrier
+  uint32_t tmem;               // TMEM stash of this thread (lane, warp's column block), or 0
 };
+
+// ---- TMEM stash of the row slice (TG_TMEM_STASH) ------------------------------
+// Phase 1 copies each thread's raw chunk data (kVecPerThread x 16 B = 16 fp32
+// columns) into its own TMEM lane and frees the shared-memory slot at once; phase
+// 2 reads it back with tcgen05.ld.  The 224 KB ring then only streams (whole-ring
+// read-ahead) and the resident row slices live in the otherwise idle 256 KB of
+// TMEM: warp w owns lanes 32 (w % 4) .. + 31 and columns 128 (w / 4) .. + 127,
+// i.e. a ring of kTSlots chunks per warp (one 152 KB slice + a 3-chunk prefix
+// of the next row at V = 151,936, CL = 2).
+#ifndef TG_TMEM_STASH
+#define TG_TMEM_STASH 1
+#endif
+constexpr bool kStash = TG_TMEM_STASH != 0;
+constexpr int kTSlots = 8;
+constexpr int kTCols = kVecPerThread * 4;  // 32-bit TMEM columns per thread per chunk
+static_assert(!kStash || (kConsumerWarps == 16 && kTSlots * kTCols == 128),
+              "stash layout: 16 consumer warps, 128 columns per warp");
+
+__device__ __forceinline__ uint32_t stash_addr(const RingBase& rb, uint32_t chunk) {
+  return rb.tmem + (chunk % uint32_t(kTSlots)) * uint32_t(kTCols);
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint4 (&u)[4]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(u[0].x), "r"(u[0].y), "r"(u[0].z), "r"(u[0].w), "r"(u[1].x), "r"(u[1].y), "r"(u[1].z),
+      "r"(u[1].w), "r"(u[2].x), "r"(u[2].y), "r"(u[2].z), "r"(u[2].w), "r"(u[3].x), "r"(u[3].y),
+      "r"(u[3].z), "r"(u[3].w)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint4 (&u)[4]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(u[0].x), "=r"(u[0].y), "=r"(u[0].z), "=r"(u[0].w), "=r"(u[1].x), "=r"(u[1].y),
+        "=r"(u[1].z), "=r"(u[1].w), "=r"(u[2].x), "=r"(u[2].y), "=r"(u[2].z), "=r"(u[2].w),
+        "=r"(u[3].x), "=r"(u[3].y), "=r"(u[3].z), "=r"(u[3].w)
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
 
 // Ring position as a running chunk counter: slot = c mod kSlots, mbarrier phase
 // parity = (c / kSlots) & 1 (compile-time divisor: a multiply-shift at most).
@@ -206,7 +250,7 @@ __device__ __forceinline__ void phase1_checked(Acc1& acc, uint4 (&u)[kVecPerThre
   acc.fresh = false;
 }
 
-template <typename T, bool kPartial, bool kMaskTail>
+template <typename T, bool kPartial, bool kMaskTail, bool kStashRow = false>
 __device__ __forceinline__ void phase1_chunk(Acc1& acc, RingIt& it, const RingBase& rb,
                                              int vbase, const Slice& sl, int tid) {
   uint4 u[kVecPerThread];
@@ -222,6 +266,12 @@ __device__ __forceinline__ void phase1_chunk(Acc1& acc, RingIt& it, const RingBa
     const int vec = vbase + g * kConsumers + tid;
     valid[g] = !kPartial || vec < sl.v1;
     u[g] = valid[g] ? lds128(a + g * kConsumers * 16) : Pk<T>::neutral();
+  }
+  if constexpr (kStashRow) {
+    static_assert(kVecPerThread == 4, "16-column stash");
+    tmem_st16(stash_addr(rb, it.c), u);  // raw data, for phase 2
+    __syncwarp();
+    if ((tid & 31) == 0) arrive_u32(it.empty(rb));  // the slot streams on
   }
   it.next();
   if constexpr (!kPartial && !kMaskTail) {
@@ -262,12 +312,14 @@ __device__ __forceinline__ void phase2_chunk(const RingIt& it, const RingBase& r
   constexpr int EPV = Vec<T>::N;
   char* dst = dzrow + int64_t(vbase + tid) * 16;
   const uint32_t a = it.addr(rb) + tid * 16;
+  uint4 su[kVecPerThread];
+  if constexpr (kStash) tmem_ld16(stash_addr(rb, it.c), su);  // whole warp, before any branch
 #pragma unroll
   for (int g = 0; g < kVecPerThread; ++g) {
     const int vec = vbase + g * kConsumers + tid;
     if (!kCheck || vec < sl.v1) {
       float d[EPV];
-      dz_vec<T, kHasH>(lds128(a + g * kConsumers * 16), d, nl2, av2, hz2);
+      dz_vec<T, kHasH>(kStash ? su[g] : lds128(a + g * kConsumers * 16), d, nl2, av2, hz2);
       bool done = false;
       if (kCheck) {
         if (vec == vy) {
@@ -308,8 +360,10 @@ __device__ __forceinline__ void phase2_row(const Slice& sl, RingIt it, const Rin
     else
       phase2_chunk<T, kHasH, false>(it, rb, vbase, sl, dzrow, vy, ye, s_t, nl2, av2, hz2,
                                                 tid);
-    __syncwarp();
-    if (lane == 0) arrive_u32(it.empty(rb));
+    if constexpr (!kStash) {  // (stash: the slot was freed in phase 1)
+      __syncwarp();
+      if (lane == 0) arrive_u32(it.empty(rb));
+    }
     it.next();
     vbase = vend;
   }
@@ -326,11 +380,11 @@ __device__ __forceinline__ void phase1_range(Acc1& acc, RingIt row_it, const Rin
     const int vend = vbase + kVecPerChunk;
     const bool has_tail = sl.tail_vec >= vbase && sl.tail_vec < vend;
     if (vend <= sl.v1 && !has_tail)
-      phase1_chunk<T, false, false>(acc, it, rb, vbase, sl, tid);
+      phase1_chunk<T, false, false, kStash>(acc, it, rb, vbase, sl, tid);
     else if (!has_tail)
-      phase1_chunk<T, true, false>(acc, it, rb, vbase, sl, tid);
+      phase1_chunk<T, true, false, kStash>(acc, it, rb, vbase, sl, tid);
     else
-      phase1_chunk<T, true, true>(acc, it, rb, vbase, sl, tid);
+      phase1_chunk<T, true, true, kStash>(acc, it, rb, vbase, sl, tid);
     vbase = vend;
   }
 }
@@ -386,7 +440,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* ring = smem;
   FusedSmemTail* tail = reinterpret_cast<FusedSmemTail*>(smem + size_t(kSlots) * kChunk);
-  const RingBase rb = {smem_u32(ring), smem_u32(&tail->full[0]), smem_u32(&tail->empty[0])};
+  const RingBase rb0 = {smem_u32(ring), smem_u32(&tail->full[0]), smem_u32(&tail->empty[0]), 0u};
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -406,7 +460,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   sl.tail_vec = (V % EPV) ? nvec - 1 : -1;  // global vector holding columns >= V
   sl.tail_valid = V - (nvec - 1) * EPV;
   // next-row phase-1 chunks that fit in the ring beside this row's slice
-  const int pre = min(min(kMaxPrefixChunks, kSlots - sl.nchunk), sl.nchunk);
+  const int pre = min(min(kMaxPrefixChunks, (kStash ? kTSlots : kSlots) - sl.nchunk), sl.nchunk);
 
   if (tid == 0) {
     for (int i = 0; i < kSlots; ++i) {
@@ -426,10 +480,24 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     }
 #endif
   }
+  if constexpr (kStash) {
+    if (warp == kProducerWarp) {  // one full warp allocates (and later frees) the stash
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       smem_u32(&tail->tmem_base))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  }
   if (CL > 1)
     cluster_sync_all();
   else
     __syncthreads();
+  RingBase rb = rb0;
+  if constexpr (kStash) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    rb.tmem = tail->tmem_base + ((uint32_t(32 * (warp & 3))) << 16) + uint32_t(warp >> 2) * 128u;
+  }
 #ifdef TG_FUSED_PROF
   const long long t_start = clock64();
 #endif
@@ -654,6 +722,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         mbar_wait_u32<TG_SLEEP_BCAST>(smem_u32(&tail->bbar[par]), uint32_t((k >> 1) & 1));
         TG_PROF_ADD(tail, 1);
       }
+      if constexpr (kStash) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       const float4 bc = tail->bcast[par];
       const float a = bc.x, hz = bc.y, s_t = bc.w;
       const float lseL = bc.z * kLog2e;
@@ -675,6 +744,14 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   }
   if (CL > 1)
     cluster_sync_all();  // no CTA leaves while a peer may still st.async into it
+  if constexpr (kStash) {
+    if (CL == 1) __syncthreads();
+    if (warp == kProducerWarp) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tail->tmem_base)
+                   : "memory");
+    }
+  }
 #ifdef TG_FUSED_PROF
   __syncthreads();
   if (tid < 16) g_fused_prof[blockIdx.x][tid] = tail->prof[tid];
@@ -969,6 +1046,9 @@ extern "C" int tg_debug_fused_prof(unsigned long long* out, int n_ctas) {
 
 int fused_chunk_bytes() { return kChunk; }
 int fused_max_slots() { return kSlots; }
+// chunks of a row slice (+ look-ahead) that can stay resident: the shared-memory
+// ring, or with the TMEM stash the per-warp TMEM ring
+int fused_resident_chunks() { return kStash ? kTSlots : kSlots; }
 size_t rowmeta_bytes() { return sizeof(RowMeta); }
 
 }  // namespace tg
