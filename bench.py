@@ -511,9 +511,22 @@ def run_e2e(args, loss, dev, world, rank, n_tok_g, n_seq_g):
     from paper_2505_17826_b200.packing import PackedBatch
 
     K, Lr = args.group_size, args.resp_len
-    rows = K * Lr
     ng = args.e2e_groups
     nbuf = min(3, ng)
+    # pinned host memory: 2 * nbuf * rows * V * 2 bytes per rank (30 GB at the
+    # defaults).  With many ranks per box, shrink the rotation depth, then the
+    # per-call response length (whole groups are kept), to stay within a share
+    # of the host's free memory -- the metric is rows/s either way.
+    try:
+        import psutil
+        budget = 0.4 * psutil.virtual_memory().available / max(world, 1)
+    except Exception:  # pragma: no cover
+        budget = float("inf")
+    if 2 * nbuf * K * Lr * V * 2 > budget and nbuf > 2:
+        nbuf = 2
+    while 2 * nbuf * K * Lr * V * 2 > budget and Lr > 256:
+        Lr //= 2
+    rows = K * Lr
     rng = np.random.default_rng(99 + rank)
     host_in = torch.empty((nbuf, rows, V), dtype=torch.bfloat16, pin_memory=True)
     host_out = torch.empty((nbuf, rows, V), dtype=torch.bfloat16, pin_memory=True)
