@@ -7,30 +7,33 @@
 // write of d loss / d logits (4V bytes per row, the HBM roofline minimum).
 //
 // Design (B200-first):
-//  * A thread-block cluster of CL CTAs (CL = 1 for V <= ~110k bf16, 2 for
-//    Qwen's 151,936) owns one row at a time; CTA rank r owns a contiguous
-//    column slice of the row.  The slice never leaves the SM: a producer warp
-//    streams it into an 8-slot shared-memory ring (28 KB chunks, 224 KB) with
-//    1-D bulk TMA (cp.async.bulk ... mbarrier::complete_tx), a full / empty
-//    mbarrier pair per slot, and prefetches upcoming rows' slices into L2
-//    (cp.async.bulk.prefetch.L2).
-//  * 14 consumer warps, four 16-byte vectors per thread per chunk.  Phase 1
-//    (as chunks land): online max / sum-exp / sum p*z in packed fp32x2
-//    arithmetic (FFMA2 / FADD2) with MUFU ex2; -inf logits are clamped to
-//    -1e30 with packed bf16x2 max; the running max is updated lazily behind a
-//    warp vote.  Each warp posts its partial and arrives on an mbarrier.
-//  * A dedicated epilogue warp merges the partials, reads the target logit
-//    from the resident chunk, exchanges the CTA partial with its cluster peers
-//    through DSMEM (st.async completing tx bytes on the peer's mbarrier;
-//    rank-order merge => bit-identical lse on every CTA), evaluates the
-//    registry epilogue (tg_rowcoef.cuh) and broadcasts (a, h, lse, s) through
-//    a second mbarrier.  Meanwhile the consumers already run phase 1 of the
-//    next row on the ring's free slots, so the epilogue is off their path.
-//  * Phase 2 re-reads the resident chunks from SMEM and writes
-//    dz = p (s + h((z - lse) + H)) - s[v = y] with 128-bit streaming stores,
-//    releasing each slot to the producer, which refills it with the next row.
-//  * Persistent grid: one CTA per SM (16 warps -> 128 registers / thread),
-//    as many clusters as can be co-resident, striding over rows.
+//  * A thread-block cluster of CL CTAs (CL = 1 for V <= ~98k bf16, 2 for
+//    Qwen's 151,936, 4 for fp32 at that vocabulary) owns one row at a time;
+//    CTA rank r owns a contiguous column slice of the row, read from HBM
+//    exactly once: a producer warp streams it into a 7-slot shared-memory ring
+//    (32 KB chunks, 224 KB) with 1-D bulk TMA (cp.async.bulk ...
+//    mbarrier::complete_tx), a full / empty mbarrier pair per slot.
+//  * 16 consumer warps (4 per SM sub-partition), four 16-byte vectors per
+//    thread per chunk.  Phase 1 (as chunks land): online sum-exp / sum p*z in
+//    packed fp32x2 arithmetic (FFMA2 / FADD2) with MUFU ex2, speculatively
+//    against the lane's reference max (clamp / max / rescale only when the
+//    chunk's sums are unsafe).  Each thread copies its raw chunk data into its
+//    own TMEM lane (tcgen05.st) and the shared-memory slot is released at once:
+//    the row slices stay resident in the otherwise idle TMEM, the ring is pure
+//    read-ahead.  Each warp posts its partial to every CTA of the cluster
+//    (DSMEM st.async completing tx bytes on the peers' partials barrier).
+//  * A dedicated epilogue warp merges all CL x 16 partials in a fixed lane
+//    order (bit-identical lse on every CTA), takes the target logit it read
+//    from global memory ahead of the wait, evaluates the registry epilogue
+//    (tg_rowcoef.cuh) and broadcasts (a, h, lse, s) through an mbarrier.
+//    Meanwhile the consumers already run phase 1 of the next row (up to 3
+//    chunks of look-ahead), so the epilogue is off their path.
+//  * Phase 2 reads the resident chunks back from TMEM (tcgen05.ld) and writes
+//    dz = p (s + h((z - lse) + H)) - s[v = y] with 128-bit streaming stores.
+//  * Persistent grid: one CTA per SM (18 warps), as many clusters as can be
+//    co-resident, striding over rows.
+//  * k_fwd_tma (below) is the forward-only sibling: same ring and phase 1,
+//    chunks released after phase 1, no resident rows, no cluster.
 #include "tg_common.cuh"
 #include "tg_rowcoef.cuh"
 #include "tg_vecmath.cuh"
