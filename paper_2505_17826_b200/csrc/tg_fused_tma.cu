@@ -222,8 +222,8 @@ struct Slice {
 // previous row), s >= 2^-20 (no significant term lost to underflow).  Otherwise
 // (a -inf logit gives 0 * -inf = NaN in the sum of p z, a new maximum more
 // than ~22 above m, the first rows) the warp redoes the chunk on the checked
-// path: clamp, vector max, rescale, sums.  The checked path is what partial
-// and tail chunks always take.
+// path: clamp, vector max, rescale, sums.  Partial and tail chunks take the
+// same speculative path (neutral / masked elements contribute exactly 0).
 struct Acc1 {
   Acc2 a;
   bool fresh;  // no chunk of the current row accumulated yet by this lane
@@ -277,7 +277,14 @@ __device__ __forceinline__ void phase1_chunk(Acc1& acc, RingIt& it, const RingBa
     if ((tid & 31) == 0) arrive_u32(it.empty(rb));  // the slot streams on
   }
   it.next();
-  if constexpr (!kPartial && !kMaskTail) {
+  {
+    // partial chunks: lanes past the slice hold the neutral -1e30 vector (p = 0,
+    // p z = 0); the tail vector's columns >= V are masked to -1e30 the same way
+    if constexpr (kMaskTail) {
+#pragma unroll
+      for (int g = 0; g < kVecPerThread; ++g)
+        if (vbase + g * kConsumers + tid == sl.tail_vec) Pk<T>::mask_from(u[g], sl.tail_valid);
+    }
     const uint64_t l2e2 = pk2(kLog2e, kLog2e);
     uint64_t s2 = pk2(0.f, 0.f), t2 = pk2(0.f, 0.f);
 #pragma unroll
