@@ -226,10 +226,49 @@ struct Slice {
 // same speculative path (neutral / masked elements contribute exactly 0).
 struct Acc1 {
   Acc2 a;
-  bool fresh;  // no chunk of the current row accumulated yet by this lane
+  bool fresh;  // no chunk of the current row accumulated yet (warp-uniform)
 };
 
-template <typename T, bool kPartial, bool kMaskTail>
+// kWM (short rows, CL = 1): the reference max m is warp-uniform -- the checked
+// path takes the warp's maximum (one REDUX on an order-preserving integer
+// image of the floats) -- so a warp's per-row partial is (m, sum s, sum t), plain
+// butterfly sums instead of a 5-level online merge.  Measured: +6 % at
+// V = 32,000 (2-chunk rows), -1.5 % at V = 151,936 (5-chunk slices), where
+// per-lane maxima stay.
+__device__ __forceinline__ float warp_max_f(float v) {
+  const int i = __float_as_int(v);
+  const int key = __reduce_max_sync(0xffffffffu, i >= 0 ? i : i ^ 0x7fffffff);
+  return __int_as_float(key >= 0 ? key : key ^ 0x7fffffff);
+}
+
+__device__ __forceinline__ float warp_sum_f(float v) {
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+  return v;
+}
+
+// the warp's partial of the current row (neutral when the warp saw nothing);
+// kWM: m is warp-uniform, plain sums; otherwise an online merge of lane partials
+template <bool kWM>
+__device__ __forceinline__ Online warp_partial(const Acc1& acc) {
+  float s0, s1, t0, t1;
+  upk2(acc.a.s2, s0, s1);
+  upk2(acc.a.t2, t0, t1);
+  float s = s0 + s1, t = t0 + t1;
+  if constexpr (kWM) {
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+      s += __shfl_xor_sync(0xffffffffu, s, d);
+      t += __shfl_xor_sync(0xffffffffu, t, d);
+    }
+    return Online{s > 0.f ? acc.a.m : kNegInf, s, t};
+  } else {
+    // a lane that saw no element of the row carries a stale m: neutral
+    return warp_merge(Online{s > 0.f ? acc.a.m : kNegInf, s, t});
+  }
+}
+
+template <typename T, bool kPartial, bool kMaskTail, bool kWM>
 __device__ __forceinline__ void phase1_checked(Acc1& acc, uint4 (&u)[kVecPerThread],
                                                const bool (&valid)[kVecPerThread], int vbase,
                                                const Slice& sl, int tid) {
@@ -239,8 +278,9 @@ __device__ __forceinline__ void phase1_checked(Acc1& acc, uint4 (&u)[kVecPerThre
     Pk<T>::clamp(u[g]);
     if (kMaskTail && vec == sl.tail_vec) Pk<T>::mask_from(u[g], sl.tail_valid);
   }
-  const float vmax = group_max<T>(u);
-  if (acc.fresh) {  // empty sums: take this chunk's max as the reference
+  const float gmax = group_max<T>(u);
+  const float vmax = kWM ? warp_max_f(gmax) : gmax;
+  if (acc.fresh) {  // empty sums: take this chunk's (warp) max as the reference
     acc.a.m = vmax;
     const float nmL = -vmax * kLog2e;
     acc.a.nm2 = pk2(nmL, nmL);
@@ -253,7 +293,7 @@ __device__ __forceinline__ void phase1_checked(Acc1& acc, uint4 (&u)[kVecPerThre
   acc.fresh = false;
 }
 
-template <typename T, bool kPartial, bool kMaskTail, bool kStashRow = false>
+template <typename T, bool kPartial, bool kMaskTail, bool kStashRow = false, bool kWM = false>
 __device__ __forceinline__ void phase1_chunk(Acc1& acc, RingIt& it, const RingBase& rb,
                                              int vbase, const Slice& sl, int tid) {
   uint4 u[kVecPerThread];
@@ -301,16 +341,23 @@ __device__ __forceinline__ void phase1_chunk(Acc1& acc, RingIt& it, const RingBa
     upk2(s2, s0, s1);
     upk2(t2, t0, t1);
     const float sc = s0 + s1, tc = t0 + t1;
-    const bool ok = sc <= 4294967296.0f && fabsf(tc) <= 3.0e38f &&
-                    (!acc.fresh || sc >= 9.5367431640625e-07f);
-    if (__all_sync(0xffffffffu, ok)) {
+    bool ok;
+    if constexpr (kWM) {
+      ok = __all_sync(0xffffffffu, sc <= 4294967296.0f && fabsf(tc) <= 3.0e38f);
+      if (ok && acc.fresh)  // stale m from the previous row: the warp must keep 2^-20
+        ok = warp_sum_f(sc) >= 9.5367431640625e-07f;
+    } else {
+      ok = __all_sync(0xffffffffu, sc <= 4294967296.0f && fabsf(tc) <= 3.0e38f &&
+                                       (!acc.fresh || sc >= 9.5367431640625e-07f));
+    }
+    if (ok) {
       acc.a.s2 = add2(acc.a.s2, s2);
       acc.a.t2 = add2(acc.a.t2, t2);
       acc.fresh = false;
       return;
     }
   }
-  phase1_checked<T, kPartial, kMaskTail>(acc, u, valid, vbase, sl, tid);
+  phase1_checked<T, kPartial, kMaskTail, kWM>(acc, u, valid, vbase, sl, tid);
 }
 
 // ---- phase 2: dz for one chunk ------------------------------------------------
@@ -380,7 +427,7 @@ __device__ __forceinline__ void phase2_row(const Slice& sl, RingIt it, const Rin
 }
 
 // phase 1 over chunks [c0, c1) of a row whose first chunk is at `row_it`
-template <typename T>
+template <typename T, bool kWM>
 __device__ __forceinline__ void phase1_range(Acc1& acc, RingIt row_it, const RingBase& rb,
                                              const Slice& sl, int c0, int c1, int tid) {
   RingIt it = row_it;
@@ -390,11 +437,11 @@ __device__ __forceinline__ void phase1_range(Acc1& acc, RingIt row_it, const Rin
     const int vend = vbase + kVecPerChunk;
     const bool has_tail = sl.tail_vec >= vbase && sl.tail_vec < vend;
     if (vend <= sl.v1 && !has_tail)
-      phase1_chunk<T, false, false, kStash>(acc, it, rb, vbase, sl, tid);
+      phase1_chunk<T, false, false, kStash, kWM>(acc, it, rb, vbase, sl, tid);
     else if (!has_tail)
-      phase1_chunk<T, true, false, kStash>(acc, it, rb, vbase, sl, tid);
+      phase1_chunk<T, true, false, kStash, kWM>(acc, it, rb, vbase, sl, tid);
     else
-      phase1_chunk<T, true, true, kStash>(acc, it, rb, vbase, sl, tid);
+      phase1_chunk<T, true, true, kStash, kWM>(acc, it, rb, vbase, sl, tid);
     vbase = vend;
   }
 }
@@ -677,7 +724,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     // ===================== consumer warps =====================
     RingIt pos0 = {0u};  // the current row's first chunk
     Acc1 acc = acc_init();
-    if (cid < NR) phase1_range<T>(acc, pos0, rb, sl, 0, pre, tid);  // first row's prefix
+    constexpr bool kWM = CL == 1;  // short rows: warp-uniform reference max
+    if (cid < NR) phase1_range<T, kWM>(acc, pos0, rb, sl, 0, pre, tid);  // first row's prefix
     int y_cur = (cid < NR) ? __ldg(&meta[cid].y) : 0;
     int64_t k = 0;
     for (int64_t row = cid; row < NR; row += ncl, ++k) {
@@ -689,16 +737,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       const int par = int(k & 1);
 
       // ---------------- phase 1 (rest of the row) ----------------
-      phase1_range<T>(acc, pos0, rb, sl, pre, sl.nchunk, tid);
-      Online o;
-      {
-        float s0, s1, t0, t1;
-        upk2(acc.a.s2, s0, s1);
-        upk2(acc.a.t2, t0, t1);
-        const float sl_s = s0 + s1;
-        // a lane that saw no element of the row carries a stale m: neutral
-        o = warp_merge(Online{sl_s > 0.f ? acc.a.m : kNegInf, sl_s, t0 + t1});
-      }
+      phase1_range<T, kWM>(acc, pos0, rb, sl, pre, sl.nchunk, tid);
+      const Online o = warp_partial<kWM>(acc);
       if (lane == 0) {
         // the warp partial goes to every CTA of the cluster (peers: DSMEM st.async
         // completing tx bytes on their partials barrier), so each epilogue merges
@@ -724,7 +764,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       RingIt npos = pos0;
       npos.advance(sl.nchunk);
       acc_new_row(acc);
-      if (nrow < NR) phase1_range<T>(acc, npos, rb, sl, 0, pre, tid);
+      if (nrow < NR) phase1_range<T, kWM>(acc, npos, rb, sl, 0, pre, tid);
 
       // ---------------- phase 2: dz from the resident slice ----------------
       {
@@ -901,14 +941,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_fwd_tma(const KParams P) {
     for (int64_t row = blockIdx.x; row < NR; row += gridDim.x, ++k) {
       acc_new_row(acc);
       phase1_stream_row<T>(acc, it, rb, sl, tid, lane);
-      Online o;
-      {
-        float s0, s1, t0, t1;
-        upk2(acc.a.s2, s0, s1);
-        upk2(acc.a.t2, t0, t1);
-        const float sl_s = s0 + s1;
-        o = warp_merge(Online{sl_s > 0.f ? acc.a.m : kNegInf, sl_s, t0 + t1});
-      }
+      const Online o = warp_partial<false>(acc);
       const int slot = int(k % kFwdPar);
       if (lane == 0) {
         if (k >= kFwdPar)  // the epilogue has read this buffer's previous row
