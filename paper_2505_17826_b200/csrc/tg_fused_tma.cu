@@ -725,7 +725,21 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     RingIt pos0 = {0u};  // the current row's first chunk
     Acc1 acc = acc_init();
     constexpr bool kWM = CL == 1;  // short rows: warp-uniform reference max
-    if (cid < NR) phase1_range<T, kWM>(acc, pos0, rb, sl, 0, pre, tid);  // first row's prefix
+    // Virtual thread index for the chunk layout: the warps of SM sub-partitions
+    // 2 and 3 come first, so a partial last chunk's valid vectors go to them --
+    // sub-partitions 0 and 1 also host the epilogue and producer warps.  (Any
+    // permutation is valid: each thread stashes its own data in its own TMEM
+    // lane and phase 2 uses the same mapping.)
+#ifndef TG_VWARP_PERM
+#define TG_VWARP_PERM 1
+#endif
+    int vtid = tid;
+    if constexpr (TG_VWARP_PERM && kConsumerWarps == 16) {
+      const int q = warp & 3, grp = warp >> 2;
+      const int vw = (q >= 2) ? (grp * 2 + (q - 2)) : (8 + grp * 2 + q);
+      vtid = vw * 32 + lane;
+    }
+    if (cid < NR) phase1_range<T, kWM>(acc, pos0, rb, sl, 0, pre, vtid);  // first row's prefix
     int y_cur = (cid < NR) ? __ldg(&meta[cid].y) : 0;
     int64_t k = 0;
     for (int64_t row = cid; row < NR; row += ncl, ++k) {
@@ -737,7 +751,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       const int par = int(k & 1);
 
       // ---------------- phase 1 (rest of the row) ----------------
-      phase1_range<T, kWM>(acc, pos0, rb, sl, pre, sl.nchunk, tid);
+      phase1_range<T, kWM>(acc, pos0, rb, sl, pre, sl.nchunk, vtid);
       const Online o = warp_partial<kWM>(acc);
       if (lane == 0) {
         // the warp partial goes to every CTA of the cluster (peers: DSMEM st.async
@@ -764,7 +778,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       RingIt npos = pos0;
       npos.advance(sl.nchunk);
       acc_new_row(acc);
-      if (nrow < NR) phase1_range<T, kWM>(acc, npos, rb, sl, 0, pre, tid);
+      if (nrow < NR) phase1_range<T, kWM>(acc, npos, rb, sl, 0, pre, vtid);
 
       // ---------------- phase 2: dz from the resident slice ----------------
       {
@@ -779,9 +793,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       const uint64_t nl2 = pk2(-lseL, -lseL), av2 = pk2(a, a), hz2 = pk2(hz, hz);
       char* dzrow = reinterpret_cast<char*>(P.dz) + row * P.ld_out * ESZ;
       if (hz == 0.f)
-        phase2_row<T, false>(sl, pos0, rb, dzrow, vy, ye, s_t, nl2, av2, hz2, tid, lane);
+        phase2_row<T, false>(sl, pos0, rb, dzrow, vy, ye, s_t, nl2, av2, hz2, vtid, lane);
       else
-        phase2_row<T, true>(sl, pos0, rb, dzrow, vy, ye, s_t, nl2, av2, hz2, tid, lane);
+        phase2_row<T, true>(sl, pos0, rb, dzrow, vy, ye, s_t, nl2, av2, hz2, vtid, lane);
       pos0 = npos;
       y_cur = y_next;
 #ifdef TG_FUSED_PROF
