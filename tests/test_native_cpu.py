@@ -141,3 +141,36 @@ def test_config_validation_and_registry():
         ("opmd", "vanilla", "seq-sum", 0.2)
     assert RFTLossConfig.from_variant("SFT").loss_agg_mode == "seq-mean-token-sum"
     assert RFTLossConfig.from_variant("DPO").coupled
+
+
+def test_lmhead_and_update_argument_validation():
+    """tg_lmhead_logprob_fwd / tg_apply_update reject bad arguments before any
+    device work (no GPU needed)."""
+    L = N.lib()
+    p = ctypes.c_void_p(16)  # never dereferenced: validation fails first
+    # dim not a multiple of 64
+    rc = L.tg_lmhead_logprob_fwd(p, 96, p, 96, 128, 1000, 96, None, None, p, p, None, 0, None)
+    assert rc == N.TG_EINVAL and b"multiple of 64" in L.tg_last_error()
+    # row pitch below dim
+    rc = L.tg_lmhead_logprob_fwd(p, 64, p, 64, 128, 1000, 128, None, None, p, p, None, 0, None)
+    assert rc == N.TG_EINVAL and b"pitch" in L.tg_last_error()
+    # lp without target
+    rc = L.tg_lmhead_logprob_fwd(p, 128, p, 128, 128, 1000, 128, None, p, p, p, None, 0, None)
+    assert rc == N.TG_EINVAL and b"target" in L.tg_last_error()
+    # zero rows: nothing to do
+    assert L.tg_lmhead_logprob_fwd(p, 128, p, 128, 0, 1000, 128, None, None, p, p, None, 0,
+                                   None) == N.TG_OK
+    # apply_update: learning rate, pitch, dtype, too many touched states
+    args = dict(ld_table=100, n_states=8, vocab=100, dtype=N.TG_DTYPE_F32, ld_grad=100,
+                n_touched=2, n_rows=4, lr=0.1)
+
+    def upd(**kw):
+        a = {**args, **kw}
+        return L.tg_apply_update(p, a["ld_table"], a["n_states"], a["vocab"], p, a["dtype"],
+                                 a["ld_grad"], p, p, p, a["n_touched"], a["n_rows"], a["lr"], p,
+                                 None)
+
+    assert upd(lr=0.0) == N.TG_EINVAL and b"learning_rate" in L.tg_last_error()
+    assert upd(ld_grad=50) == N.TG_EINVAL
+    assert upd(dtype=7) == N.TG_EINVAL
+    assert upd(n_touched=70000) == N.TG_EINVAL
