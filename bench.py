@@ -77,7 +77,8 @@ def parse():
     p.add_argument("--mb-groups", type=int, default=8, help="groups per micro-batch")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--e2e-groups", type=int, default=8)
+    p.add_argument("--e2e-groups", type=int, default=0,
+                   help="groups per e2e step (0 = the whole step's groups, as the device metric)")
     p.add_argument("--cpu-rows", type=int, default=256)
     p.add_argument("--quiet", action="store_true")
     p.add_argument("--variant", default="grpo",
@@ -499,7 +500,8 @@ def main():
 
 
 def run_e2e(args, loss, dev, world, rank, n_tok_g, n_seq_g):
-    """Public API with HOST buffers.  A step is `e2e_groups` RFTLoss calls, one
+    """Public API with HOST buffers.  A step is `e2e_groups` (default: all of the
+    step's groups, i.e. the same 1,048,576 rows as the device metric) RFTLoss calls, one
     GRPO group (8 x 2048 rows, 5 GB of bf16 logits) each: the group's logits
     and metadata are copied H2D from pinned memory on a copy stream, the loss
     runs on the compute stream (dlogits in place), and dlogits + the stats
@@ -511,7 +513,7 @@ def run_e2e(args, loss, dev, world, rank, n_tok_g, n_seq_g):
     from paper_2505_17826_b200.packing import PackedBatch
 
     K, Lr = args.group_size, args.resp_len
-    ng = args.e2e_groups
+    ng = args.e2e_groups if args.e2e_groups > 0 else args.groups
     nbuf = min(3, ng)
     # pinned host memory: 2 * nbuf * rows * V * 2 bytes per rank (30 GB at the
     # defaults).  With many ranks per box, shrink the rotation depth, then the
@@ -584,7 +586,7 @@ def run_e2e(args, loss, dev, world, rank, n_tok_g, n_seq_g):
 
     one_step()  # warm
     times = []
-    for _ in range(max(2, min(args.steps, 3))):
+    for _ in range(2):
         t0 = time.perf_counter()
         one_step()
         times.append(time.perf_counter() - t0)
