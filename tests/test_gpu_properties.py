@@ -1,0 +1,84 @@
+"""The reference's invariance / identity tests (test_algorithms.py:194-246),
+restated on the CUDA path at LLM shapes (V = 151,936, bf16 logits): they hold
+for any size, so they check the kernels where the CPU oracle is too slow.
+
+  * reward-shift invariance: adding a constant to every reward of a group
+    leaves OPMD_SIMPLE / KIMI / PAIRWISE and GRPO losses and gradients
+    unchanged (test_algorithms.py:194-227);
+  * pairwise / simple identity at the reference point: grad[pairwise] /
+    (1 + tau)^2 == (2 tau K / (1 + tau)) grad[simple]  (test_algorithms.py:230-246);
+  * dlogits rows sum to zero (softmax gradient, test_policy.py:444-451), to
+    fp32 accuracy.
+Tolerances: bf16 dlogits, |a - b| <= 2^-7 max|b| (two bf16 roundings)."""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2505_17826_b200 import RFTLoss, RFTLossConfig, logprob_fwd, pack_arrays
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs CUDA", allow_module_level=True)
+
+V = 151936
+
+
+def batch(seed, lens, groups, reward, seq_ref_lp=None, fp32=False):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    T = int(sum(lens))
+    x = torch.randn(T, V, device="cuda", generator=g) * 2.0
+    tgt = np.random.default_rng(seed).integers(0, V, T)
+    x[torch.arange(T, device="cuda"), torch.as_tensor(tgt, device="cuda")] += 13.5
+    x = x if fp32 else x.to(torch.bfloat16)
+    return pack_arrays(x, tgt, lens, groups, np.asarray(reward, np.float32),
+                       seq_ref_lp=seq_ref_lp)
+
+
+def close(a, b, rel=2.0 ** -7):
+    a, b = a.float(), b.float()
+    scale = float(b.abs().max())
+    assert float((a - b).abs().max()) <= rel * scale + 1e-12
+
+
+@pytest.mark.parametrize("cfg", [RFTLossConfig.from_variant("OPMD_SIMPLE", tau=0.6),
+                                 RFTLossConfig.from_variant("OPMD_KIMI", tau=0.6),
+                                 RFTLossConfig.from_variant("OPMD_PAIRWISE", tau=0.6),
+                                 RFTLossConfig(advantage_fn="grpo", policy_loss_fn="ppo_clip",
+                                               loss_agg_mode="token-mean")],
+                         ids=["simple", "kimi", "pairwise", "grpo_ppo"])
+def test_reward_shift_invariance(cfg):
+    lens, groups = [40, 25, 33, 18, 27, 31], [3, 3]
+    reward = [0.9, 0.1, 0.4, 1.0, 0.0, 0.5]
+    a = RFTLoss(cfg)(batch(1, lens, groups, reward))
+    b = RFTLoss(cfg)(batch(1, lens, groups, [r + 7.5 for r in reward]))
+    la, lb = a.stats_dict()["loss"], b.stats_dict()["loss"]
+    assert lb == pytest.approx(la, rel=1e-5, abs=1e-6)
+    close(b.dlogits, a.dlogits)
+
+
+def test_pairwise_simple_gradient_identity_at_reference_point():
+    tau, lens, groups = 0.8, [30, 22, 41, 17], [4]
+    reward = [1.3, -0.2, 0.6, 0.9]
+    probe = batch(2, lens, groups, reward, fp32=True)
+    seq_lp = logprob_fwd(probe)[3].double().cpu().numpy()  # LP_i: the reference point
+    b = batch(2, lens, groups, reward, seq_ref_lp=seq_lp.astype(np.float32), fp32=True)
+    pair = RFTLoss(RFTLossConfig.from_variant("OPMD_PAIRWISE", tau=tau))(b)
+    simple = RFTLoss(RFTLossConfig.from_variant("OPMD_SIMPLE", tau=tau))(b)
+    k = len(lens)
+    lhs = pair.dlogits / (1.0 + tau) ** 2
+    rhs = simple.dlogits * (2.0 * tau * k / (1.0 + tau))
+    close(lhs, rhs, rel=1e-4)  # fp32 logits and dlogits
+
+
+def test_dlogits_rows_sum_to_zero():
+    lens, groups = [64, 64, 64, 64], [2, 2]
+    out = RFTLoss(RFTLossConfig(advantage_fn="grpo", policy_loss_fn="ppo_clip",
+                                kl_fn="low_var_kl", kl_coef=0.001,
+                                loss_agg_mode="token-mean"))(
+        batch(3, lens, groups, [1.0, 0.0, 0.0, 1.0], fp32=True))
+    # a row sums to s (sum_v p_v - 1): fp32 with ex2.approx over 151,936 terms
+    # keeps |sum p - 1| at a few 1e-6 (the reference's f64 bound is 1e-12)
+    rows = out.dlogits.double().sum(1)
+    assert float(rows.abs().max()) <= 1e-5 * float(out.dlogits.abs().max())
