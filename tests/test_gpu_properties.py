@@ -82,3 +82,45 @@ def test_dlogits_rows_sum_to_zero():
     # keeps |sum p - 1| at a few 1e-6 (the reference's f64 bound is 1e-12)
     rows = out.dlogits.double().sum(1)
     assert float(rows.abs().max()) <= 1e-5 * float(out.dlogits.abs().max())
+
+
+def test_baseline_size_micro_batch_properties():
+    """One full micro-batch of BASELINE configs[1] (8 groups x 8 x 2,048 =
+    131,072 rows x V = 151,936 bf16: 40 GB in, 40 GB out) -- sizes the oracle
+    cannot reach, checked through properties: the fused kernel and the
+    two-pass route agree, its lp equals the forward-only kernel's, dz[y] =
+    s (e^lp - 1) on every row, statistics are exact counts, and reruns are
+    bit-identical."""
+    T, lens, groups = 131072, [2048] * 64, [8] * 8
+    x = torch.empty((T, V), dtype=torch.bfloat16, device="cuda")
+    g = torch.Generator(device="cuda").manual_seed(11)
+    for r in range(0, T, 8192):
+        x[r:r + 8192].normal_(0.0, 2.0, generator=g)
+    tgt = np.random.default_rng(11).integers(0, V, T)
+    tgt_d = torch.as_tensor(tgt, device="cuda")
+    x[torch.arange(T, device="cuda"), tgt_d] += 13.5
+    reward = np.random.default_rng(12).integers(0, 2, 64).astype(np.float32)
+    b = pack_arrays(x, tgt, lens, groups, reward)
+    cfg = RFTLossConfig(advantage_fn="grpo", policy_loss_fn="vanilla", loss_agg_mode="token-mean")
+    loss = RFTLoss(cfg)
+    assert loss.route(b) == 1
+    dz = torch.empty_like(x)
+    out = loss(b, dlogits=dz)
+    st = out.stats_dict()
+    assert st["n_tok"] == T and st["n_seqs"] == 64 and st["n_groups"] == 8
+    assert st["nonfinite"] == 0 and st["invalid"] == 0
+    lp_fwd = logprob_fwd(b)[0]
+    assert float((out.lp - lp_fwd).abs().max()) <= 1e-4
+    s = out.seq_adv.repeat_interleave(2048) / T  # token-mean weight
+    dzy = dz[torch.arange(T, device="cuda"), tgt_d].float()
+    expect = s * (torch.exp(out.lp) - 1.0)
+    assert torch.all((dzy - expect).abs() <= 1e-2 * expect.abs() + 1e-9)
+    again = loss(b, dlogits=torch.empty_like(x))
+    assert torch.equal(again.dlogits, dz) and torch.equal(again.stats, out.stats)
+    del again
+    two = RFTLoss(cfg.with_(force_two_pass=True))(b, dlogits=torch.empty_like(x))
+    scale = max(float(dz[r:r + 8192].float().abs().max()) for r in range(0, T, 8192))
+    diff = max(float((two.dlogits[r:r + 8192].float() - dz[r:r + 8192].float()).abs().max())
+               for r in range(0, T, 8192))  # chunked: a full fp32 copy would be 80 GB
+    assert diff <= 2.0 ** -8 * scale
+    assert two.stats_dict()["loss"] == pytest.approx(st["loss"], rel=1e-5, abs=1e-9)
