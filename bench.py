@@ -20,9 +20,17 @@ One process per GPU (torchrun for N > 1); each rank processes its own
 statistics vector per step.  `value` = rows of all ranks / max-over-ranks
 device time.  `e2e` = the same metric through the public API with pinned
 HOST logits: H2D of the logits + metadata and D2H of dlogits + stats inside
-the timed region.
+the timed region, one e2e step = the same 1,048,576 rows (64 calls, 3-deep
+copy / compute overlap).
+
+`--variant c1|c3|c4|c5` runs the per-GPU workloads of BASELINE configs[0],
+[2], [3], [4] (V = 32,000; PPO + k3 + entropy at 4,096 tokens; GRPO + SFT mix;
+ragged long-CoT through row_index); `grpo_two_pass`, `opmd_kimi`,
+`opmd_pairwise` measure the two-pass / sequence-coupled routes.  Kernel A/B:
+TG_LOSS_LIB selects a library build (scripts/gpu_libab.sh).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--variant V]
 """
 
 from __future__ import annotations
