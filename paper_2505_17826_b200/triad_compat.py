@@ -209,6 +209,79 @@ def group_loss(group, params, config: AlgorithmConfig, sft_params=None,
     return group_losses([group], params, config, sft_params=sft_params, ref_params=ref_params)
 
 
+# ---- the per-variant entry points and helpers of algorithms.py ----------------
+
+def loss_opmd_kimi(group, params, config: AlgorithmConfig, ref_params=None) -> LossReport:
+    """algorithms.py:118-153 (ref_logprobs from the group unless ref_params)."""
+    if config.tau <= 0:
+        raise AlgorithmError("OPMD_KIMI requires tau > 0")
+    if ref_params is None and getattr(group, "ref_logprobs", None) is None:
+        raise AlgorithmError("OPMD_KIMI requires ref_logprobs")
+    return group_losses([group], params, _as_variant(config, Variant.OPMD_KIMI),
+                        ref_params=ref_params)
+
+
+def loss_opmd_pairwise(group, params, config: AlgorithmConfig) -> LossReport:
+    """algorithms.py:156-190."""
+    return group_losses([group], params, _as_variant(config, Variant.OPMD_PAIRWISE))
+
+
+def loss_opmd_simple(group, params, config: AlgorithmConfig, sft_params=None) -> LossReport:
+    """algorithms.py:220-253 (plus beta * regularizer_g with an anchor table)."""
+    return group_losses([group], params, _as_variant(config, Variant.OPMD_SIMPLE),
+                        sft_params=sft_params)
+
+
+def _as_variant(config: AlgorithmConfig, variant: Variant) -> AlgorithmConfig:
+    return AlgorithmConfig(variant, tau=config.tau, beta=config.beta, dpo_beta=config.dpo_beta,
+                           learning_rate=config.learning_rate)
+
+
+def tau_log_zhat(rewards: Sequence[float], tau: float) -> float:
+    """algorithms.py:93-101 (host helper; the kernels compute it per group)."""
+    if tau <= 0:
+        raise AlgorithmError(f"tau must be > 0, got {tau}")
+    if not rewards:
+        raise AlgorithmError("rewards must be nonempty")
+    m = max(rewards)
+    mean_exp = sum(math.exp((r - m) / tau) for r in rewards) / len(rewards)
+    return m + tau * math.log(mean_exp)
+
+
+def experience_logprob(params, exp) -> float:
+    """algorithms.py:81-85: total logprob of a stored experience under params
+    (tg_logprob_fwd over the table rows it scores)."""
+    dev = _device()
+    h = flatten_groups([_OneGroup([exp if exp.reward is not None else _with_reward(exp)])])
+    S, V = int(params.num_buckets), int(params.vocab.size)
+    states, target = scored_states(h, S)
+    _check_vocab(h, target, V)
+    if target.size == 0:
+        return 0.0
+    return float(_seq_logprob(_table(params, dev), states, target, h.seq_lengths)[0])
+
+
+def experience_grad(params, exp) -> SparseGrad:
+    """algorithms.py:88-90: d logprob / d table rows (e_y - p per scored token)
+    -- the negated gradient of SFT's loss over the single experience."""
+    rep = loss_sft([exp], params)
+    return rep.gradient.scaled(-1.0)
+
+
+def regularizer_g(params, sft_params, group) -> Tuple[float, SparseGrad]:
+    """algorithms.py:193-217: the anchor KL term alone -- OPMD_SIMPLE with
+    beta = 1 over the group with its rewards zeroed (the centred policy term
+    then vanishes identically)."""
+    if tuple(np.shape(params.logits)) != tuple(np.shape(sft_params.logits)):
+        raise AlgorithmError(f"parameter shapes differ: {np.shape(params.logits)} vs "
+                             f"{np.shape(sft_params.logits)}")
+    zeroed = _OneGroup([_with_reward(e) for e in group.experiences],
+                       getattr(group, "ref_logprobs", None))
+    cfg = RFTLossConfig.from_variant(Variant.OPMD_SIMPLE, 0.0, 1.0)
+    rep = _run([zeroed], params, cfg, anchor=sft_params)
+    return rep.loss, rep.gradient
+
+
 class _OneGroup:
     def __init__(self, exps, ref=None):
         self.experiences = list(exps)
