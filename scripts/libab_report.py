@@ -18,4 +18,5 @@ for v, ds in rows.items():
         r = d["roofline"]
         print(f"{v:12s} {d['value'] / 1e6:7.3f} Mtok/s  fused {r['achieved']:7.1f} GB/s "
               f"frac {r['frac']:.3f} ({r['kernel_ms']:.3f} ms)  sm {d['clocks']['sm_mhz']} "
+              f"{d['clocks'].get('power_w', '-')} W "
               f"{d['clocks']['reasons']}  loss {d['check']['loss']:.6e}")
