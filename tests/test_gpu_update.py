@@ -72,8 +72,11 @@ def test_apply_update_refuses_nonfinite_and_bad_state():
     assert torch.equal(table, before)
 
 
-def test_device_trainer_matches_host_trainer():
-    """Three GRPO-analogue steps (OPMD_SIMPLE, reference golden inputs): the
+@pytest.mark.parametrize("name,variant,tau", [("simple_tau05", "OPMD_SIMPLE", 0.5),
+                                              ("kimi", "OPMD_KIMI", 1.0),
+                                              ("pairwise", "OPMD_PAIRWISE", 1.0)])
+def test_device_trainer_matches_host_trainer(name, variant, tau):
+    """Three steps of each reference group loss (golden inputs): the
     device-resident table + tg_apply_update equals the host numpy path."""
     from _golden import groups_of, load
 
@@ -89,9 +92,10 @@ def test_device_trainer_matches_host_trainer():
                 size = self.logits.shape[1]
             self.vocab = vocab if vocab is not None else _V()
 
-    fx = load("simple_tau05")
+    fx = load(name)
     groups = groups_of(fx)
-    algo = C.AlgorithmConfig("OPMD_SIMPLE", tau=0.5, learning_rate=0.1)
+    algo = C.AlgorithmConfig(variant, tau=float(fx["tau"]) if "tau" in fx else tau,
+                             learning_rate=0.1)
     host = C.Trainer(P(fx["theta"]), algo)
     dev = C.DeviceTrainer(P(fx["theta"]), algo)
     for _ in range(3):
