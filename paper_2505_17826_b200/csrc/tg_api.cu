@@ -56,7 +56,7 @@ size_t fwd_tma_smem_bytes();
 void launch_bwd(const KParams& P, bool anchor, bool vec, int grid, cudaStream_t st);
 void launch_rowcoef(const KParams& P, const void* meta, bool coupled, bool anchor, int grid,
                     cudaStream_t st);
-void launch_group_prep(const KParams& P, bool coupled, cudaStream_t st);
+int launch_group_prep(const KParams& P, bool coupled, cudaStream_t st);
 void launch_rowmeta(const KParams& P, void* meta, cudaStream_t st);
 void launch_seq_reduce(const KParams& P, cudaStream_t st);
 void launch_coupled(const KParams& P, cudaStream_t st);
@@ -424,9 +424,7 @@ int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspa
 
   cudaEvent_t ev_begin = g_ev_begin, ev_end = g_ev_end;
   g_ev_begin = g_ev_end = nullptr;
-  launch_group_prep(P, coupled, st);
-  launch_rowmeta(P, meta, st);
-  count_launches(1 + (b->n_groups > 0 ? 1 : 0) + (b->n_seqs > 0 ? 1 : 0));
+  count_launches(launch_group_prep(P, coupled, st));
   if (route == 1) {
     const FusedPlan fp = fused_plan(b, o);
     // TG_FUSED_IMPL=l2: the L2-reread variant (tg_fused_l2.cu), for A/B
@@ -436,6 +434,10 @@ int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspa
     P.n_partials = l2 ? l2_ctas : fp.n_ctas;
     if (P.n_partials > kMaxPartials) return fail(TG_EUNSUPPORTED, "too many CTAs");
     if (b->n_rows > 0) {
+      if (l2) {  // the L2 variant reads the packed per-row metadata
+        launch_rowmeta(P, meta, st);
+        count_launches(b->n_seqs > 0 ? 1 : 0);
+      }
       if (ev_begin) cudaEventRecord(ev_begin, st);
       cudaError_t e = l2 ? launch_fused_l2(P, meta, l2_ctas, fp.prefetch_rows, st)
                          : launch_fused(P, meta, fp.cl, fp.n_slots, fp.n_ctas, fp.prefetch_rows, st);
@@ -448,6 +450,8 @@ int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspa
     launch_seq_reduce(P, st);
     count_launches(b->n_seqs > 0 ? 1 : 0);
   } else {
+    launch_rowmeta(P, meta, st);
+    count_launches(b->n_seqs > 0 ? 1 : 0);
     const bool vin = vec_ok(b->logits, b->ld, esz) &&
                      (!anchor || vec_ok(b->anchor_logits, b->ld_anchor, esz));
     const int grid = stream_grid(b->n_rows);

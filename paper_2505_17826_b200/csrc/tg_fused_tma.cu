@@ -210,6 +210,35 @@ struct Slice {
   int v0, v1, nchunk, tail_vec, tail_valid;
 };
 
+// Row metadata built on the fly from the per-sequence arrays of the group
+// prologue (no packed RowMeta pass): a CTA's rows ascend, so its sequence
+// cursor only moves forward (amortised O(1) per row).
+__device__ __forceinline__ RowMeta row_meta(const KParams& P, int64_t row, int& seq) {
+  while (seq + 1 < P.n_seqs && int64_t(P.seq_off[seq + 1]) <= row) ++seq;
+  RowMeta m;
+  m.y = P.target[row];
+  m.seq = seq;
+  m.A = P.sA[seq];
+  m.w = P.sW[seq];
+  m.old = P.old_lp ? P.old_lp[row] : 0.f;
+  m.ref = P.ref_lp ? P.ref_lp[row] : 0.f;
+  const bool rl = P.seq_kind == nullptr || P.seq_kind[seq] == 0;
+  const bool bad = m.y < 0 || int64_t(m.y) >= P.vocab;
+  m.flags = (rl ? 1u : 0u) | (bad ? 2u : 0u);
+  m.ca = P.anchor_beta > 0.f ? P.anchor_beta / P.sK[seq] : 0.f;
+  return m;
+}
+
+// first sequence containing `row` (binary search over the prefix sums)
+__device__ __forceinline__ int seq_of_row(const KParams& P, int64_t row) {
+  int lo = 0, hi = P.n_seqs;  // invariant: seq_off[lo] <= row < seq_off[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (int64_t(P.seq_off[mid]) <= row) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
 // ---- phase 1: one chunk (kVecPerThread vectors per consumer thread) ---------
 // kPartial: the chunk may run past the slice end (lanes there use a neutral
 // -1e30 vector and skip the sums, but still vote, so the rescale test is
@@ -609,19 +638,27 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     double sd[15];
 #pragma unroll
     for (int i = 0; i < 15; ++i) sd[i] = 0.0;
+    // the row's metadata and target logit are fetched one row ahead (after the
+    // previous row's broadcast), so their dependent loads stay off the path
+    int seq_cur = (lane == 0 && cid < NR) ? seq_of_row(P, cid) : 0;
+    RowMeta nxt;
+    float nzy = kNegInf;
+    auto fetch = [&](int64_t r) {
+      nxt = row_meta(P, r, seq_cur);
+      nzy = kNegInf;  // raw, unclamped target logit
+      if (nxt.y >= 0 && nxt.y < V) {
+        const int64_t src_row = P.row_index ? P.row_index[r] : r;
+        nzy = Vec<T>::load1(reinterpret_cast<const char*>(P.logits) + src_row * P.ld * ESZ, nxt.y);
+      }
+    };
+    if (lane == 0 && cid < NR) fetch(cid);
     int64_t k = 0;
     for (int64_t row = cid; row < NR; row += ncl, ++k) {
       const int par = int(k & 1);
       const uint32_t parity = uint32_t((k >> 1) & 1);
-      RowMeta cur;
-      float tzy = kNegInf;  // the target logit, read ahead of the wait (raw, unclamped)
+      const RowMeta cur = nxt;
+      const float tzy = nzy;
       if (lane == 0) {
-        cur = load_meta(meta, row);
-        const int y = cur.y;
-        if (y >= 0 && y < V) {
-          const int64_t src_row = P.row_index ? P.row_index[row] : row;
-          tzy = Vec<T>::load1(reinterpret_cast<const char*>(P.logits) + src_row * P.ld * ESZ, y);
-        }
         if constexpr (CL > 1)
           mbar_arrive_expect_tx(&tail->pbar[par], (CL - 1) * kConsumerWarps * 16);
       }
@@ -670,6 +707,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         }
         tail->bcast[par] = make_float4(o.s + o.h * (H - lse), o.h, lse, o.s);
         arrive_u32(smem_u32(&tail->bbar[par]));
+        if (row + ncl < NR) fetch(row + ncl);
 #ifdef TG_FUSED_PROF
         tail->prof[7] += (unsigned long long)(clock64() - t_crit);
         tail->prof[8] += (unsigned long long)(clock64() - t_xdone);
@@ -740,11 +778,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       vtid = vw * 32 + lane;
     }
     if (cid < NR) phase1_range<T, kWM>(acc, pos0, rb, sl, 0, pre, vtid);  // first row's prefix
-    int y_cur = (cid < NR) ? __ldg(&meta[cid].y) : 0;
+    int y_cur = (cid < NR) ? __ldg(&P.target[cid]) : 0;
     int64_t k = 0;
     for (int64_t row = cid; row < NR; row += ncl, ++k) {
       const int64_t nrow = row + ncl;
-      const int y_next = (nrow < NR) ? __ldg(&meta[nrow].y) : 0;  // prefetch
+      const int y_next = (nrow < NR) ? __ldg(&P.target[nrow]) : 0;  // prefetch
       const int y = y_cur;
       const int vy = (y >= 0 && y < V) ? (y / EPV) : -1;  // global vector holding the target
       const int ye = (vy >= 0) ? y - vy * EPV : 0;

@@ -57,13 +57,10 @@ __global__ void k_counts(const KParams P) {
   if (threadIdx.x < 4) P.counts[threadIdx.x] = int64_t(c[threadIdx.x]);
 }
 
-__global__ void k_prep(const KParams P) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= P.n_groups) return;
+// group g's advantages and aggregation weights (per sequence) and metrics
+__device__ void prep_group(const KParams& P, int g, int64_t n_tok, int64_t n_seq,
+                           int64_t n_sft) {
   const int a = P.grp_off[g], b = P.grp_off[g + 1];
-  const int64_t n_tok = P.n_tok_g > 0 ? P.n_tok_g : P.counts[0];
-  const int64_t n_seq = P.n_seq_g > 0 ? P.n_seq_g : P.counts[1];
-  const int64_t n_sft = P.n_sft_g > 0 ? P.n_sft_g : P.counts[2];
   double sum = 0.0;
   int k = 0;
   for (int i = a; i < b; ++i)
@@ -115,6 +112,49 @@ __global__ void k_prep(const KParams P) {
   P.gF[4 * g + 1] = mean;
   P.gF[4 * g + 2] = 0.0;
   P.gF[4 * g + 3] = double(k);
+}
+
+__global__ void k_prep(const KParams P) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= P.n_groups) return;
+  prep_group(P, g, P.n_tok_g > 0 ? P.n_tok_g : P.counts[0],
+             P.n_seq_g > 0 ? P.n_seq_g : P.counts[1], P.n_sft_g > 0 ? P.n_sft_g : P.counts[2]);
+}
+
+// k_counts + k_prep in one CTA (one launch instead of two on every call):
+// the batch counts are reduced in shared memory, then the threads stride over
+// the groups.
+__global__ void __launch_bounds__(1024) k_counts_prep(const KParams P) {
+  __shared__ unsigned long long c[4];
+  if (threadIdx.x < 4) c[threadIdx.x] = 0;
+  __syncthreads();
+  unsigned long long rl_rows = 0, rl_seqs = 0, sft = 0, bad = 0;
+  for (int i = threadIdx.x; i < P.n_seqs; i += blockDim.x) {
+    const int n = P.seq_off[i + 1] - P.seq_off[i];
+    if (n < 0) ++bad;
+    if (is_rl(P, i)) {
+      rl_rows += n > 0 ? n : 0;
+      ++rl_seqs;
+    } else {
+      ++sft;
+    }
+  }
+  for (int g = threadIdx.x; g < P.n_groups; g += blockDim.x) {
+    const int k = P.grp_off[g + 1] - P.grp_off[g];
+    if (k < 1) ++bad;
+    if (P.pg == TG_PG_OPMD_PAIRWISE && k < 2) ++bad;
+    if (P.pg == TG_PG_DPO && k != 2) ++bad;
+  }
+  if (rl_rows) atomicAdd(&c[0], rl_rows);
+  if (rl_seqs) atomicAdd(&c[1], rl_seqs);
+  if (sft) atomicAdd(&c[2], sft);
+  if (bad) atomicAdd(&c[3], bad);
+  __syncthreads();
+  if (threadIdx.x < 4) P.counts[threadIdx.x] = int64_t(c[threadIdx.x]);
+  const int64_t n_tok = P.n_tok_g > 0 ? P.n_tok_g : int64_t(c[0]);
+  const int64_t n_seq = P.n_seq_g > 0 ? P.n_seq_g : int64_t(c[1]);
+  const int64_t n_sft = P.n_sft_g > 0 ? P.n_sft_g : int64_t(c[2]);
+  for (int g = threadIdx.x; g < P.n_groups; g += blockDim.x) prep_group(P, g, n_tok, n_seq, n_sft);
 }
 
 // one warp per sequence
@@ -299,13 +339,17 @@ __global__ void k_finalize(const KParams P, int coupled) {
 
 // ---------------------------------------------------------------------------
 
-void launch_group_prep(const KParams& P, bool coupled, cudaStream_t st) {
-  k_counts<<<1, 256, 0, st>>>(P);
-  if (P.n_groups > 0 && !coupled) k_prep<<<(P.n_groups + 127) / 128, 128, 0, st>>>(P);
-  if (P.n_groups > 0 && coupled) {
-    // coupled variants need A only after the forward; give rowmeta neutral values now
-    k_prep<<<(P.n_groups + 127) / 128, 128, 0, st>>>(P);
+// counts + group prep: one CTA for batches of up to 8,192 groups (every
+// realistic micro-batch), two kernels beyond
+int launch_group_prep(const KParams& P, bool coupled, cudaStream_t st) {
+  (void)coupled;  // coupled variants get neutral per-sequence values now, A after the forward
+  if (P.n_groups <= 8192) {
+    k_counts_prep<<<1, 1024, 0, st>>>(P);
+    return 1;
   }
+  k_counts<<<1, 256, 0, st>>>(P);
+  k_prep<<<(P.n_groups + 127) / 128, 128, 0, st>>>(P);
+  return 2;
 }
 
 void launch_rowmeta(const KParams& P, void* meta, cudaStream_t st) {
