@@ -88,8 +88,9 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
             _run(["g++", "-O2", "-std=c++17", "-fPIC", "-I", str(ROOT / "include"), "-c",
                   str(CSRC / src), "-o", str(obj)], verbose)
     if force or _stale(LIB_, objs):
-        _run([nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(LIB_), *map(str, objs)],
-             verbose)
+        # --no-undefined: a missing definition fails the build, not the dlopen
+        _run([nvcc(), *ARCH, "-shared", "-cudart", "static", "-Xlinker", "--no-undefined",
+              "-o", str(LIB_), *map(str, objs)], verbose)
     return LIB_
 
 
