@@ -100,7 +100,11 @@ enum {
 enum {
   TG_FLAG_FORCE_TWO_PASS = 1,  /* use the forward + backward streaming kernels even when
                                   the fused single-pass kernel applies (testing / A-B)  */
-  TG_FLAG_NO_FUSED_TMA = 2     /* alias kept for clarity: same effect                   */
+  TG_FLAG_NO_FUSED_TMA = 2,    /* alias kept for clarity: same effect                   */
+  TG_FLAG_ROWS_GIVEN = 4       /* forward-only loss from precomputed per-row values: out.lp,
+                                  out.entropy, out.lse are INPUTS (e.g. from
+                                  tg_lmhead_logprob_fwd); no logits are read (batch.logits
+                                  may be NULL) and out.dlogits must be NULL               */
 };
 
 /* stats[] layout (double).  Sums are over this call's rows / groups; the

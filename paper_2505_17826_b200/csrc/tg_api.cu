@@ -156,7 +156,7 @@ bool coupled_pg(int pg) {
   return pg == TG_PG_OPMD_KIMI || pg == TG_PG_OPMD_PAIRWISE || pg == TG_PG_DPO;
 }
 
-int validate_batch(const TgBatch* b) {
+int validate_batch(const TgBatch* b, bool rows_given = false) {
   if (!b) return fail(TG_EINVAL, "batch is NULL");
   if (b->dtype != TG_DTYPE_BF16 && b->dtype != TG_DTYPE_F32)
     return fail(TG_EINVAL, "unknown dtype %d", b->dtype);
@@ -166,7 +166,7 @@ int validate_batch(const TgBatch* b) {
   if (b->vocab < 1) return fail(TG_EINVAL, "vocab must be >= 1, got %lld", (long long)b->vocab);
   if (b->ld < b->vocab)
     return fail(TG_EINVAL, "ld %lld < vocab %lld", (long long)b->ld, (long long)b->vocab);
-  if (b->n_rows > 0 && (!b->logits || !b->target))
+  if (b->n_rows > 0 && ((!b->logits && !rows_given) || !b->target))
     return fail(TG_EINVAL, "logits and target are required when n_rows > 0");
   if (!b->seq_offsets) return fail(TG_EINVAL, "seq_offsets is required");
   if (b->n_groups > 0 && !b->group_offsets) return fail(TG_EINVAL, "group_offsets is required");
@@ -349,6 +349,7 @@ void run_forward(const KParams& P, const TgBatch* b, bool anchor, bool vin, int 
 
 int route_of(const TgBatch* b, const TgConfig* c, const TgOut* o) {
   if (coupled_pg(c->policy_loss_fn)) return 3;
+  if (c->flags & TG_FLAG_ROWS_GIVEN) return 2;
   if (c->anchor_beta > 0) return 2;
   if (c->flags & (TG_FLAG_FORCE_TWO_PASS | TG_FLAG_NO_FUSED_TMA)) return 2;
   if (!o || !o->dlogits) return 2;
@@ -397,7 +398,15 @@ int tg_route(const TgBatch* batch, const TgConfig* cfg) {
 
 int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspace,
                     size_t workspace_bytes, void* stream) {
-  int rc = validate_batch(b);
+  const bool rows_given = c && (c->flags & TG_FLAG_ROWS_GIVEN);
+  if (rows_given) {
+    if (!o || !o->lp || !o->entropy || !o->lse)
+      return fail(TG_EINVAL, "TG_FLAG_ROWS_GIVEN needs out.lp, out.entropy and out.lse (inputs)");
+    if (o->dlogits) return fail(TG_EINVAL, "TG_FLAG_ROWS_GIVEN is forward-only: dlogits must be NULL");
+    if (b && b->anchor_logits)
+      return fail(TG_EINVAL, "TG_FLAG_ROWS_GIVEN cannot evaluate the anchor KL (needs logits)");
+  }
+  int rc = validate_batch(b, rows_given);
   if (rc) return rc;
   rc = validate_cfg(b, c);
   if (rc) return rc;
@@ -456,7 +465,7 @@ int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspa
                      (!anchor || vec_ok(b->anchor_logits, b->ld_anchor, esz));
     const int grid = stream_grid(b->n_rows);
     if (ev_begin) cudaEventRecord(ev_begin, st);
-    if (b->n_rows > 0) {
+    if (b->n_rows > 0 && !rows_given) {
       run_forward(P, b, anchor, vin, grid, st);
       count_launches(1);
     }

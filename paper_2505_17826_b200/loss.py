@@ -202,6 +202,44 @@ class RFTLoss:
         out.dlogits = dz
         return out
 
+    def from_rows(self, batch: PackedBatch, lp: torch.Tensor, entropy: torch.Tensor,
+                  lse: torch.Tensor, *, n_tok_global: int = 0, n_seq_global: int = 0,
+                  n_sft_seq_global: int = 0, stream: Optional[torch.cuda.Stream] = None
+                  ) -> LossOutput:
+        """Forward-only loss and metrics from precomputed per-row lp / entropy /
+        lse (``TG_FLAG_ROWS_GIVEN``), e.g. from ``lmhead_logprob_fwd``: no
+        logits are read, so a batch built with ``rows_batch`` (empty logits)
+        suffices.  Anchor KL needs logits and is rejected."""
+        L = N.lib()
+        cb = c_batch(batch)
+        cfg = self.cfg
+        if cfg.coupled and cfg.policy_loss_fn == "dpo" and n_seq_global == 0:
+            n_seq_global = batch.n_seqs
+        cc = cfg.to_c(n_tok_global, n_seq_global, n_sft_seq_global)
+        cc.flags |= N.TG_FLAG_ROWS_GIVEN
+        dev = batch.device
+        T, B = batch.n_rows, batch.n_seqs
+        for name, t in (("lp", lp), ("entropy", entropy), ("lse", lse)):
+            if t.dtype != torch.float32 or t.device != dev or t.shape != (T,) or \
+                    not t.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous float32 [{T}] tensor on {dev}")
+        f32 = dict(dtype=torch.float32, device=dev)
+        out = LossOutput(stats=torch.empty(N.NSTAT, dtype=torch.float64, device=dev), lp=lp,
+                         entropy=entropy, lse=lse, seq_lp=torch.empty(B, **f32),
+                         seq_adv=torch.empty(B, **f32))
+        co = N.TgOut()
+        co.lp, co.entropy, co.lse = lp.data_ptr(), entropy.data_ptr(), lse.data_ptr()
+        co.seq_lp, co.seq_adv, co.stats = (out.seq_lp.data_ptr(), out.seq_adv.data_ptr(),
+                                           out.stats.data_ptr())
+        nbytes = L.tg_workspace_size(ctypes.byref(cb), ctypes.byref(cc))
+        ws = self._ws.get(dev, nbytes)
+        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        with torch.cuda.device(dev):
+            N.check(L.tg_loss_fwd_bwd(ctypes.byref(cb), ctypes.byref(cc), ctypes.byref(co),
+                                      ws.data_ptr(), ws.numel(), s.cuda_stream))
+        out.dlogits = None
+        return out
+
 
 def logprob_fwd(batch: PackedBatch, stream: Optional[torch.cuda.Stream] = None):
     """Forward-only per-row logprob / entropy / lse and per-sequence LP
@@ -263,3 +301,22 @@ def lmhead_logprob_fwd(hidden: torch.Tensor, weight: torch.Tensor,
             tgt.data_ptr() if tgt is not None else None, lp.data_ptr() if lp is not None else None,
             ent.data_ptr(), lse.data_ptr(), ws.data_ptr(), ws.numel(), s.cuda_stream))
     return lp, ent, lse
+
+
+def lmhead_loss_fwd(hidden: torch.Tensor, weight: torch.Tensor, loss: "RFTLoss", target,
+                    seq_lengths, group_sizes, reward, **pack_kw) -> LossOutput:
+    """RFT loss and metrics straight from hidden states: the fused LM-head
+    kernel gives per-row lp / entropy / lse (no [T, V] logits anywhere), then
+    the loss epilogue runs on those rows (``RFTLoss.from_rows``).  ``pack_kw``
+    takes pack_arrays' side inputs (old_lp, ref_lp, seq_ref_lp, seq_kind, ...)
+    and the global denominators (n_tok_global, ...)."""
+    from .packing import pack_arrays
+    glob = {k: pack_kw.pop(k) for k in ("n_tok_global", "n_seq_global", "n_sft_seq_global")
+            if k in pack_kw}
+    V = int(weight.shape[0])
+    tgt = torch.as_tensor(target, device=hidden.device).to(torch.int32)
+    lp, ent, lse = lmhead_logprob_fwd(hidden, weight, tgt)
+    rows = torch.empty((0, V), dtype=torch.bfloat16, device=hidden.device)
+    batch = pack_arrays(rows, tgt.cpu().numpy(), seq_lengths, group_sizes, reward,
+                        vocab=V, **pack_kw)
+    return loss.from_rows(batch, lp, ent, lse, **glob)

@@ -6,6 +6,7 @@ Tolerances: the tensor cores multiply bf16 exactly and accumulate in fp32, so
 the only difference from the fp32 reference is summation order over d terms:
 lse / lp within 2e-4 abs + 1e-5 rel, entropy within 2e-4 abs."""
 
+import numpy as np
 import pytest
 import torch
 
@@ -83,3 +84,39 @@ def test_lmhead_argument_errors():
         lmhead_logprob_fwd(h, w[:, :32].contiguous(), y)
     with pytest.raises(TypeError):
         lmhead_logprob_fwd(h.float(), w, y)
+
+
+@pytest.mark.parametrize("cfg_kw", [
+    dict(advantage_fn="grpo", policy_loss_fn="ppo_clip", kl_fn="low_var_kl", kl_coef=0.001,
+         entropy_loss_fn="default", entropy_coef=0.001, loss_agg_mode="token-mean"),
+    dict(policy_loss_fn="opmd_kimi", tau=0.7),
+    dict(advantage_fn="grpo", policy_loss_fn="ppo_clip", loss_agg_mode="token-mean",
+         sft_weight=1.0),
+], ids=["grpo_ppo_k3_ent", "kimi", "mixed_sft"])
+def test_loss_from_hidden_states_matches_logits_path(cfg_kw):
+    """RFT loss straight from hidden states (LM-head kernel + loss epilogue on
+    the rows, TG_FLAG_ROWS_GIVEN) equals the loss computed from fp32 logits."""
+    from paper_2505_17826_b200 import RFTLoss, RFTLossConfig, lmhead_loss_fwd, pack_arrays
+    T_seq, B, d, V = 64, 8, 256, 32000
+    T = T_seq * B
+    h, w, y = make(T, V, d, seed=5)
+    rng = np.random.default_rng(5)
+    reward = rng.integers(0, 2, B).astype(np.float32)
+    old = (rng.normal(-8.0, 0.5, T)).astype(np.float32)
+    ref = (rng.normal(-8.0, 0.5, T)).astype(np.float32)
+    seq_ref = rng.normal(-500.0, 10.0, B).astype(np.float32)
+    kind = np.array([0, 0, 0, 0, 1, 1, 1, 1], np.uint8) if cfg_kw.get("sft_weight") else None
+    side = dict(old_lp=old, ref_lp=ref, seq_ref_lp=seq_ref, seq_kind=kind)
+    cfg = RFTLossConfig(**cfg_kw)
+    loss = RFTLoss(cfg)
+    got = lmhead_loss_fwd(h, w, loss, y.cpu().numpy(), [T_seq] * B, [4, 4], reward, **side)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    z = (h.float() @ w.float().T).contiguous()
+    want = loss(pack_arrays(z, y.cpu().numpy(), [T_seq] * B, [4, 4], reward, **side),
+                dlogits=None)
+    a, b = got.stats_dict(), want.stats_dict()
+    for k in ("loss", "pg_loss", "kl_loss", "entropy_loss", "sft_loss", "sum_lp",
+              "sum_entropy", "clip_count", "n_tok"):
+        assert a[k] == pytest.approx(b[k], rel=1e-4, abs=1e-5), k
+    torch.testing.assert_close(got.seq_lp, want.seq_lp, atol=2e-3, rtol=1e-5)
+    assert got.dlogits is None

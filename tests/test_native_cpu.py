@@ -174,3 +174,22 @@ def test_lmhead_and_update_argument_validation():
     assert upd(ld_grad=50) == N.TG_EINVAL
     assert upd(dtype=7) == N.TG_EINVAL
     assert upd(n_touched=70000) == N.TG_EINVAL
+
+
+def test_rows_given_flag_validation():
+    """TG_FLAG_ROWS_GIVEN (loss from precomputed rows) is forward-only and
+    needs lp / entropy / lse as inputs; rejected before any device work."""
+    L = N.lib()
+    b = N.TgBatch()
+    b.dtype, b.n_rows, b.vocab, b.ld, b.n_seqs, b.n_groups = N.TG_DTYPE_BF16, 4, 100, 100, 1, 1
+    cfg = N.TgConfig()
+    cfg.flags = N.TG_FLAG_ROWS_GIVEN
+    cfg.dpo_beta = 0.1
+    o = N.TgOut()
+    o.stats = 16
+    rc = L.tg_loss_fwd_bwd(ctypes.byref(b), ctypes.byref(cfg), ctypes.byref(o), None, 0, None)
+    assert rc == N.TG_EINVAL and b"out.lp" in L.tg_last_error()
+    o.lp = o.entropy = o.lse = 16
+    o.dlogits, o.ld_out = 16, 100
+    rc = L.tg_loss_fwd_bwd(ctypes.byref(b), ctypes.byref(cfg), ctypes.byref(o), None, 0, None)
+    assert rc == N.TG_EINVAL and b"forward-only" in L.tg_last_error()
