@@ -15,6 +15,7 @@ import ctypes
 from dataclasses import dataclass
 from typing import Dict, Optional, Union
 
+import numpy as np
 import torch
 
 from . import _native as N
@@ -314,9 +315,10 @@ def lmhead_loss_fwd(hidden: torch.Tensor, weight: torch.Tensor, loss: "RFTLoss",
     glob = {k: pack_kw.pop(k) for k in ("n_tok_global", "n_seq_global", "n_sft_seq_global")
             if k in pack_kw}
     V = int(weight.shape[0])
-    tgt = torch.as_tensor(target, device=hidden.device).to(torch.int32)
-    lp, ent, lse = lmhead_logprob_fwd(hidden, weight, tgt)
+    # the packer validates targets on the host: pass a host array (a device
+    # tensor costs one synchronising copy here)
+    tgt_host = target.cpu().numpy() if torch.is_tensor(target) else np.asarray(target)
     rows = torch.empty((0, V), dtype=torch.bfloat16, device=hidden.device)
-    batch = pack_arrays(rows, tgt.cpu().numpy(), seq_lengths, group_sizes, reward,
-                        vocab=V, **pack_kw)
+    batch = pack_arrays(rows, tgt_host, seq_lengths, group_sizes, reward, vocab=V, **pack_kw)
+    lp, ent, lse = lmhead_logprob_fwd(hidden, weight, batch.target)
     return loss.from_rows(batch, lp, ent, lse, **glob)

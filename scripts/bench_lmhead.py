@@ -51,6 +51,21 @@ def main():
         torch.matmul(h, w.T, out=logits)
         logprob_fwd(batch)
     ms_unfused = timed(unfused)
+    # the RFT loss forward from hidden states vs GEMM + the loss from logits
+    from paper_2505_17826_b200 import RFTLoss, RFTLossConfig, lmhead_loss_fwd
+    rl = RFTLoss(RFTLossConfig(advantage_fn="grpo", policy_loss_fn="ppo_clip", kl_fn="low_var_kl",
+                               kl_coef=0.001, loss_agg_mode="token-mean"))
+    n_seq = max(1, T // 2048)
+    lens, groups = [T // n_seq] * n_seq, [n_seq]
+    rew = np.random.default_rng(0).integers(0, 2, n_seq).astype(np.float32)
+    tgt_h = y.cpu().numpy()
+    ms_loss_fused = timed(lambda: lmhead_loss_fwd(h, w, rl, tgt_h, lens, groups, rew), reps=5)
+    lbatch = pack_arrays(logits, tgt_h, lens, groups, rew)
+
+    def loss_unfused():
+        torch.matmul(h, w.T, out=logits)
+        rl(lbatch, dlogits=None)
+    ms_loss_unfused = timed(loss_unfused, reps=5)
     lp_f, _, lse_f = lmhead_logprob_fwd(h, w, y)
     lp_u, _, lse_u, _ = logprob_fwd(batch)
     dlse = float((lse_f - lse_u).abs().max())
@@ -68,7 +83,9 @@ def main():
            "cublas_gemm_only_ms": ms_cublas, "cublas_tflops": flops / ms_cublas / 1e9,
            "tokens_per_s": T / ms * 1e3, "unfused_cublas_plus_logprob_ms": ms_unfused,
            "speedup_vs_unfused": ms_unfused / ms,
-           "max_abs_lse_diff_vs_unfused_bf16_logits": dlse}
+           "max_abs_lse_diff_vs_unfused_bf16_logits": dlse,
+           "loss_fwd_from_hidden_ms": ms_loss_fused,
+           "loss_fwd_unfused_gemm_plus_loss_ms": ms_loss_unfused}
     print(json.dumps(out))
 
 
