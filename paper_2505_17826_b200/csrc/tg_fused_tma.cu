@@ -101,6 +101,7 @@ struct FusedSmemTail {
 // prof[10] first -> last local warp partial posted (intra-CTA skew)
 // prof[11..14] post lag behind the first local post, summed over the consumer
 //              warps of SM sub-partition 0..3 (warp % 4)
+// prof[15] phase-1 chunks that took the checked path (counted per warp)
 #ifdef TG_FUSED_PROF
 __device__ unsigned long long g_fused_prof[1024][16];
 __device__ __forceinline__ FusedSmemTail* prof_tail() {
@@ -258,12 +259,11 @@ struct Acc1 {
   bool fresh;  // no chunk of the current row accumulated yet (warp-uniform)
 };
 
-// kWM (short rows, CL = 1): the reference max m is warp-uniform -- the checked
-// path takes the warp's maximum (one REDUX on an order-preserving integer
-// image of the floats) -- so a warp's per-row partial is (m, sum s, sum t), plain
-// butterfly sums instead of a 5-level online merge.  Measured: +6 % at
-// V = 32,000 (2-chunk rows), -1.5 % at V = 151,936 (5-chunk slices), where
-// per-lane maxima stay.
+// kWM: the reference max m is warp-uniform -- the checked path takes the warp's
+// maximum (one REDUX on an order-preserving integer image of the floats) -- so a
+// warp's per-row partial is (m, sum s, sum t), plain butterfly sums instead of a
+// 5-level online merge.  Measured: +6 % at V = 32,000 (2-chunk rows), +0.4 % at
+// V = 151,936 (3 % fewer cycles per row in the instrumented build).
 __device__ __forceinline__ float warp_max_f(float v) {
   const int i = __float_as_int(v);
   const int key = __reduce_max_sync(0xffffffffu, i >= 0 ? i : i ^ 0x7fffffff);
@@ -386,6 +386,9 @@ __device__ __forceinline__ void phase1_chunk(Acc1& acc, RingIt& it, const RingBa
       return;
     }
   }
+#ifdef TG_FUSED_PROF
+  if ((tid & 31) == 0) atomicAdd(&prof_tail()->prof[15], 1ull);  // checked-path chunks (warps)
+#endif
   phase1_checked<T, kPartial, kMaskTail, kWM>(acc, u, valid, vbase, sl, tid);
 }
 
@@ -762,7 +765,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     // ===================== consumer warps =====================
     RingIt pos0 = {0u};  // the current row's first chunk
     Acc1 acc = acc_init();
-    constexpr bool kWM = CL == 1;  // short rows: warp-uniform reference max
+#ifndef TG_WM_ALL
+#define TG_WM_ALL 1
+#endif
+    constexpr bool kWM = CL == 1 || TG_WM_ALL;  // warp-uniform reference max
     // Virtual thread index for the chunk layout: the warps of SM sub-partitions
     // 2 and 3 come first, so a partial last chunk's valid vectors go to them --
     // sub-partitions 0 and 1 also host the epilogue and producer warps.  (Any

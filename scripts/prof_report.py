@@ -24,5 +24,6 @@ for f in sys.argv[1:]:
     print(f"  per row: span {(span / rows).mean():.0f} cyc, epilogue critical path "
           f"{(a[:, 7] / rows).mean():.0f} cyc; first local partial -> epilogue wake "
           f"{(a[:, 9] / rows).mean():.0f} cyc, intra-CTA post skew {(a[:, 10] / rows).mean():.0f} cyc")
+    print(f"  checked-path phase-1 chunks per row per warp: {(a[:, 15] / rows / NCW).mean():.3f}")
     lag = [(a[:, 11 + q] / rows / (NCW / 4)).mean() for q in range(4)]
     print("  mean post lag by SM sub-partition (warp % 4): " + ", ".join(f"{x:.0f}" for x in lag))
