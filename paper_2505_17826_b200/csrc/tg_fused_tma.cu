@@ -241,12 +241,12 @@ __device__ __forceinline__ int seq_of_row(const KParams& P, int64_t row) {
 }
 
 // ---- phase 1: one chunk (kVecPerThread vectors per consumer thread) ---------
-// kPartial: the chunk may run past the slice end (lanes there use a neutral
-// -1e30 vector and skip the sums, but still vote, so the rescale test is
-// always a full-warp vote).  kMaskTail: the chunk holds the tail padding.
+// kPartial: the chunk may run past the slice end (lanes there load a neutral
+// -1e30 vector, which adds exactly 0 to the sums, so every lane takes part in
+// the warp vote).  kMaskTail: the chunk holds the tail padding.
 //
-// Speculative fast path (full chunks): the sums are taken straight away with
-// the lane's current reference max m -- no -inf clamp, no vector max, no
+// Speculative fast path: the sums are taken straight away with the current
+// reference max m (warp-uniform under kWM) -- no -inf clamp, no vector max, no
 // pre-vote -- and accepted when they are safe: finite, s <= 2^32 (no term near
 // overflow) and, for the first chunk of a row (m carried over from the
 // previous row), s >= 2^-20 (no significant term lost to underflow).  Otherwise
