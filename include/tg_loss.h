@@ -54,7 +54,7 @@
 extern "C" {
 #endif
 
-#define TG_ABI_VERSION 1
+#define TG_ABI_VERSION 2
 
 /* return codes */
 enum { TG_OK = 0, TG_EINVAL = 1, TG_ECUDA = 2, TG_EUNSUPPORTED = 3, TG_EWORKSPACE = 4 };
@@ -176,6 +176,11 @@ typedef struct TgOut {
   float* seq_lp;     /* optional [B] sum of lp over each sequence               */
   float* seq_adv;    /* optional [B] advantage (or coupled coefficient)         */
   double* stats;     /* [TG_NSTAT] device, required                             */
+  float* row_coef;   /* optional [3, T] per-row gradient coefficients (a, hz, s):
+                        d loss / d z_tv = p_tv (a_t + hz_t z_tv) - s_t [v = y_t],
+                        p = exp(z - lse).  Requesting them selects the two-pass
+                        route (the fused kernel keeps them on chip); with
+                        TG_FLAG_ROWS_GIVEN they feed tg_lmhead_dlogits.        */
 } TgOut;
 
 /* Workspace bytes needed by tg_loss_fwd_bwd / tg_logprob_fwd for this batch. */
@@ -206,6 +211,22 @@ int tg_lmhead_logprob_fwd(const void* hidden, int64_t ld_hidden, const void* wei
                           int64_t ld_weight, int64_t n_rows, int64_t vocab, int64_t dim,
                           const int32_t* target, float* lp, float* entropy, float* lse,
                           void* workspace, size_t workspace_bytes, void* stream);
+
+/* Backward half of the fused LM head (vocabulary chunked):
+   recomputes z = hidden x weight[col0 : col0 + n_cols]^T on the tensor cores
+   and writes, for every row t and chunk column j (v = col0 + j),
+       dz[t, j] = exp(z_tv - lse_t) * (a_t + hz_t * z_tv) - s_t * [v == target_t]
+   in bf16 to dz [n_rows, ld_dz] (ld_dz >= n_cols, a multiple of 8) -- the
+   d loss / d logits of one vocabulary chunk, from the row coefficients
+   TgOut.row_coef (a = row_coef[0:T], hz = [T:2T], s = [2T:3T]) and lse of the
+   forward.  The caller turns each chunk into d hidden += dz . W_chunk and
+   d W_chunk = dz^T . hidden (plain GEMMs), so the [T, V] logits never exist:
+   peak memory is T x n_cols.  Replaces policy.grad_logprob (policy.py:253-270)
+   behind an LM head.  Same size rules as tg_lmhead_logprob_fwd. */
+int tg_lmhead_dlogits(const void* hidden, int64_t ld_hidden, const void* weight,
+                      int64_t ld_weight, int64_t n_rows, int64_t vocab, int64_t dim,
+                      int64_t col0, int64_t n_cols, const int32_t* target, const float* lse,
+                      const float* row_coef, void* dz, int64_t ld_dz, void* stream);
 
 /* Optimizer step: algorithms.apply_update (algorithms.py:329-348) on the
    device.  table [n_states, ld_table] fp32 (updated in place) gets

@@ -66,6 +66,7 @@ class TgOut(ctypes.Structure):
     _fields_ = [
         ("dlogits", c_void_p), ("ld_out", c_int64), ("lp", c_void_p), ("entropy", c_void_p),
         ("lse", c_void_p), ("seq_lp", c_void_p), ("seq_adv", c_void_p), ("stats", c_void_p),
+        ("row_coef", c_void_p),
     ]
 
 
@@ -73,8 +74,10 @@ EXPORTED = [
     "tg_workspace_size", "tg_loss_fwd_bwd", "tg_logprob_fwd", "tg_route", "tg_strerror",
     "tg_last_error", "tg_abi_version", "tg_scored_states", "tg_group_by_task",
     "tg_set_timing_events", "tg_launch_count", "tg_pack_rows", "tg_lmhead_logprob_fwd",
-    "tg_lmhead_workspace_size", "tg_apply_update",
+    "tg_lmhead_workspace_size", "tg_apply_update", "tg_lmhead_dlogits",
 ]
+
+ABI_VERSION = 2  # include/tg_loss.h TG_ABI_VERSION
 
 _lib = None
 
@@ -140,7 +143,11 @@ def lib() -> ctypes.CDLL:
                                   c_void_p, c_void_p]
     L.tg_lmhead_workspace_size.restype = c_size_t
     L.tg_lmhead_workspace_size.argtypes = [c_int64, c_int64]
-    if L.tg_abi_version() != 1:
+    L.tg_lmhead_dlogits.restype = c_int
+    L.tg_lmhead_dlogits.argtypes = [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64,
+                                    c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
+                                    c_void_p, c_int64, c_void_p]
+    if L.tg_abi_version() != ABI_VERSION:
         raise RuntimeError("libtg_loss ABI mismatch")
     _lib = L
     return L

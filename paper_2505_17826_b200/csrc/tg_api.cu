@@ -37,6 +37,11 @@ cudaError_t launch_lmhead_logprob(const void* hidden, int64_t ld_hidden, const v
                                   void* workspace, size_t workspace_bytes, int n_sms,
                                   cudaStream_t stream);
 size_t lm_workspace_bytes(int64_t n_rows, int64_t vocab, int n_sms);
+cudaError_t launch_lmhead_dz(const void* hidden, int64_t ld_hidden, const void* weight,
+                             int64_t ld_weight, int64_t n_rows, int64_t vocab, int64_t dim,
+                             int64_t col0, int64_t n_cols, const int32_t* target,
+                             const float* lse, const float* coef, void* dz, int64_t ld_dz,
+                             int n_sms, cudaStream_t stream);
 cudaError_t launch_update(float* table, int64_t ld_table, int64_t n_states, int64_t vocab,
                           const void* grad, int dtype, int64_t ld_grad, const int64_t* state_ids,
                           const int64_t* state_offsets, const int64_t* row_order,
@@ -247,9 +252,15 @@ void fill_params(KParams& P, const TgBatch* b, const TgConfig* c, const TgOut* o
   P.sLP = reinterpret_cast<double*>(ws + L.sLP);
   P.sRef = reinterpret_cast<double*>(ws + L.sRef);
   P.gF = reinterpret_cast<double*>(ws + L.gF);
-  P.rS = reinterpret_cast<float*>(ws + L.rS);
-  P.rA = reinterpret_cast<float*>(ws + L.rA);
-  P.rHz = reinterpret_cast<float*>(ws + L.rHz);
+  if (o && o->row_coef) {  // caller-visible row coefficients [3, T]: a, hz, s
+    P.rA = o->row_coef;
+    P.rHz = o->row_coef + b->n_rows;
+    P.rS = o->row_coef + 2 * b->n_rows;
+  } else {
+    P.rS = reinterpret_cast<float*>(ws + L.rS);
+    P.rA = reinterpret_cast<float*>(ws + L.rA);
+    P.rHz = reinterpret_cast<float*>(ws + L.rHz);
+  }
   P.rCa = reinterpret_cast<float*>(ws + L.rCa);
   P.rLseQ = reinterpret_cast<float*>(ws + L.rLseQ);
   P.rAkl = reinterpret_cast<float*>(ws + L.rAkl);
@@ -351,6 +362,7 @@ int route_of(const TgBatch* b, const TgConfig* c, const TgOut* o) {
   if (coupled_pg(c->policy_loss_fn)) return 3;
   if (c->flags & TG_FLAG_ROWS_GIVEN) return 2;
   if (c->anchor_beta > 0) return 2;
+  if (o && o->row_coef) return 2;  // the fused kernel keeps the coefficients on chip
   if (c->flags & (TG_FLAG_FORCE_TWO_PASS | TG_FLAG_NO_FUSED_TMA)) return 2;
   if (!o || !o->dlogits) return 2;
   if (fused_plan(b, o).cl == 0) return 2;
@@ -411,6 +423,8 @@ int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspa
   rc = validate_cfg(b, c);
   if (rc) return rc;
   if (!o || !o->stats) return fail(TG_EINVAL, "out.stats is required");
+  if (o->row_coef && c->anchor_beta > 0)
+    return fail(TG_EINVAL, "out.row_coef cannot describe the anchor-KL gradient (anchor_beta > 0)");
   if (o->dlogits) {
     if (o->ld_out < b->vocab) return fail(TG_EINVAL, "ld_out < vocab");
     if (o->dlogits == b->logits && (b->row_index || o->ld_out != b->ld))
@@ -523,10 +537,9 @@ int tg_logprob_fwd(const TgBatch* b, TgOut* o, void* workspace, size_t workspace
   return check_cuda("tg_logprob_fwd");
 }
 
-int tg_lmhead_logprob_fwd(const void* hidden, int64_t ld_hidden, const void* weight,
-                          int64_t ld_weight, int64_t n_rows, int64_t vocab, int64_t dim,
-                          const int32_t* target, float* lp, float* entropy, float* lse,
-                          void* workspace, size_t workspace_bytes, void* stream) {
+// size / pitch / alignment rules shared by the LM-head entry points
+static int lmhead_check(const void* hidden, int64_t ld_hidden, const void* weight,
+                        int64_t ld_weight, int64_t n_rows, int64_t vocab, int64_t dim) {
   if (n_rows < 0 || vocab < 1 || dim < 1)
     return fail(TG_EINVAL, "bad sizes (rows %lld, vocab %lld, dim %lld)", (long long)n_rows,
                 (long long)vocab, (long long)dim);
@@ -538,11 +551,20 @@ int tg_lmhead_logprob_fwd(const void* hidden, int64_t ld_hidden, const void* wei
     return fail(TG_EINVAL, "row pitches must be multiples of 8 elements (16 bytes)");
   if (vocab > (int64_t(1) << 31) - 256 || n_rows > (int64_t(1) << 31) - 128)
     return fail(TG_EINVAL, "vocab / rows too large");
-  if (n_rows == 0) return TG_OK;
-  if (!hidden || !weight || !lse || !entropy)
-    return fail(TG_EINVAL, "hidden, weight, entropy and lse are required");
-  if (!aligned16(hidden) || !aligned16(weight))
+  if (n_rows > 0 && (!hidden || !weight)) return fail(TG_EINVAL, "hidden and weight are required");
+  if (n_rows > 0 && (!aligned16(hidden) || !aligned16(weight)))
     return fail(TG_EINVAL, "hidden and weight must be 16-byte aligned");
+  return TG_OK;
+}
+
+int tg_lmhead_logprob_fwd(const void* hidden, int64_t ld_hidden, const void* weight,
+                          int64_t ld_weight, int64_t n_rows, int64_t vocab, int64_t dim,
+                          const int32_t* target, float* lp, float* entropy, float* lse,
+                          void* workspace, size_t workspace_bytes, void* stream) {
+  const int rc = lmhead_check(hidden, ld_hidden, weight, ld_weight, n_rows, vocab, dim);
+  if (rc) return rc;
+  if (n_rows == 0) return TG_OK;
+  if (!lse || !entropy) return fail(TG_EINVAL, "entropy and lse are required");
   if (lp && !target) return fail(TG_EINVAL, "lp requires target");
   const DevInfo d = dev_info();
   const int sms = d.sms > 0 ? d.sms : 148;
@@ -559,6 +581,35 @@ int tg_lmhead_logprob_fwd(const void* hidden, int64_t ld_hidden, const void* wei
     return fail(TG_EUNSUPPORTED, "cuTensorMapEncodeTiled is unavailable (driver too old)");
   count_launches(lm_split(n_rows, vocab, sms) > 1 ? 2 : 1);
   if (e != cudaSuccess) return fail(TG_ECUDA, "tg_lmhead_logprob_fwd: %s", cudaGetErrorString(e));
+  return TG_OK;
+}
+
+int tg_lmhead_dlogits(const void* hidden, int64_t ld_hidden, const void* weight,
+                      int64_t ld_weight, int64_t n_rows, int64_t vocab, int64_t dim,
+                      int64_t col0, int64_t n_cols, const int32_t* target, const float* lse,
+                      const float* row_coef, void* dz, int64_t ld_dz, void* stream) {
+  const int rc = lmhead_check(hidden, ld_hidden, weight, ld_weight, n_rows, vocab, dim);
+  if (rc) return rc;
+  if (col0 < 0 || n_cols < 1 || col0 + n_cols > vocab)
+    return fail(TG_EINVAL, "vocabulary chunk [%lld, %lld) outside [0, %lld)", (long long)col0,
+                (long long)(col0 + n_cols), (long long)vocab);
+  if (ld_dz < n_cols || ld_dz % 8 != 0)
+    return fail(TG_EINVAL, "ld_dz must be >= n_cols and a multiple of 8, got %lld",
+                (long long)ld_dz);
+  if (n_rows == 0) return TG_OK;
+  if (!target || !lse || !row_coef || !dz)
+    return fail(TG_EINVAL, "target, lse, row_coef and dz are required");
+  if (!aligned16(dz)) return fail(TG_EINVAL, "dz must be 16-byte aligned");
+  const DevInfo d = dev_info();
+  const int sms = d.sms > 0 ? d.sms : 148;
+  cudaGetLastError();
+  cudaError_t e = launch_lmhead_dz(hidden, ld_hidden, weight, ld_weight, n_rows, vocab, dim, col0,
+                                   n_cols, target, lse, row_coef, dz, ld_dz, sms,
+                                   reinterpret_cast<cudaStream_t>(stream));
+  if (e == cudaErrorNotSupported)
+    return fail(TG_EUNSUPPORTED, "cuTensorMapEncodeTiled is unavailable (driver too old)");
+  count_launches(1);
+  if (e != cudaSuccess) return fail(TG_ECUDA, "tg_lmhead_dlogits: %s", cudaGetErrorString(e));
   return TG_OK;
 }
 

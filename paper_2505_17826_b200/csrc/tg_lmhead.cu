@@ -46,12 +46,18 @@ constexpr uint32_t LM_TMEM_COLS = 512;           // 2 accumulators x 256 fp32 co
 
 struct LmParams {
   int64_t n_rows, vocab, dim;
+  int64_t col0, n_cols;   // vocabulary columns [col0, col0 + n_cols) covered by the tiles
   int n_split;            // vocabulary splits per row block (> 1: partials + merge kernel)
   float4* partial;        // [n_split, T] (m, sum e, sum e z, z_target) when n_split > 1
   const int32_t* target;  // [T] (may be null: lp not produced)
   float* lp;              // [T]
   float* ent;             // [T]
   float* lse;             // [T]
+  // backward (kDz): dz[t, j] = p (a + hz z) - s [col0 + j == y] for the chunk
+  const float* coef;      // [3, T]: a, hz, s
+  const float* lse_in;    // [T]
+  uint16_t* dz;           // bf16 [T, ld_dz]
+  int64_t ld_dz;
 };
 
 constexpr int LM_MAX_STAGES = 6;
@@ -70,9 +76,14 @@ template <bool kPair>
 constexpr int lm_stages() { return kPair ? 6 : LM_STAGES; }
 template <bool kPair>
 constexpr int lm_stage_bytes() { return LM_A_BYTES + (kPair ? LM_BN / 2 : LM_BN) * LM_BK * 2; }
+// backward epilogue staging: per epilogue warp two [32 rows x 32 bf16] tiles
+// (64-byte rows, 64-byte swizzle) that a TMA bulk-tensor store writes out
+constexpr int LM_DZ_TILE_BYTES = 32 * 64;
+constexpr int LM_DZ_STAGE_BYTES = 4 * 2 * LM_DZ_TILE_BYTES;  // 16 KB
 template <bool kPair>
 size_t lm_smem_bytes() {
-  return size_t(lm_stages<kPair>()) * lm_stage_bytes<kPair>() + sizeof(LmSmemTail) + 1024;
+  return size_t(lm_stages<kPair>()) * lm_stage_bytes<kPair>() + LM_DZ_STAGE_BYTES +
+         sizeof(LmSmemTail) + 1024;
 }
 
 // ---- PTX wrappers -------------------------------------------------------------
@@ -163,6 +174,30 @@ __device__ __forceinline__ void lm_tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// TMA bulk-tensor store of a shared-memory tile (bulk-group completion)
+__device__ __forceinline__ void lm_tma_store_2d(const CUtensorMap* map, uint32_t src, int c0,
+                                                int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(src)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
+                                             uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
+}
+// wait until at most N committed stores still read shared memory
+template <int N>
+__device__ __forceinline__ void lm_store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // ---- cluster-pair helpers (kPair: cta_group::2, M = 256 across two SMs) ----------
 
 __device__ __forceinline__ uint32_t lm_peer0(uint32_t smem_addr) {  // same offset in CTA rank 0
@@ -217,10 +252,13 @@ constexpr uint32_t lm_idesc_t() {
 //   tcgen05.mma.cta_group::2 (M 256, N 256) reading both CTAs' shared memory, and
 //   each CTA's TMEM receives its 128 rows: per SM the W-tile traffic halves.
 
-template <bool kPair>
+// kDz = false: the forward (per-row lse / entropy / lp).  kDz = true: the
+// backward of one vocabulary chunk -- the epilogue turns each logit tile into
+// bf16 d loss / d z from the forward's lse and the loss's row coefficients.
+template <bool kPair, bool kDz>
 __global__ void __launch_bounds__(LM_THREADS, 1)
     k_lmhead_logprob(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
-                     const LmParams P) {
+                     const __grid_constant__ CUtensorMap tmD, const LmParams P) {
   constexpr int B_ROWS = kPair ? LM_BN / 2 : LM_BN;      // W rows staged per CTA
   constexpr int STAGE = lm_stage_bytes<kPair>();
   constexpr int NST = lm_stages<kPair>();
@@ -229,7 +267,8 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
   // 1 KB alignment for the 128-byte swizzle atoms
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(lm_smem_raw) + 1023) & ~uintptr_t(1023));
-  LmSmemTail* tail = reinterpret_cast<LmSmemTail*>(smem + size_t(NST) * STAGE);
+  LmSmemTail* tail =
+      reinterpret_cast<LmSmemTail*>(smem + size_t(NST) * STAGE + LM_DZ_STAGE_BYTES);
   const uint32_t ring = smem_u32(smem);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -240,7 +279,7 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
   const int64_t T = P.n_rows;
   const int V = int(P.vocab);
   const int n_mb = int((T + ROWS_PER_UNIT - 1) / ROWS_PER_UNIT);
-  const int n_nt = (V + LM_BN - 1) / LM_BN;
+  const int n_nt = int((P.n_cols + LM_BN - 1) / LM_BN);
   // work unit u = (row block u / n_split, vocabulary split u % n_split)
   const int n_split = P.n_split;
   const int n_units = n_mb * n_split;
@@ -297,7 +336,7 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
         unit_tiles(u, mb, nt0, nt1);
         const int xrow = mb * ROWS_PER_UNIT + int(rank) * LM_BM;
         for (int nt = nt0; nt < nt1; ++nt) {
-          const int wrow = nt * LM_BN + int(rank) * B_ROWS;
+          const int wrow = int(P.col0) + nt * LM_BN + int(rank) * B_ROWS;
           for (int kb = 0; kb < n_kb; ++kb) {
             lm_wait(smem_u32(&tail->empty[stage]), phase ^ 1u);
             const uint32_t fb = smem_u32(&tail->full[stage]);
@@ -375,6 +414,84 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
     const uint32_t lane_base = uint32_t(32 * q) << 16;
     const uint64_t l2e2 = pk2(kLog2e, kLog2e);
     uint32_t tile = 0;
+    if constexpr (kDz) {
+      const uint32_t stage_dz = ring + uint32_t(NST * STAGE) + uint32_t(q) * 2u * LM_DZ_TILE_BYTES;
+      int sbuf = 0;
+      if (lane == 0)
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmD)) : "memory");
+      for (int u = unit0; u < n_units; u += unit_stride) {
+        int mb, nt0, nt1;
+        unit_tiles(u, mb, nt0, nt1);
+        const int64_t row = int64_t(mb) * ROWS_PER_UNIT + int64_t(rank) * LM_BM + 32 * q + lane;
+        const bool live = row < T;
+        const int64_t row0 = row - lane;  // first row of the warp's 32-row slab
+        // chunk-relative target column (outside [0, n_cols): no one-hot term here)
+        const int64_t yr = live ? int64_t(P.target[row]) - P.col0 : -1;
+        const float nl = live ? -P.lse_in[row] * kLog2e : 0.f;
+        const float a = live ? P.coef[row] : 0.f, hz = live ? P.coef[T + row] : 0.f;
+        const float sy = live ? P.coef[2 * T + row] : 0.f;
+        const uint64_t nl2 = pk2(nl, nl), a2 = pk2(a, a), hz2 = pk2(hz, hz);
+        for (int nt = nt0; nt < nt1; ++nt, ++tile) {
+          const uint32_t acc = tile & 1u, acc_phase = (tile >> 1) & 1u;
+          lm_wait_sleep(smem_u32(&tail->tfull[acc]), acc_phase);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < LM_BN; c += 32) {
+            float v[32];
+            __syncwarp();
+            lm_tmem_ld32(tmem + lane_base + acc * LM_BN + uint32_t(c), v);
+            const int64_t j0 = int64_t(nt) * LM_BN + c;
+            if (j0 >= P.n_cols) continue;  // warp-uniform: the whole tile is past the chunk
+            float d[32];
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              const uint64_t x = pk2(v[i], v[i + 1]);
+              const uint64_t p = ex2x2(fma2(x, l2e2, nl2));
+              upk2(mul2(p, fma2(hz2, x, a2)), d[i], d[i + 1]);
+            }
+            if (yr >= j0 && yr < j0 + 32) {
+              const int yo = int(yr - j0);
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                asm("{\n\t.reg .pred p;\n\tsetp.eq.s32 p, %1, %2;\n\t@p sub.f32 %0, %0, %3;\n\t}"
+                    : "+f"(d[i])
+                    : "r"(yo), "r"(i), "f"(sy));
+            }
+            // stage the warp's [32 rows x 32 columns] bf16 tile (64-byte swizzle:
+            // 16-byte granule g of row r at g ^ ((r >> 1) & 3), conflict-free) and
+            // let one lane TMA-store it; rows >= T / columns >= n_cols are clipped
+            const uint32_t buf = stage_dz + uint32_t(sbuf) * LM_DZ_TILE_BYTES;
+            if (lane == 0) lm_store_wait_read<1>();  // this buffer's previous store has read it
+            __syncwarp();
+            if (live) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const uint32_t g = uint32_t(k) ^ ((uint32_t(lane) >> 1) & 3u);
+                st_shared_v4(buf + uint32_t(lane) * 64u + g * 16u,
+                             Vec<bf16_t>::pack2(d[8 * k], d[8 * k + 1]),
+                             Vec<bf16_t>::pack2(d[8 * k + 2], d[8 * k + 3]),
+                             Vec<bf16_t>::pack2(d[8 * k + 4], d[8 * k + 5]),
+                             Vec<bf16_t>::pack2(d[8 * k + 6], d[8 * k + 7]));
+              }
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) lm_tma_store_2d(&tmD, buf, int(j0), int(row0));
+            sbuf ^= 1;
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (kPair)
+              lm_arrive_cluster(lm_peer0(smem_u32(&tail->tempty[acc])));
+            else
+              mbar_arrive(&tail->tempty[acc]);
+          }
+        }
+      }
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      __syncwarp();
+    } else
     for (int u = unit0; u < n_units; u += unit_stride) {
       int mb, nt0, nt1;
       unit_tiles(u, mb, nt0, nt1);
@@ -504,22 +621,25 @@ __global__ void k_lmhead_merge(const LmParams P) {
   }
 }
 
-// Single CTAs by default; TG_LMHEAD_PAIR=1 selects the 2-CTA (cta_group::2)
-// variant.  A/B on B200 (profiles/r01_lmhead_ab.txt): pairs +1 % at d = 1536,
-// -6 % at d = 3584, so the simpler single-CTA kernel stays the default.
-static bool lm_pair_mode() {
-  static int mode = -1;
-  if (mode < 0) {
+// Forward: single CTAs by default -- A/B on B200 (profiles/r01_lmhead_ab.txt):
+// pairs +1 % at d = 1536, -6 % at d = 3584 over the full vocabulary.  Backward
+// (dz) chunks: 2-CTA pairs by default -- +9 % at d = 1536 and 3584
+// (profiles/r01_lmhead_bwd.txt): the dz staging writes and TMA-store reads
+// compete with the UMMA operand reads for shared-memory bandwidth, and pairs
+// halve the W-tile bytes each SM stages and reads.  TG_LMHEAD_PAIR=0/1 forces
+// one mode for both.
+static bool lm_pair_mode(bool dz = false) {
+  static int mode = -2;
+  if (mode == -2) {
     const char* v = getenv("TG_LMHEAD_PAIR");
-    mode = (v && *v) ? (atoi(v) != 0) : 0;
+    mode = (v && *v) ? (atoi(v) != 0) : -1;
   }
-  return mode != 0;
+  return mode < 0 ? dz : mode != 0;
 }
 
 // Vocabulary splits per row block: enough work units to fill the SMs (or SM
 // pairs) in whole waves -- small row counts would otherwise leave SMs idle.
-int lm_split(int64_t n_rows, int64_t vocab, int n_sms) {
-  const bool pair = lm_pair_mode();
+int lm_split(int64_t n_rows, int64_t vocab, int n_sms, bool pair) {
   const int64_t rows_per_unit = pair ? 2 * LM_BM : LM_BM;
   const int64_t slots = pair ? n_sms / 2 : n_sms;
   const int64_t n_mb = (n_rows + rows_per_unit - 1) / rows_per_unit;
@@ -536,6 +656,10 @@ int lm_split(int64_t n_rows, int64_t vocab, int n_sms) {
     }
   }
   return best;
+}
+
+int lm_split(int64_t n_rows, int64_t vocab, int n_sms) {
+  return lm_split(n_rows, vocab, n_sms, lm_pair_mode());
 }
 
 size_t lm_workspace_bytes(int64_t n_rows, int64_t vocab, int n_sms) {
@@ -560,50 +684,33 @@ static PFN_cuTensorMapEncodeTiled_v12000 lm_encode_fn() {
   return fn;
 }
 
-// bf16 [rows, ld] row-major, box [box_rows, 64] with the 128-byte swizzle
+// bf16 [rows, ld] row-major, box [box_rows, box_cols]: operand loads use
+// 64-column boxes with the 128-byte swizzle, the dz stores 32 x 32 boxes with
+// the 64-byte swizzle
 static bool lm_make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld,
-                        uint32_t box_rows) {
+                        uint32_t box_rows, uint32_t box_cols = LM_BK,
+                        CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto enc = lm_encode_fn();
   if (!enc) return false;
   cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
   cuuint64_t strides[1] = {cuuint64_t(ld) * 2};
-  cuuint32_t box[2] = {cuuint32_t(LM_BK), box_rows};
+  cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// returns a cudaError_t; cudaErrorNotSupported when the driver entry point is missing
-cudaError_t launch_lmhead_logprob(const void* hidden, int64_t ld_hidden, const void* weight,
-                                  int64_t ld_weight, int64_t n_rows, int64_t vocab, int64_t dim,
-                                  const int32_t* target, float* lp, float* ent, float* lse,
-                                  void* workspace, size_t workspace_bytes, int n_sms,
-                                  cudaStream_t stream) {
-  const bool pair = lm_pair_mode();
-  CUtensorMap mx, mw;
-  if (!lm_make_map(&mx, hidden, n_rows, dim, ld_hidden, LM_BM)) return cudaErrorNotSupported;
-  if (!lm_make_map(&mw, weight, vocab, dim, ld_weight, pair ? LM_BN / 2 : LM_BN))
-    return cudaErrorNotSupported;
-  LmParams P;
-  P.n_rows = n_rows;
-  P.vocab = vocab;
-  P.dim = dim;
-  P.target = target;
-  P.lp = lp;
-  P.ent = ent;
-  P.lse = lse;
-  P.n_split = lm_split(n_rows, vocab, n_sms);
-  P.partial = reinterpret_cast<float4*>(workspace);
-  if (P.n_split > 1 && (!workspace || workspace_bytes < lm_workspace_bytes(n_rows, vocab, n_sms)))
-    return cudaErrorInvalidValue;
+template <bool kDz>
+static cudaError_t lm_launch(const CUtensorMap& mx, const CUtensorMap& mw, const CUtensorMap& md,
+                             const LmParams& P, bool pair, int n_sms, cudaStream_t stream) {
   cudaError_t e;
   if (pair) {
     const size_t smem = lm_smem_bytes<true>();
-    e = cudaFuncSetAttribute(k_lmhead_logprob<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(smem));
+    e = cudaFuncSetAttribute(k_lmhead_logprob<true, kDz>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    const int64_t units = ((n_rows + 2 * LM_BM - 1) / (2 * LM_BM)) * P.n_split;
+    const int64_t units = ((P.n_rows + 2 * LM_BM - 1) / (2 * LM_BM)) * P.n_split;
     const int64_t pairs = units < n_sms / 2 ? units : n_sms / 2;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(2 * pairs));
@@ -617,19 +724,77 @@ cudaError_t launch_lmhead_logprob(const void* hidden, int64_t ld_hidden, const v
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, k_lmhead_logprob<true>, mx, mw, P);
-    if (e != cudaSuccess) return e;
-  } else {
-    const size_t smem = lm_smem_bytes<false>();
-    e = cudaFuncSetAttribute(k_lmhead_logprob<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(smem));
-    if (e != cudaSuccess) return e;
-    const int64_t units = ((n_rows + LM_BM - 1) / LM_BM) * P.n_split;
-    const int grid = int(units < n_sms ? units : n_sms);
-    k_lmhead_logprob<false><<<grid, LM_THREADS, smem, stream>>>(mx, mw, P);
+    return cudaLaunchKernelEx(&cfg, k_lmhead_logprob<true, kDz>, mx, mw, md, P);
   }
+  const size_t smem = lm_smem_bytes<false>();
+  e = cudaFuncSetAttribute(k_lmhead_logprob<false, kDz>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  const int64_t units = ((P.n_rows + LM_BM - 1) / LM_BM) * P.n_split;
+  const int grid = int(units < n_sms ? units : n_sms);
+  k_lmhead_logprob<false, kDz><<<grid, LM_THREADS, smem, stream>>>(mx, mw, md, P);
+  return cudaGetLastError();
+}
+
+// returns a cudaError_t; cudaErrorNotSupported when the driver entry point is missing
+cudaError_t launch_lmhead_logprob(const void* hidden, int64_t ld_hidden, const void* weight,
+                                  int64_t ld_weight, int64_t n_rows, int64_t vocab, int64_t dim,
+                                  const int32_t* target, float* lp, float* ent, float* lse,
+                                  void* workspace, size_t workspace_bytes, int n_sms,
+                                  cudaStream_t stream) {
+  const bool pair = lm_pair_mode();
+  CUtensorMap mx, mw;
+  if (!lm_make_map(&mx, hidden, n_rows, dim, ld_hidden, LM_BM)) return cudaErrorNotSupported;
+  if (!lm_make_map(&mw, weight, vocab, dim, ld_weight, pair ? LM_BN / 2 : LM_BN))
+    return cudaErrorNotSupported;
+  LmParams P = {};
+  P.n_rows = n_rows;
+  P.vocab = vocab;
+  P.dim = dim;
+  P.col0 = 0;
+  P.n_cols = vocab;
+  P.target = target;
+  P.lp = lp;
+  P.ent = ent;
+  P.lse = lse;
+  P.n_split = lm_split(n_rows, vocab, n_sms);
+  P.partial = reinterpret_cast<float4*>(workspace);
+  if (P.n_split > 1 && (!workspace || workspace_bytes < lm_workspace_bytes(n_rows, vocab, n_sms)))
+    return cudaErrorInvalidValue;
+  cudaError_t e = lm_launch<false>(mx, mw, mx, P, pair, n_sms, stream);  // no dz map
+  if (e != cudaSuccess) return e;
   if (P.n_split > 1) k_lmhead_merge<<<int((n_rows + 255) / 256), 256, 0, stream>>>(P);
   return cudaGetLastError();
+}
+
+// backward of one vocabulary chunk [col0, col0 + n_cols): bf16 dz tiles, no
+// workspace (tiles are independent; the split only fills the SMs)
+cudaError_t launch_lmhead_dz(const void* hidden, int64_t ld_hidden, const void* weight,
+                             int64_t ld_weight, int64_t n_rows, int64_t vocab, int64_t dim,
+                             int64_t col0, int64_t n_cols, const int32_t* target,
+                             const float* lse, const float* coef, void* dz, int64_t ld_dz,
+                             int n_sms, cudaStream_t stream) {
+  const bool pair = lm_pair_mode(true);
+  CUtensorMap mx, mw;
+  if (!lm_make_map(&mx, hidden, n_rows, dim, ld_hidden, LM_BM)) return cudaErrorNotSupported;
+  if (!lm_make_map(&mw, weight, vocab, dim, ld_weight, pair ? LM_BN / 2 : LM_BN))
+    return cudaErrorNotSupported;
+  LmParams P = {};
+  P.n_rows = n_rows;
+  P.vocab = vocab;
+  P.dim = dim;
+  P.col0 = col0;
+  P.n_cols = n_cols;
+  P.target = target;
+  P.lse_in = lse;
+  P.coef = coef;
+  P.dz = reinterpret_cast<uint16_t*>(dz);
+  P.ld_dz = ld_dz;
+  P.n_split = lm_split(n_rows, n_cols, n_sms, pair);
+  CUtensorMap md;
+  if (!lm_make_map(&md, dz, n_rows, n_cols, ld_dz, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+    return cudaErrorNotSupported;
+  return lm_launch<true>(mx, mw, md, P, pair, n_sms, stream);
 }
 
 }  // namespace tg

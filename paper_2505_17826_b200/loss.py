@@ -90,6 +90,8 @@ class LossOutput:
     seq_lp: torch.Tensor                  # [B] f32
     seq_adv: torch.Tensor                 # [B] f32 (advantage, or coupled coefficient)
     dlogits: Optional[torch.Tensor] = None
+    row_coef: Optional[torch.Tensor] = None  # [3, T] f32 (a, hz, s), when requested
+    target: Optional[torch.Tensor] = None    # [T] i32 packed targets (loss from hidden states)
 
     def stats_dict(self) -> Dict[str, float]:
         """Device -> host read of the statistics (the only sync)."""
@@ -205,12 +207,14 @@ class RFTLoss:
 
     def from_rows(self, batch: PackedBatch, lp: torch.Tensor, entropy: torch.Tensor,
                   lse: torch.Tensor, *, n_tok_global: int = 0, n_seq_global: int = 0,
-                  n_sft_seq_global: int = 0, stream: Optional[torch.cuda.Stream] = None
-                  ) -> LossOutput:
+                  n_sft_seq_global: int = 0, stream: Optional[torch.cuda.Stream] = None,
+                  row_coef: bool = False) -> LossOutput:
         """Forward-only loss and metrics from precomputed per-row lp / entropy /
         lse (``TG_FLAG_ROWS_GIVEN``), e.g. from ``lmhead_logprob_fwd``: no
         logits are read, so a batch built with ``rows_batch`` (empty logits)
-        suffices.  Anchor KL needs logits and is rejected."""
+        suffices.  Anchor KL needs logits and is rejected.  ``row_coef=True``
+        also returns the per-row gradient coefficients ``out.row_coef`` [3, T]
+        (a, hz, s: dz = p (a + hz z) - s [v = y]) for ``lmhead_dlogits``."""
         L = N.lib()
         cb = c_batch(batch)
         cfg = self.cfg
@@ -232,6 +236,9 @@ class RFTLoss:
         co.lp, co.entropy, co.lse = lp.data_ptr(), entropy.data_ptr(), lse.data_ptr()
         co.seq_lp, co.seq_adv, co.stats = (out.seq_lp.data_ptr(), out.seq_adv.data_ptr(),
                                            out.stats.data_ptr())
+        if row_coef:
+            out.row_coef = torch.empty(3, T, **f32)
+            co.row_coef = out.row_coef.data_ptr()
         nbytes = L.tg_workspace_size(ctypes.byref(cb), ctypes.byref(cc))
         ws = self._ws.get(dev, nbytes)
         s = stream if stream is not None else torch.cuda.current_stream(dev)
@@ -272,15 +279,7 @@ def lmhead_logprob_fwd(hidden: torch.Tensor, weight: torch.Tensor,
     ``z = hidden @ weight.T`` without materialising the [T, V] logits
     (policy.logprob, policy.py:194-212, behind an LM head).  ``lp`` is None
     when no target is given."""
-    if hidden.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
-        raise TypeError("hidden and weight must be bfloat16")
-    if hidden.dim() != 2 or weight.dim() != 2 or hidden.shape[1] != weight.shape[1]:
-        raise ValueError(f"shape mismatch: hidden {tuple(hidden.shape)}, weight "
-                         f"{tuple(weight.shape)}")
-    if not hidden.is_cuda or hidden.device != weight.device:
-        raise ValueError("hidden and weight must be on the same CUDA device")
-    if hidden.stride(1) != 1 or weight.stride(1) != 1:
-        raise ValueError("hidden and weight need unit stride along d")
+    _check_lmhead(hidden, weight)
     L = N.lib()
     dev = hidden.device
     T, d = hidden.shape
@@ -304,8 +303,96 @@ def lmhead_logprob_fwd(hidden: torch.Tensor, weight: torch.Tensor,
     return lp, ent, lse
 
 
+def _check_lmhead(hidden: torch.Tensor, weight: torch.Tensor) -> None:
+    if hidden.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
+        raise TypeError("hidden and weight must be bfloat16")
+    if hidden.dim() != 2 or weight.dim() != 2 or hidden.shape[1] != weight.shape[1]:
+        raise ValueError(f"shape mismatch: hidden {tuple(hidden.shape)}, weight "
+                         f"{tuple(weight.shape)}")
+    if not hidden.is_cuda or hidden.device != weight.device:
+        raise ValueError("hidden and weight must be on the same CUDA device")
+    if hidden.stride(1) != 1 or weight.stride(1) != 1:
+        raise ValueError("hidden and weight need unit stride along d")
+
+
+def lmhead_dlogits(hidden: torch.Tensor, weight: torch.Tensor, target: torch.Tensor,
+                   lse: torch.Tensor, row_coef: torch.Tensor, col0: int, n_cols: int,
+                   out: Optional[torch.Tensor] = None,
+                   stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """d loss / d logits of the vocabulary chunk [col0, col0 + n_cols) as bf16
+    [T, n_cols], recomputed from hidden states on the tensor cores
+    (``tg_lmhead_dlogits``; policy.grad_logprob, policy.py:253-270, behind an
+    LM head).  ``lse`` comes from the forward, ``row_coef`` from
+    ``RFTLoss.from_rows(..., row_coef=True)``.  ``out`` may be a column slice of
+    a wider buffer (row pitch a multiple of 8)."""
+    _check_lmhead(hidden, weight)
+    L = N.lib()
+    dev = hidden.device
+    T, d = hidden.shape
+    V = weight.shape[0]
+    if out is None:  # row pitch a multiple of 8 elements (16-byte vector stores)
+        out = torch.empty(T, (n_cols + 7) // 8 * 8, dtype=torch.bfloat16, device=dev)[:, :n_cols]
+    if out.dtype != torch.bfloat16 or out.shape != (T, n_cols) or out.stride(1) != 1:
+        raise ValueError(f"out must be a bf16 [{T}, {n_cols}] tensor with unit column stride")
+    tgt = target.to(device=dev, dtype=torch.int32).contiguous()
+    for name, t, shape in (("lse", lse, (T,)), ("row_coef", row_coef, (3, T))):
+        if t.dtype != torch.float32 or t.shape != shape or not t.is_contiguous() or \
+                t.device != dev:
+            raise ValueError(f"{name} must be a contiguous float32 {list(shape)} tensor on {dev}")
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    with torch.cuda.device(dev):
+        N.check(L.tg_lmhead_dlogits(
+            hidden.data_ptr(), hidden.stride(0), weight.data_ptr(), weight.stride(0), T, V, d,
+            int(col0), int(n_cols), tgt.data_ptr(), lse.data_ptr(), row_coef.data_ptr(),
+            out.data_ptr(), out.stride(0), s.cuda_stream))
+    return out
+
+
+def lmhead_loss_fwd_bwd(hidden: torch.Tensor, weight: torch.Tensor, loss: "RFTLoss", target,
+                        seq_lengths, group_sizes, reward, *, chunk_cols: int = 16384,
+                        grad_weight: bool = True, **pack_kw):
+    """RFT loss and its gradients w.r.t. the hidden states and the LM-head
+    weight, without the [T, V] logits (vocabulary-chunked):
+
+    1. ``tg_lmhead_logprob_fwd``: per-row lp / entropy / lse on the tensor cores;
+    2. the loss epilogue on those rows (``TG_FLAG_ROWS_GIVEN``), which also
+       returns the per-row gradient coefficients;
+    3. per vocabulary chunk of ``chunk_cols`` columns: ``tg_lmhead_dlogits``
+       recomputes the chunk's logits and writes its bf16 d loss / d z, then two
+       plain GEMMs (cuBLAS through torch) accumulate d hidden += dz . W_chunk
+       (fp32) and write d W_chunk = dz^T . hidden.
+
+    Peak extra memory is T x chunk_cols bf16.  Returns ``(LossOutput,
+    d_hidden [T, d] fp32, d_weight [V, d] bf16 or None)``."""
+    _check_lmhead(hidden, weight)
+    out = lmhead_loss_fwd(hidden, weight, loss, target, seq_lengths, group_sizes, reward,
+                          row_coef=True, **pack_kw)
+    T, d = hidden.shape
+    V = int(weight.shape[0])
+    dev = hidden.device
+    d_hidden = torch.zeros(T, d, dtype=torch.float32, device=dev)
+    d_weight = torch.empty(V, d, dtype=torch.bfloat16, device=dev) if grad_weight else None
+    if T == 0:
+        if d_weight is not None:
+            d_weight.zero_()
+        return out, d_hidden, d_weight
+    chunk = max(8, min(int(chunk_cols), V))
+    pitch = (chunk + 7) // 8 * 8
+    buf = torch.empty(T, pitch, dtype=torch.bfloat16, device=dev)
+    tgt = out.target
+    for c0 in range(0, V, chunk):
+        nc = min(chunk, V - c0)
+        dz = lmhead_dlogits(hidden, weight, tgt, out.lse, out.row_coef, c0, nc, out=buf[:, :nc])
+        w_c = weight[c0:c0 + nc]
+        d_hidden = torch.addmm(d_hidden, dz, w_c, out_dtype=torch.float32)
+        if d_weight is not None:
+            torch.mm(dz.t(), hidden, out=d_weight[c0:c0 + nc])
+    return out, d_hidden, d_weight
+
+
 def lmhead_loss_fwd(hidden: torch.Tensor, weight: torch.Tensor, loss: "RFTLoss", target,
-                    seq_lengths, group_sizes, reward, **pack_kw) -> LossOutput:
+                    seq_lengths, group_sizes, reward, *, row_coef: bool = False,
+                    **pack_kw) -> LossOutput:
     """RFT loss and metrics straight from hidden states: the fused LM-head
     kernel gives per-row lp / entropy / lse (no [T, V] logits anywhere), then
     the loss epilogue runs on those rows (``RFTLoss.from_rows``).  ``pack_kw``
@@ -321,4 +408,6 @@ def lmhead_loss_fwd(hidden: torch.Tensor, weight: torch.Tensor, loss: "RFTLoss",
     rows = torch.empty((0, V), dtype=torch.bfloat16, device=hidden.device)
     batch = pack_arrays(rows, tgt_host, seq_lengths, group_sizes, reward, vocab=V, **pack_kw)
     lp, ent, lse = lmhead_logprob_fwd(hidden, weight, batch.target)
-    return loss.from_rows(batch, lp, ent, lse, **glob)
+    out = loss.from_rows(batch, lp, ent, lse, row_coef=row_coef, **glob)
+    out.target = batch.target
+    return out

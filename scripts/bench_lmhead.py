@@ -1,6 +1,8 @@
 """Throughput of the fused LM-head logprob forward (tg_lmhead_logprob_fwd) at
 Qwen2.5 shapes: TFLOP/s of the logits GEMM (2 T V d) against the measured bf16
-peak, with cuBLAS (torch.matmul into materialised logits) timed beside it.
+peak, with cuBLAS (torch.matmul into materialised logits) timed beside it;
+plus the training step from hidden states (loss + d hidden + d W), vocabulary
+chunked through tg_lmhead_dlogits, against the unfused GEMM + loss + GEMMs.
 
     python scripts/bench_lmhead.py [--rows 16384] [--dim 1536] [--vocab 151936]
 """
@@ -34,6 +36,7 @@ def main():
     p.add_argument("--rows", type=int, default=16384)
     p.add_argument("--dim", type=int, default=1536)
     p.add_argument("--vocab", type=int, default=151936)
+    p.add_argument("--chunk", type=int, default=16384, help="vocabulary chunk of the backward")
     a = p.parse_args()
     T, d, V = a.rows, a.dim, a.vocab
     h = torch.randn(T, d, device="cuda").to(torch.bfloat16)
@@ -66,6 +69,27 @@ def main():
         torch.matmul(h, w.T, out=logits)
         rl(lbatch, dlogits=None)
     ms_loss_unfused = timed(loss_unfused, reps=5)
+    # training step from hidden states: loss + d hidden + d W.  Chunked
+    # (tg_lmhead_dlogits recompute + two GEMMs per vocabulary chunk, no [T, V]
+    # buffer) against the unfused step (GEMM -> logits, the fused loss kernel
+    # in place, then the two gradient GEMMs over the full [T, V] dlogits).
+    from paper_2505_17826_b200 import lmhead_dlogits, lmhead_loss_fwd_bwd
+    ms_train_chunked = timed(lambda: lmhead_loss_fwd_bwd(h, w, rl, tgt_h, lens, groups, rew,
+                                                         chunk_cols=a.chunk), reps=3)
+    dh_u = torch.empty(T, d, dtype=torch.bfloat16, device="cuda")
+    dw_u = torch.empty(V, d, dtype=torch.bfloat16, device="cuda")
+
+    def train_unfused():
+        torch.matmul(h, w.T, out=logits)
+        rl(lbatch, dlogits="inplace")
+        torch.mm(logits, w, out=dh_u)
+        torch.mm(logits.T, h, out=dw_u)
+    ms_train_unfused = timed(train_unfused, reps=3)
+    fo = lmhead_loss_fwd(h, w, rl, tgt_h, lens, groups, rew, row_coef=True)
+    nc = min(a.chunk, V)
+    dzb = torch.empty(T, nc, dtype=torch.bfloat16, device="cuda")
+    ms_dz = timed(lambda: lmhead_dlogits(h, w, fo.target, fo.lse, fo.row_coef, 0, nc, out=dzb))
+    del dzb
     lp_f, _, lse_f = lmhead_logprob_fwd(h, w, y)
     lp_u, _, lse_u, _ = logprob_fwd(batch)
     dlse = float((lse_f - lse_u).abs().max())
@@ -85,7 +109,11 @@ def main():
            "speedup_vs_unfused": ms_unfused / ms,
            "max_abs_lse_diff_vs_unfused_bf16_logits": dlse,
            "loss_fwd_from_hidden_ms": ms_loss_fused,
-           "loss_fwd_unfused_gemm_plus_loss_ms": ms_loss_unfused}
+           "loss_fwd_unfused_gemm_plus_loss_ms": ms_loss_unfused,
+           "train_step_chunked_ms": ms_train_chunked, "train_chunk_cols": a.chunk,
+           "train_step_unfused_ms": ms_train_unfused,
+           "dlogits_kernel_ms_per_chunk": ms_dz,
+           "dlogits_kernel_tflops": 2.0 * T * nc * d / ms_dz / 1e9}
     print(json.dumps(out))
 
 

@@ -120,3 +120,87 @@ def test_loss_from_hidden_states_matches_logits_path(cfg_kw):
         assert a[k] == pytest.approx(b[k], rel=1e-4, abs=1e-5), k
     torch.testing.assert_close(got.seq_lp, want.seq_lp, atol=2e-3, rtol=1e-5)
     assert got.dlogits is None
+
+
+@pytest.mark.parametrize("cfg_kw", [
+    dict(advantage_fn="grpo", policy_loss_fn="ppo_clip", kl_fn="low_var_kl", kl_coef=0.001,
+         entropy_loss_fn="default", entropy_coef=0.001, loss_agg_mode="token-mean"),
+    dict(policy_loss_fn="opmd_kimi", tau=0.7),
+    dict(advantage_fn="grpo", policy_loss_fn="ppo_clip", loss_agg_mode="token-mean",
+         sft_weight=1.0),
+], ids=["grpo_ppo_k3_ent", "kimi", "mixed_sft"])
+def test_loss_backward_from_hidden_states_matches_fp32(cfg_kw):
+    """Vocabulary-chunked backward from hidden states (tg_lmhead_dlogits +
+    two GEMMs per chunk) against the fp32-logits path: dlogits of the fp32
+    logits (the parity-tested fp32 kernel path), then d hidden = dz W and
+    d W = dz^T h in fp32.  The chunk (1,000 columns) is not a multiple of the
+    256-column tile and V = 3,000 is not either.
+
+    Tolerances: dz is stored in bf16 (relative rounding 2^-9 per element), so
+    per element 2^-8 max|dz| + 1e-2 |dz| (the parity bar of the dlogits
+    tests); d hidden / d W as relative Frobenius error <= 1e-2."""
+    from paper_2505_17826_b200 import (RFTLoss, RFTLossConfig, lmhead_dlogits,
+                                       lmhead_loss_fwd_bwd, pack_arrays)
+    T_seq, B, d, V = 48, 8, 256, 3000
+    T = T_seq * B
+    h, w, y = make(T, V, d, seed=11)
+    rng = np.random.default_rng(11)
+    reward = rng.integers(0, 2, B).astype(np.float32)
+    old = (rng.normal(-8.0, 0.5, T)).astype(np.float32)
+    ref = (rng.normal(-8.0, 0.5, T)).astype(np.float32)
+    seq_ref = rng.normal(-400.0, 10.0, B).astype(np.float32)
+    kind = np.array([0, 0, 0, 0, 1, 1, 1, 1], np.uint8) if cfg_kw.get("sft_weight") else None
+    side = dict(old_lp=old, ref_lp=ref, seq_ref_lp=seq_ref, seq_kind=kind)
+    loss = RFTLoss(RFTLossConfig(**cfg_kw))
+    got, dh, dw = lmhead_loss_fwd_bwd(h, w, loss, y.cpu().numpy(), [T_seq] * B, [4, 4], reward,
+                                      chunk_cols=1000, **side)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    z = (h.float() @ w.float().T).contiguous()
+    want = loss(pack_arrays(z, y.cpu().numpy(), [T_seq] * B, [4, 4], reward, **side),
+                dlogits="new")
+    a, b = got.stats_dict(), want.stats_dict()
+    for k in ("loss", "pg_loss", "kl_loss", "entropy_loss", "sft_loss", "sum_lp"):
+        assert a[k] == pytest.approx(b[k], rel=1e-4, abs=1e-5), k
+    dl = want.dlogits
+    dh_ref = dl @ w.float()
+    dw_ref = dl.T @ h.float()
+    assert torch.isfinite(dh).all() and torch.isfinite(dw.float()).all()
+    assert float((dh - dh_ref).norm() / dh_ref.norm()) < 1e-2
+    assert float((dw.float() - dw_ref).norm() / dw_ref.norm()) < 1e-2
+    # one chunk directly, at an offset that is not tile aligned
+    dz = lmhead_dlogits(h, w, got.target, got.lse, got.row_coef, 1234, 777).float()
+    want_c = dl[:, 1234:1234 + 777]
+    tol = 2.0 ** -8 * float(want_c.abs().max()) + 1e-2 * want_c.abs()
+    assert bool(((dz - want_c).abs() <= tol).all())
+
+
+def test_lmhead_dlogits_argument_errors():
+    from paper_2505_17826_b200 import lmhead_dlogits
+    from paper_2505_17826_b200._native import NativeError
+    h, w, y = make(128, 512, 64, seed=4)
+    lse = torch.zeros(128, device="cuda")
+    coef = torch.zeros(3, 128, device="cuda")
+    with pytest.raises(NativeError):
+        lmhead_dlogits(h, w, y, lse, coef, 500, 100)  # chunk past the vocabulary
+    buf = torch.empty(128, 100, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(NativeError):
+        lmhead_dlogits(h, w, y, lse, coef, 0, 99, out=buf[:, 1:])  # misaligned out
+    with pytest.raises(ValueError):
+        lmhead_dlogits(h, w, y, lse, coef[:2], 0, 64)
+
+
+@pytest.mark.skipif(bool(__import__("os").environ.get("TG_LMHEAD_PAIR")),
+                    reason="already pinned to one CTA mode by the environment")
+@pytest.mark.parametrize("pair", ["0", "1"])
+def test_lmhead_backward_in_both_cta_modes(pair):
+    """The backward chunk kernel runs as 2-CTA pairs by default and as single
+    CTAs with TG_LMHEAD_PAIR=0 (the forward the other way round); the mode is
+    read once per process, so each runs the parity tests in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, TG_LMHEAD_PAIR=pair)
+    r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-q", "-x", "-p",
+                        "no:cacheprovider", "-k", "matches_torch_fp32 or backward_from_hidden"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
