@@ -24,6 +24,12 @@
 //    next tile's MMAs already run into the other accumulator.
 //  Rows past T and vocabulary columns past V come in as TMA zero fill and are
 //  masked in the epilogue.
+//
+// Backward (kDz = true, tg_lmhead_dlogits): the same pipeline over one
+// vocabulary chunk; the epilogue writes bf16 d loss / d z = p (a + hz z) - s [v = y]
+// of each tile (policy.grad_logprob, policy.py:253-270, behind an LM head)
+// through swizzled shared-memory staging and TMA bulk-tensor stores.  2-CTA
+// pairs by default for this mode (see lm_pair_mode).
 #include "tg_common.cuh"
 #include "tg_vecmath.cuh"
 
