@@ -54,6 +54,7 @@ struct LmParams {
   int64_t n_rows, vocab, dim;
   int64_t col0, n_cols;   // vocabulary columns [col0, col0 + n_cols) covered by the tiles
   int n_split;            // vocabulary splits per row block (> 1: partials + merge kernel)
+  int sp_major;           // work-unit order: split-major (1) or row-block-major (0)
   float4* partial;        // [n_split, T] (m, sum e, sum e z, z_target) when n_split > 1
   const int32_t* target;  // [T] (may be null: lp not produced)
   float* lp;              // [T]
@@ -289,11 +290,21 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
   // work unit u = (row block u / n_split, vocabulary split u % n_split)
   const int n_split = P.n_split;
   const int n_units = n_mb * n_split;
+  // kSpMajor: units ordered split-major, so the CTAs resident at once share a
+  // vocabulary range and each W tile is fetched from DRAM once per wave and
+  // served to the other CTAs from L2 (row-block-major otherwise)
   auto unit_tiles = [&](int u, int& mb, int& nt0, int& nt1) {
-    mb = u / n_split;
-    const int sp = u - mb * n_split;
+    int sp;
+    if (P.sp_major) {
+      sp = u / n_mb;
+      mb = u - sp * n_mb;
+    } else {
+      mb = u / n_split;
+      sp = u - mb * n_split;
+    }
     nt0 = int((int64_t(sp) * n_nt) / n_split);
     nt1 = int((int64_t(sp + 1) * n_nt) / n_split);
+    return sp;
   };
   const int n_kb = int(P.dim / LM_BK);
 
@@ -500,7 +511,7 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
     } else
     for (int u = unit0; u < n_units; u += unit_stride) {
       int mb, nt0, nt1;
-      unit_tiles(u, mb, nt0, nt1);
+      const int sp_u = unit_tiles(u, mb, nt0, nt1);
       const int64_t row = int64_t(mb) * ROWS_PER_UNIT + int64_t(rank) * LM_BM + 32 * q + lane;
       const int y = (row < T && P.target) ? P.target[row] : -1;
       float m = -1.0e30f, zy = kNegInf;
@@ -579,7 +590,7 @@ __global__ void __launch_bounds__(LM_THREADS, 1)
         upk2(t2, t0, t1);
         const float s = s0 + s1, t = t0 + t1;
         if (n_split > 1) {
-          P.partial[int64_t(u - mb * n_split) * T + row] = make_float4(m, s, t, zy);
+          P.partial[int64_t(sp_u) * T + row] = make_float4(m, s, t, zy);
         } else {
           const float l = m + logf(s);
           P.lse[row] = l;
@@ -641,6 +652,24 @@ static bool lm_pair_mode(bool dz = false) {
     mode = (v && *v) ? (atoi(v) != 0) : -1;
   }
   return mode < 0 ? dz : mode != 0;
+}
+
+// Work-unit order.  Split-major when the CTAs resident at once (one 128-row X
+// block each, all on the same vocabulary range) keep their X blocks and the
+// W range in L2 -- each W tile then comes from DRAM once and is served to the
+// other CTAs from L2; row-block-major otherwise (a few X blocks, the CTAs that
+// share a range walk the W tiles in step).  Measured (profiles/r01_lmhead_bwd.txt):
+// split-major +3 % at d = 1,536 (116 MB working set), -20 % at d = 3,584
+// (272 MB).  TG_LMHEAD_ORDER=0/1 forces one order.
+static int lm_sp_major(int64_t cols, int64_t dim, int n_split, int n_sms) {
+  static int mode = -2;
+  if (mode == -2) {
+    const char* v = getenv("TG_LMHEAD_ORDER");
+    mode = (v && *v) ? (atoi(v) != 0) : -1;
+  }
+  if (mode >= 0) return mode;
+  const double ws = 2.0 * double(dim) * (double(n_sms) * LM_BM + double(cols) / n_split);
+  return ws <= 120.0 * 1024 * 1024 ? 1 : 0;
 }
 
 // Vocabulary splits per row block: enough work units to fill the SMs (or SM
@@ -764,6 +793,7 @@ cudaError_t launch_lmhead_logprob(const void* hidden, int64_t ld_hidden, const v
   P.ent = ent;
   P.lse = lse;
   P.n_split = lm_split(n_rows, vocab, n_sms);
+  P.sp_major = lm_sp_major(vocab, dim, P.n_split, n_sms);
   P.partial = reinterpret_cast<float4*>(workspace);
   if (P.n_split > 1 && (!workspace || workspace_bytes < lm_workspace_bytes(n_rows, vocab, n_sms)))
     return cudaErrorInvalidValue;
@@ -797,6 +827,7 @@ cudaError_t launch_lmhead_dz(const void* hidden, int64_t ld_hidden, const void* 
   P.dz = reinterpret_cast<uint16_t*>(dz);
   P.ld_dz = ld_dz;
   P.n_split = lm_split(n_rows, n_cols, n_sms, pair);
+  P.sp_major = lm_sp_major(n_cols, dim, P.n_split, n_sms);
   CUtensorMap md;
   if (!lm_make_map(&md, dz, n_rows, n_cols, ld_dz, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
     return cudaErrorNotSupported;
