@@ -16,7 +16,7 @@
 //  * 16 consumer warps (4 per SM sub-partition), four 16-byte vectors per
 //    thread per chunk.  Phase 1 (as chunks land): online sum-exp / sum p*z in
 //    packed fp32x2 arithmetic (FFMA2 / FADD2) with MUFU ex2, speculatively
-//    against the lane's reference max (clamp / max / rescale only when the
+//    against the warp's reference max (clamp / max / rescale only when the
 //    chunk's sums are unsafe).  Each thread copies its raw chunk data into its
 //    own TMEM lane (tcgen05.st) and the shared-memory slot is released at once:
 //    the row slices stay resident in the otherwise idle TMEM, the ring is pure
