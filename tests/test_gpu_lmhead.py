@@ -189,6 +189,30 @@ def test_lmhead_dlogits_argument_errors():
         lmhead_dlogits(h, w, y, lse, coef[:2], 0, 64)
 
 
+@pytest.mark.parametrize("T,V,d,col0,n_cols", [(1, 700, 64, 0, 700), (129, 1000, 128, 37, 601),
+                                               (300, 4097, 192, 4000, 97),
+                                               (513, 2048, 256, 256, 1792)])
+def test_lmhead_dlogits_matches_formula(T, V, d, col0, n_cols):
+    """tg_lmhead_dlogits against the formula in fp32 torch, with arbitrary row
+    coefficients: dz = exp(z - lse) (a + hz z) - s [v = y] over the chunk.
+    Row counts off the 128-row tile, chunk offsets / widths off the 256-column
+    tile and the 8-column store granule."""
+    from paper_2505_17826_b200 import lmhead_dlogits
+    h, w, y = make(T, V, d, seed=T + col0)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    z = h.float() @ w.float().T
+    lse = torch.logsumexp(z, 1).contiguous()
+    g = torch.Generator(device="cuda").manual_seed(5)
+    coef = (torch.randn(3, T, device="cuda", generator=g) * 0.3).contiguous()
+    got = lmhead_dlogits(h, w, y, lse, coef, col0, n_cols).float()
+    zc = z[:, col0:col0 + n_cols]
+    want = torch.exp(zc - lse[:, None]) * (coef[0][:, None] + coef[1][:, None] * zc)
+    onehot = (y.long()[:, None] == torch.arange(col0, col0 + n_cols, device="cuda")[None, :])
+    want = want - coef[2][:, None] * onehot.float()
+    tol = 2.0 ** -8 * float(want.abs().max()) + 1e-2 * want.abs()
+    assert bool(((got - want).abs() <= tol).all())
+
+
 @pytest.mark.skipif(bool(__import__("os").environ.get("TG_LMHEAD_PAIR")),
                     reason="already pinned to one CTA mode by the environment")
 @pytest.mark.parametrize("pair", ["0", "1"])
@@ -201,6 +225,6 @@ def test_lmhead_backward_in_both_cta_modes(pair):
     import sys
     env = dict(os.environ, TG_LMHEAD_PAIR=pair)
     r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-q", "-x", "-p",
-                        "no:cacheprovider", "-k", "matches_torch_fp32 or backward_from_hidden"],
+                        "no:cacheprovider", "-k", "matches_torch_fp32 or backward_from_hidden or matches_formula"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
