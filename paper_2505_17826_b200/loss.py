@@ -397,7 +397,9 @@ def lmhead_loss_fwd(hidden: torch.Tensor, weight: torch.Tensor, loss: "RFTLoss",
     kernel gives per-row lp / entropy / lse (no [T, V] logits anywhere), then
     the loss epilogue runs on those rows (``RFTLoss.from_rows``).  ``pack_kw``
     takes pack_arrays' side inputs (old_lp, ref_lp, seq_ref_lp, seq_kind, ...)
-    and the global denominators (n_tok_global, ...)."""
+    and the global denominators (n_tok_global, ...).  ``row_coef=True`` also
+    returns the per-row gradient coefficients (``out.row_coef``) that
+    ``lmhead_dlogits`` needs; ``out.target`` holds the packed device targets."""
     from .packing import pack_arrays
     glob = {k: pack_kw.pop(k) for k in ("n_tok_global", "n_seq_global", "n_sft_seq_global")
             if k in pack_kw}
