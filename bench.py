@@ -95,6 +95,7 @@ def parse():
     p.add_argument("--quiet", action="store_true")
     p.add_argument("--variant", default="grpo",
                    choices=["grpo", "grpo_two_pass", "opmd_kimi", "opmd_pairwise", "sft",
+                            "opmd_kimi_unscaled", "opmd_pairwise_unscaled",
                             "c1", "c3", "c4", "c5"],
                    help="loss variant (the headline metric is 'grpo' = configs[1]; c3 / c4 / c5 "
                         "are the per-GPU shards of BASELINE configs[2..4]; the others measure "
@@ -318,8 +319,9 @@ def main():
                         kl_coef=0.001, loss_agg_mode="token-mean", clip_lo=0.2, clip_hi=0.28)
     if args.variant == "grpo_two_pass":
         cfg = cfg.with_(force_two_pass=True)
-    elif args.variant in ("opmd_kimi", "opmd_pairwise"):
-        cfg = RFTLossConfig(policy_loss_fn=args.variant, tau=1.0)
+    elif args.variant in ("opmd_kimi", "opmd_pairwise", "opmd_kimi_unscaled",
+                          "opmd_pairwise_unscaled"):
+        cfg = RFTLossConfig(policy_loss_fn=args.variant.replace("_unscaled", ""), tau=1.0)
     elif args.variant == "sft":
         cfg = RFTLossConfig.from_variant("SFT")
     elif args.variant == "c3":  # PPO clip + low_var_kl + entropy bonus
@@ -328,6 +330,8 @@ def main():
         cfg = cfg.with_(sft_weight=1.0)
     loss = RFTLoss(cfg)
     two_pass = args.variant in ("grpo_two_pass", "opmd_kimi", "opmd_pairwise")
+    # coupled loss in one pass (TG_FLAG_UNSCALED_GRAD, route 4): p - e_y rows + row scales
+    unscaled = args.variant.endswith("_unscaled")
     algo_bytes_row = (6 * V + 24) if two_pass else ALGO_BYTES_PER_ROW
 
     # ---- resident synthetic inputs (outside timing) ----
@@ -388,15 +392,16 @@ def main():
         outs.append(None)
         T += int(rows.size)
         n_sft += 0 if kind is None else int(kind.sum())
-    route = loss.route(batches[0])
-    assert route == (1 if not two_pass else (2 if args.variant == "grpo_two_pass" else 3)), route
+    route = loss.route(batches[0], unscaled=unscaled)
+    assert route == (4 if unscaled else
+                     1 if not two_pass else (2 if args.variant == "grpo_two_pass" else 3)), route
     n_tok_g, n_seq_g, n_sft_g = world * T, world * B, world * n_sft
     stats_all = torch.zeros((n_mb, N.NSTAT), dtype=torch.float64, device=dev)
 
     def step():
         for m in range(n_mb):
             outs[m] = loss(batches[m], dlogits=dz, n_tok_global=n_tok_g, n_seq_global=n_seq_g,
-                           n_sft_seq_global=n_sft_g, out=outs[m])
+                           n_sft_seq_global=n_sft_g, out=outs[m], unscaled=unscaled)
         st = torch.stack([o.stats for o in outs]).sum(0)
         return allreduce_stats(st)
 
@@ -430,7 +435,7 @@ def main():
             L.tg_set_timing_events(evs[k][0].cuda_event, evs[k][1].cuda_event)
             k += 1
             outs[m] = loss(batches[m], dlogits=dz, n_tok_global=n_tok_g, n_seq_global=n_seq_g,
-                           n_sft_seq_global=n_sft_g, out=outs[m])
+                           n_sft_seq_global=n_sft_g, out=outs[m], unscaled=unscaled)
         st = allreduce_stats(torch.stack([o.stats for o in outs]).sum(0))
     t_end.record()
     torch.cuda.synchronize()

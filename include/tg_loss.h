@@ -101,10 +101,18 @@ enum {
   TG_FLAG_FORCE_TWO_PASS = 1,  /* use the forward + backward streaming kernels even when
                                   the fused single-pass kernel applies (testing / A-B)  */
   TG_FLAG_NO_FUSED_TMA = 2,    /* alias kept for clarity: same effect                   */
-  TG_FLAG_ROWS_GIVEN = 4       /* forward-only loss from precomputed per-row values: out.lp,
+  TG_FLAG_ROWS_GIVEN = 4,      /* forward-only loss from precomputed per-row values: out.lp,
                                   out.entropy, out.lse are INPUTS (e.g. from
                                   tg_lmhead_logprob_fwd); no logits are read (batch.logits
                                   may be NULL) and out.dlogits must be NULL               */
+  TG_FLAG_UNSCALED_GRAD = 8    /* sequence-coupled losses (OPMD_KIMI / OPMD_PAIRWISE / DPO)
+                                  in ONE pass over the logits (4V bytes per row instead
+                                  of 6V): out.dlogits receives the unscaled p - e_y and
+                                  out.row_coef (required) the per-row scale s_t in its
+                                  third block, d loss / d z_t = s_t (p_t - e_y) -- the
+                                  caller folds diag(s) into its LM-head backward
+                                  (d hidden rows and the hidden rows of d W scale by s_t;
+                                  SURVEY.md 7, hard part 3).  No anchor KL.          */
 };
 
 /* stats[] layout (double).  Sums are over this call's rows / groups; the
@@ -244,7 +252,8 @@ int tg_apply_update(float* table, int64_t ld_table, int64_t n_states, int64_t vo
                     int64_t n_rows, double learning_rate, int32_t* status, void* stream);
 
 /* Which kernel route tg_loss_fwd_bwd takes for this input: 1 = fused single
-   pass (4V bytes/row), 2 = forward + backward streaming (6V), 3 = coupled. */
+   pass (4V bytes/row), 2 = forward + backward streaming (6V), 3 = coupled
+   (6V), 4 = coupled with TG_FLAG_UNSCALED_GRAD (single pass, 4V). */
 int tg_route(const TgBatch* batch, const TgConfig* cfg);
 
 /* Timing hook (measurement only): when both are non-NULL cudaEvent_t handles,

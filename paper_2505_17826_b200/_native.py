@@ -25,6 +25,7 @@ TG_ENT_NONE, TG_ENT_DEFAULT = 0, 1
  TG_AGG_SEQ_MEAN_TOKEN_SUM_NORM) = 0, 1, 2, 3, 4
 TG_FLAG_FORCE_TWO_PASS = 1
 TG_FLAG_ROWS_GIVEN = 4
+TG_FLAG_UNSCALED_GRAD = 8
 
 STAT_NAMES = [
     "loss", "pg_loss", "kl_loss", "entropy_loss", "anchor_loss", "sft_loss",

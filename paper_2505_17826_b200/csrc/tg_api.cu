@@ -359,7 +359,12 @@ void run_forward(const KParams& P, const TgBatch* b, bool anchor, bool vin, int 
 }
 
 int route_of(const TgBatch* b, const TgConfig* c, const TgOut* o) {
-  if (coupled_pg(c->policy_loss_fn)) return 3;
+  if (coupled_pg(c->policy_loss_fn)) {
+    if ((c->flags & TG_FLAG_UNSCALED_GRAD) && o && o->dlogits && c->anchor_beta <= 0 &&
+        !(c->flags & (TG_FLAG_FORCE_TWO_PASS | TG_FLAG_ROWS_GIVEN)) && fused_plan(b, o).cl != 0)
+      return 4;
+    return 3;
+  }
   if (c->flags & TG_FLAG_ROWS_GIVEN) return 2;
   if (c->anchor_beta > 0) return 2;
   if (o && o->row_coef) return 2;  // the fused kernel keeps the coefficients on chip
@@ -423,6 +428,15 @@ int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspa
   rc = validate_cfg(b, c);
   if (rc) return rc;
   if (!o || !o->stats) return fail(TG_EINVAL, "out.stats is required");
+  if (c->flags & TG_FLAG_UNSCALED_GRAD) {
+    if (!coupled_pg(c->policy_loss_fn))
+      return fail(TG_EINVAL, "TG_FLAG_UNSCALED_GRAD applies to sequence-coupled losses "
+                             "(OPMD_KIMI / OPMD_PAIRWISE / DPO) only");
+    if (!o->dlogits || !o->row_coef)
+      return fail(TG_EINVAL, "TG_FLAG_UNSCALED_GRAD needs out.dlogits and out.row_coef");
+    if (c->flags & TG_FLAG_ROWS_GIVEN)
+      return fail(TG_EINVAL, "TG_FLAG_UNSCALED_GRAD and TG_FLAG_ROWS_GIVEN exclude each other");
+  }
   if (o->row_coef && c->anchor_beta > 0)
     return fail(TG_EINVAL, "out.row_coef cannot describe the anchor-KL gradient (anchor_beta > 0)");
   if (o->dlogits) {
@@ -439,8 +453,11 @@ int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspa
   KParams P;
   fill_params(P, b, c, o, ws, L);
   void* meta = ws + L.meta;
-  const int route = route_of(b, c, o);
-  const bool coupled = route == 3;
+  int route = route_of(b, c, o);
+  if (route == 3 && (c->flags & TG_FLAG_UNSCALED_GRAD))
+    return fail(TG_EUNSUPPORTED, "TG_FLAG_UNSCALED_GRAD: no single-pass plan for this batch "
+                                 "(dtype / pitch / anchor / forced two-pass)");
+  const bool coupled = route == 3 || route == 4;
   const bool anchor = c->anchor_beta > 0;
   const int esz = esz_of(b->dtype);
   cudaGetLastError();  // clear stale errors
@@ -448,7 +465,31 @@ int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspa
   cudaEvent_t ev_begin = g_ev_begin, ev_end = g_ev_end;
   g_ev_begin = g_ev_end = nullptr;
   count_launches(launch_group_prep(P, coupled, st));
-  if (route == 1) {
+  if (route == 4) {
+    // coupled loss in one pass: the fused kernel writes p - e_y and the per-row
+    // lp / entropy / lse; the sequence sums, the coupled coefficients and the
+    // per-row scale (row_coef) follow as in route 3, without a backward pass
+    const FusedPlan fp = fused_plan(b, o);
+    P.n_partials = fp.n_ctas;
+    if (P.n_partials > kMaxPartials) return fail(TG_EUNSUPPORTED, "too many CTAs");
+    if (b->n_rows > 0) {
+      if (ev_begin) cudaEventRecord(ev_begin, st);
+      cudaError_t e = launch_fused(P, meta, fp.cl, fp.n_slots, fp.n_ctas, fp.prefetch_rows, st);
+      if (ev_end) cudaEventRecord(ev_end, st);
+      if (e != cudaSuccess) return fail(TG_ECUDA, "fused kernel launch: %s", cudaGetErrorString(e));
+      count_launches(1);
+    }
+    launch_rowmeta(P, meta, st);
+    launch_seq_reduce(P, st);
+    launch_coupled(P, st);
+    count_launches((b->n_seqs > 0 ? 2 : 0) + (b->n_groups > 0 ? 1 : 0));
+    int cgrid = int((b->n_rows + 255) / 256);
+    if (cgrid < 1) cgrid = 1;
+    if (cgrid > kMaxPartials) cgrid = kMaxPartials;
+    P.n_partials = cgrid;
+    launch_rowcoef(P, meta, true, false, cgrid, st);
+    count_launches(1);
+  } else if (route == 1) {
     const FusedPlan fp = fused_plan(b, o);
     // TG_FUSED_IMPL=l2: the L2-reread variant (tg_fused_l2.cu), for A/B
     const bool l2 = env_int("TG_FUSED_IMPL", 0) == 2;

@@ -699,11 +699,19 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       }
       const Online tot = warp_merge_first<(NP < 32 ? NP : 32)>(acc_p);
       if (lane == 0) {
-        const float lse = tot.m + __logf(tot.s);
-        const float H = lse - __fdividef(tot.t, tot.s);
+        // fast log / divide on the critical path; full precision when the row's
+        // lp feeds sequence sums that couple the gradient (route 4), as in k_fwd_tma
+        const bool precise = (P.flags & TG_FLAG_UNSCALED_GRAD) != 0;
+        const float lse = tot.m + (precise ? logf(tot.s) : __logf(tot.s));
+        const float H = lse - (precise ? tot.t / tot.s : __fdividef(tot.t, tot.s));
         const bool bad_target = (cur.flags & 2u) != 0;
         const float lp = tzy - lse;
-        RowTerms o = meta_terms(P, cur, lp, H);
+        RowTerms o;
+        if (P.flags & TG_FLAG_UNSCALED_GRAD) {  // coupled, one pass: dz = p - e, scale later
+          o = RowTerms{1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0, 0, 0};
+        } else {
+          o = meta_terms(P, cur, lp, H);
+        }
         if (bad_target) {
           o.s = 0.f;
           o.h = 0.f;

@@ -93,6 +93,11 @@ class LossOutput:
     row_coef: Optional[torch.Tensor] = None  # [3, T] f32 (a, hz, s), when requested
     target: Optional[torch.Tensor] = None    # [T] i32 packed targets (loss from hidden states)
 
+    @property
+    def row_scale(self) -> Optional[torch.Tensor]:
+        """Per-row factor of an unscaled gradient (``unscaled=True``): s_t."""
+        return None if self.row_coef is None else self.row_coef[2]
+
     def stats_dict(self) -> Dict[str, float]:
         """Device -> host read of the statistics (the only sync)."""
         host = self.stats.detach().cpu().tolist()
@@ -153,20 +158,33 @@ class RFTLoss:
         self.cfg = cfg if cfg is not None else RFTLossConfig(**kw)
         self._ws = _Workspace()
 
-    def route(self, batch: PackedBatch) -> int:
-        """1 = fused single pass, 2 = forward+backward streaming, 3 = sequence-coupled."""
-        return N.lib().tg_route(ctypes.byref(c_batch(batch)), ctypes.byref(self.cfg.to_c()))
+    def route(self, batch: PackedBatch, unscaled: bool = False) -> int:
+        """1 = fused single pass, 2 = forward+backward streaming, 3 = sequence-coupled,
+        4 = sequence-coupled in one pass with an unscaled gradient."""
+        cc = self.cfg.to_c()
+        if unscaled:
+            cc.flags |= N.TG_FLAG_UNSCALED_GRAD
+        return N.lib().tg_route(ctypes.byref(c_batch(batch)), ctypes.byref(cc))
 
     def __call__(self, batch: PackedBatch, dlogits: Union[str, torch.Tensor, None] = "new", *,
                  n_tok_global: int = 0, n_seq_global: int = 0, n_sft_seq_global: int = 0,
-                 out: Optional[LossOutput] = None, stream: Optional[torch.cuda.Stream] = None
-                 ) -> LossOutput:
+                 out: Optional[LossOutput] = None, stream: Optional[torch.cuda.Stream] = None,
+                 unscaled: bool = False) -> LossOutput:
+        """Loss, metrics and d loss / d logits of a packed batch.
+
+        ``unscaled=True`` (sequence-coupled losses only: OPMD_KIMI / OPMD_PAIRWISE
+        / DPO) reads the logits once instead of twice: ``out.dlogits`` holds
+        the unscaled ``p - e_y`` rows and ``out.row_scale`` the per-row factor,
+        d loss / d z_t = row_scale[t] * dlogits[t] -- for a caller that folds
+        the row scale into its LM-head backward."""
         L = N.lib()
         cb = c_batch(batch)
         cfg = self.cfg
         if cfg.coupled and cfg.policy_loss_fn == "dpo" and n_seq_global == 0:
             n_seq_global = batch.n_seqs
         cc = cfg.to_c(n_tok_global, n_seq_global, n_sft_seq_global)
+        if unscaled:
+            cc.flags |= N.TG_FLAG_UNSCALED_GRAD
         dev = batch.device
         T, B = batch.n_rows, batch.n_seqs
         if out is None:
@@ -196,6 +214,10 @@ class RFTLoss:
         co.lp, co.entropy, co.lse = out.lp.data_ptr(), out.entropy.data_ptr(), out.lse.data_ptr()
         co.seq_lp, co.seq_adv, co.stats = (out.seq_lp.data_ptr(), out.seq_adv.data_ptr(),
                                            out.stats.data_ptr())
+        if unscaled:
+            if out.row_coef is None or out.row_coef.shape != (3, T):
+                out.row_coef = torch.empty(3, T, dtype=torch.float32, device=dev)
+            co.row_coef = out.row_coef.data_ptr()
         nbytes = L.tg_workspace_size(ctypes.byref(cb), ctypes.byref(cc))
         ws = self._ws.get(dev, nbytes)
         s = stream if stream is not None else torch.cuda.current_stream(dev)
