@@ -1,0 +1,30 @@
+"""Throughput of the anchor-KL route (regularizer_g, algorithms.py:193-217:
+OPMD_SIMPLE + beta * anchor KL, route 2 = forward + backward streaming over the
+logits and the anchor logits, 10V bytes per row): 16,384 rows at V = 151,936.
+
+    python scripts/bench_anchor.py
+"""
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2505_17826_b200 import RFTLoss, RFTLossConfig, pack_arrays
+V=151936; T=16384; K=8; L=T//K
+z=(torch.randn(T,V,device='cuda')*2).to(torch.bfloat16)
+q=(z.float()+0.3*torch.randn(T,V,device='cuda')).to(torch.bfloat16)
+y=np.random.default_rng(0).integers(0,V,T)
+b=pack_arrays(z,y,[L]*K,[K],np.arange(K,dtype=np.float32)%2,anchor_logits=q)
+loss=RFTLoss(RFTLossConfig.from_variant("OPMD_SIMPLE",tau=1.0,beta=0.1))
+dz=torch.empty_like(z)
+for _ in range(3): loss(b,dlogits=dz)
+torch.cuda.synchronize()
+a,e=torch.cuda.Event(enable_timing=True),torch.cuda.Event(enable_timing=True)
+a.record()
+for _ in range(5): loss(b,dlogits=dz)
+e.record(); torch.cuda.synchronize()
+ms=a.elapsed_time(e)/5
+print(json.dumps({"route":loss.route(b),"rows":T,"ms":ms,"rows_per_s":T/ms*1e3,"GBs_10V":T*10*V/ms/1e6,"GBs_6V":T*6*V/ms/1e6}))
