@@ -303,7 +303,7 @@ int env_int(const char* name, int dflt) {
   return (v && *v) ? atoi(v) : dflt;
 }
 
-FusedPlan fused_plan(const TgBatch* b, const TgOut* o) {
+FusedPlan fused_plan(const TgBatch* b, const TgOut* o, bool anchor = false) {
   FusedPlan fp;
   // L2 look-ahead measured neutral at 1 row and harmful beyond (extra DRAM
   // reads from prefetched lines evicted before use): off by default
@@ -316,6 +316,12 @@ FusedPlan fused_plan(const TgBatch* b, const TgOut* o) {
   if (!aligned16(o->dlogits) || (o->ld_out * esz) % 16 != 0 || o->ld_out < b->vocab) return fp;
   const int64_t nvec = (b->vocab + epv - 1) / epv;
   if (b->ld < nvec * epv) return fp;  // TMA reads whole 16-byte vectors
+  if (anchor) {  // the anchor rows ride the same ring: bf16, aligned, whole vectors
+    if (b->dtype != TG_DTYPE_BF16 || !aligned16(b->anchor_logits) ||
+        (b->ld_anchor * esz) % 16 != 0 || b->ld_anchor < nvec * epv || b->row_index)
+      return fp;
+    if (env_int("TG_FUSED_ANCHOR", 1) == 0) return fp;
+  }
   const DevInfo d = dev_info();
   if (d.sms <= 0) return fp;
   const size_t tail = fused_smem_bytes(0);
@@ -326,9 +332,13 @@ FusedPlan fused_plan(const TgBatch* b, const TgOut* o) {
   for (int oi = 0; oi < 4; ++oi) {
     const int cl = kOrder[oi];
     if (force_cl ? cl != force_cl : cl == 3) continue;  // CL = 3 only on request
+    if (anchor && cl == 3) continue;
     const int64_t slice_vec = (nvec + cl - 1) / cl;
     const int64_t nchunk = (slice_vec * 16 + fused_chunk_bytes() - 1) / fused_chunk_bytes();
-    if (nchunk + 2 <= fused_resident_chunks()) {
+    // resident TMEM chunks: the slice + >= 2 prefix chunks (anchor: z and za
+    // chunk pairs, the slice + >= 1 prefix pair)
+    if (anchor ? 2 * (nchunk + 1) <= fused_resident_chunks()
+               : nchunk + 2 <= fused_resident_chunks()) {
       // persistent grid: as many clusters as can be co-resident, at most one per row
       int64_t clusters_max = fused_max_clusters(b->dtype, cl);
       if (clusters_max <= 0) clusters_max = d.sms / cl;
@@ -366,8 +376,12 @@ int route_of(const TgBatch* b, const TgConfig* c, const TgOut* o) {
     return 3;
   }
   if (c->flags & TG_FLAG_ROWS_GIVEN) return 2;
-  if (c->anchor_beta > 0) return 2;
   if (o && o->row_coef) return 2;  // the fused kernel keeps the coefficients on chip
+  if (c->anchor_beta > 0)  // fused anchor KL (6V) when the layout allows, else two-pass (10V)
+    return (o && o->dlogits && !(c->flags & (TG_FLAG_FORCE_TWO_PASS | TG_FLAG_NO_FUSED_TMA)) &&
+            fused_plan(b, o, true).cl != 0)
+               ? 1
+               : 2;
   if (c->flags & (TG_FLAG_FORCE_TWO_PASS | TG_FLAG_NO_FUSED_TMA)) return 2;
   if (!o || !o->dlogits) return 2;
   if (fused_plan(b, o).cl == 0) return 2;
@@ -490,7 +504,7 @@ int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspa
     launch_rowcoef(P, meta, true, false, cgrid, st);
     count_launches(1);
   } else if (route == 1) {
-    const FusedPlan fp = fused_plan(b, o);
+    const FusedPlan fp = fused_plan(b, o, anchor);
     // TG_FUSED_IMPL=l2: the L2-reread variant (tg_fused_l2.cu), for A/B
     const bool l2 = env_int("TG_FUSED_IMPL", 0) == 2;
     const int64_t l2_slots = int64_t(dev_info().sms) * (1024 / l2_threads());

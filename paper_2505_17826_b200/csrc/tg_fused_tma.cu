@@ -78,8 +78,9 @@ struct FusedSmemTail {
   uint64_t bbar[2];   // epilogue warp -> consumers: (a, h, lse, s) written
   float4 wpart[2][4 * kConsumerWarps];  // [rank * warps + warp]: every CTA's partials
   float4 bcast[2];  // (a, h, lse, s) of a row, from the epilogue warp
+  float wpart_q[2][4 * kConsumerWarps];  // kA: every CTA's anchor log-sum-exp partials
+  float bcast_ca[2];                     // kA: the row's anchor coefficient ca
   uint32_t tmem_base;  // TG_TMEM_STASH: 512 TMEM columns of this CTA
-  double stats[16];
 #ifdef TG_FUSED_PROF
   unsigned long long prof[16];
   unsigned long long post_first[2], post_last[2];
@@ -494,6 +495,261 @@ __device__ __forceinline__ Acc1 acc_init() {
   return acc;
 }
 
+// ---- fused anchor KL (regularizer_g, algorithms.py:193-217) -------------------
+// kA: the row's anchor logits za ride the same ring -- every logical chunk is a
+// z chunk followed by the za chunk of the same columns (two consecutive ring
+// slots, two consecutive TMEM stash slots) -- so each row costs 6V bytes
+// (z and za read once, dz written once) instead of the two-pass route's 10V.
+// Phase 1 adds Sigma p (z - za) (aligned with z's reference max) and the
+// anchor's own online sum; the epilogue forms lse_q and KL(p || q); phase 2
+// writes dz = p (a + hz z - ca za) - s [v = y] (k_bwd's formula).
+struct AccA {
+  Acc1 z;         // (m, nm2, s2, t2, fresh) of the logits
+  uint64_t u2;    // Sigma p (z - za), p = 2^((z - m) log2e)
+  float mq;       // anchor reference max (warp-uniform)
+  uint64_t nmq2;  // (-mq log2e, -mq log2e)
+  uint64_t sq2;   // Sigma 2^((za - mq) log2e)
+};
+
+__device__ __forceinline__ void acc_new_row_a(AccA& acc) {
+  acc.z.a.s2 = pk2(0.f, 0.f);
+  acc.z.a.t2 = pk2(0.f, 0.f);
+  acc.z.fresh = true;
+  acc.u2 = pk2(0.f, 0.f);
+  acc.sq2 = pk2(0.f, 0.f);
+}
+
+__device__ __forceinline__ AccA acc_init_a() {
+  AccA acc;
+  acc.z.a.m = 0.f;
+  acc.z.a.nm2 = pk2(0.f, 0.f);
+  acc.mq = 0.f;
+  acc.nmq2 = pk2(0.f, 0.f);
+  acc_new_row_a(acc);
+  return acc;
+}
+
+// z, za pairs of one vector pair: the sums of one chunk
+template <typename T>
+__device__ __forceinline__ void accumulate_a(const uint4& uz, const uint4& uq, uint64_t nm2,
+                                             uint64_t nmq2, uint64_t& s2, uint64_t& t2,
+                                             uint64_t& u2, uint64_t& sq2) {
+  const uint64_t l2e2 = pk2(kLog2e, kLog2e), neg2 = pk2(-1.f, -1.f);
+#pragma unroll
+  for (int w = 0; w < Vec<T>::N / 2; ++w) {
+    const uint64_t x = pair<T>(uz, w), xq = pair<T>(uq, w);
+    const uint64_t p = ex2x2(fma2(x, l2e2, nm2));
+    s2 = add2(s2, p);
+    t2 = fma2(p, x, t2);
+    u2 = fma2(p, fma2(xq, neg2, x), u2);
+    sq2 = add2(sq2, ex2x2(fma2(xq, l2e2, nmq2)));
+  }
+}
+
+template <typename T, bool kPartial, bool kMaskTail>
+__device__ __forceinline__ void phase1_chunk_a(AccA& acc, RingIt& it, const RingBase& rb,
+                                               int vbase, const Slice& sl, int tid) {
+  uint4 uz[kVecPerThread], uq[kVecPerThread];
+  bool valid[kVecPerThread];
+  RingIt iq = it;
+  iq.next();
+  wait_full(it.full(rb), it.phase());
+  const uint32_t az = it.addr(rb) + tid * 16;
+#pragma unroll
+  for (int g = 0; g < kVecPerThread; ++g) {
+    const int vec = vbase + g * kConsumers + tid;
+    valid[g] = !kPartial || vec < sl.v1;
+    uz[g] = valid[g] ? lds128(az + g * kConsumers * 16) : Pk<T>::neutral();
+  }
+  tmem_st16(stash_addr(rb, it.c), uz);
+  wait_full(iq.full(rb), iq.phase());
+  const uint32_t aq = iq.addr(rb) + tid * 16;
+#pragma unroll
+  for (int g = 0; g < kVecPerThread; ++g)
+    uq[g] = valid[g] ? lds128(aq + g * kConsumers * 16) : Pk<T>::neutral();
+  tmem_st16(stash_addr(rb, iq.c), uq);
+  __syncwarp();
+  if ((tid & 31) == 0) {
+    arrive_u32(it.empty(rb));
+    arrive_u32(iq.empty(rb));
+  }
+  it.advance(2);
+  if constexpr (kMaskTail) {
+#pragma unroll
+    for (int g = 0; g < kVecPerThread; ++g)
+      if (vbase + g * kConsumers + tid == sl.tail_vec) {
+        Pk<T>::mask_from(uz[g], sl.tail_valid);
+        Pk<T>::mask_from(uq[g], sl.tail_valid);
+      }
+  }
+  {  // speculative: the current reference maxima, accepted when the sums are safe
+    uint64_t s2 = pk2(0.f, 0.f), t2 = s2, u2 = s2, sq2 = s2;
+#pragma unroll
+    for (int g = 0; g < kVecPerThread; ++g)
+      accumulate_a<T>(uz[g], uq[g], acc.z.a.nm2, acc.nmq2, s2, t2, u2, sq2);
+    float a0, a1;
+    upk2(s2, a0, a1);
+    const float sc = a0 + a1;
+    upk2(t2, a0, a1);
+    const float tc = a0 + a1;
+    upk2(u2, a0, a1);
+    const float uc = a0 + a1;
+    upk2(sq2, a0, a1);
+    const float qc = a0 + a1;
+    bool ok = __all_sync(0xffffffffu, sc <= 4294967296.0f && qc <= 4294967296.0f &&
+                                          fabsf(tc) <= 3.0e38f && fabsf(uc) <= 3.0e38f);
+    if (ok && acc.z.fresh)
+      ok = warp_sum_f(sc) >= 9.5367431640625e-07f && warp_sum_f(qc) >= 9.5367431640625e-07f;
+    if (ok) {
+      acc.z.a.s2 = add2(acc.z.a.s2, s2);
+      acc.z.a.t2 = add2(acc.z.a.t2, t2);
+      acc.u2 = add2(acc.u2, u2);
+      acc.sq2 = add2(acc.sq2, sq2);
+      acc.z.fresh = false;
+      return;
+    }
+  }
+  // checked: clamp -inf, exact warp maxima, rescale, sums
+#pragma unroll
+  for (int g = 0; g < kVecPerThread; ++g) {
+    Pk<T>::clamp(uz[g]);
+    Pk<T>::clamp(uq[g]);
+  }
+  const float vmax = warp_max_f(group_max<T>(uz));
+  const float qmax = warp_max_f(group_max<T>(uq));
+  if (acc.z.fresh) {
+    acc.z.a.m = vmax;
+    acc.mq = qmax;
+  } else {
+    if (vmax > acc.z.a.m) {
+      const float f = ex2((acc.z.a.m - vmax) * kLog2e);
+      const uint64_t f2 = pk2(f, f);
+      acc.z.a.s2 = mul2(acc.z.a.s2, f2);
+      acc.z.a.t2 = mul2(acc.z.a.t2, f2);
+      acc.u2 = mul2(acc.u2, f2);
+      acc.z.a.m = vmax;
+    }
+    if (qmax > acc.mq) {
+      const float f = ex2((acc.mq - qmax) * kLog2e);
+      acc.sq2 = mul2(acc.sq2, pk2(f, f));
+      acc.mq = qmax;
+    }
+  }
+  const float nmL = -acc.z.a.m * kLog2e, nqL = -acc.mq * kLog2e;
+  acc.z.a.nm2 = pk2(nmL, nmL);
+  acc.nmq2 = pk2(nqL, nqL);
+#pragma unroll
+  for (int g = 0; g < kVecPerThread; ++g)
+    if (!kPartial || valid[g])
+      accumulate_a<T>(uz[g], uq[g], acc.z.a.nm2, acc.nmq2, acc.z.a.s2, acc.z.a.t2, acc.u2,
+                      acc.sq2);
+  acc.z.fresh = false;
+}
+
+// logical chunks [c0, c1) of a row whose first ring position is `row_it`
+template <typename T>
+__device__ __forceinline__ void phase1_range_a(AccA& acc, RingIt row_it, const RingBase& rb,
+                                               const Slice& sl, int c0, int c1, int tid) {
+  RingIt it = row_it;
+  it.advance(2 * c0);
+  int vbase = sl.v0 + c0 * kVecPerChunk;
+  for (int c = c0; c < c1; ++c) {
+    const int vend = vbase + kVecPerChunk;
+    const bool has_tail = sl.tail_vec >= vbase && sl.tail_vec < vend;
+    if (vend <= sl.v1 && !has_tail)
+      phase1_chunk_a<T, false, false>(acc, it, rb, vbase, sl, tid);
+    else if (!has_tail)
+      phase1_chunk_a<T, true, false>(acc, it, rb, vbase, sl, tid);
+    else
+      phase1_chunk_a<T, true, true>(acc, it, rb, vbase, sl, tid);
+    vbase = vend;
+  }
+}
+
+// the warp's (m, Sigma s, Sigma t, Sigma u) and the anchor's log-sum-exp
+__device__ __forceinline__ float4 warp_partial_a(const AccA& acc, float& lq) {
+  float s0, s1;
+  upk2(acc.z.a.s2, s0, s1);
+  float s = s0 + s1;
+  upk2(acc.z.a.t2, s0, s1);
+  float t = s0 + s1;
+  upk2(acc.u2, s0, s1);
+  float u = s0 + s1;
+  upk2(acc.sq2, s0, s1);
+  float q = s0 + s1;
+  s = warp_sum_f(s);
+  t = warp_sum_f(t);
+  u = warp_sum_f(u);
+  q = warp_sum_f(q);
+  lq = q > 0.f ? acc.mq + logf(q) : kNegInf;
+  return make_float4(s > 0.f ? acc.z.a.m : kNegInf, s, t, u);
+}
+
+// phase 2 of one logical chunk: z and za from the two stash slots
+template <typename T, bool kCheck>
+__device__ __forceinline__ void phase2_chunk_a(const RingIt& it, const RingBase& rb, int vbase,
+                                               const Slice& sl, char* dzrow, int vy, int ye,
+                                               float s_t, uint64_t nl2, uint64_t av2,
+                                               uint64_t hz2, uint64_t nca2, int tid) {
+  constexpr int EPV = Vec<T>::N;
+  char* dst = dzrow + int64_t(vbase + tid) * 16;
+  uint4 sz[kVecPerThread], sq[kVecPerThread];
+  tmem_ld16(stash_addr(rb, it.c), sz);
+  tmem_ld16(stash_addr(rb, it.c + 1u), sq);
+  const uint64_t l2e2 = pk2(kLog2e, kLog2e);
+#pragma unroll
+  for (int g = 0; g < kVecPerThread; ++g) {
+    const int vec = vbase + g * kConsumers + tid;
+    if (!kCheck || vec < sl.v1) {
+      uint4 uz = sz[g], uq = sq[g];
+      Pk<T>::clamp(uz);
+      Pk<T>::clamp(uq);
+      float d[EPV];
+#pragma unroll
+      for (int w = 0; w < EPV / 2; ++w) {
+        const uint64_t x = pair<T>(uz, w), xq = pair<T>(uq, w);
+        const uint64_t p = ex2x2(fma2(x, l2e2, nl2));
+        const uint64_t c = fma2(nca2, xq, fma2(hz2, x, av2));
+        upk2(mul2(p, c), d[2 * w], d[2 * w + 1]);
+      }
+      bool done = false;
+      if (kCheck) {
+        if (vec == vy) {
+#pragma unroll
+          for (int e = 0; e < EPV; ++e)
+            if (e == ye) d[e] -= s_t;
+        }
+        if (vec == sl.tail_vec) {
+#pragma unroll
+          for (int e = 0; e < EPV; ++e)
+            if (e < sl.tail_valid) Vec<T>::store1(dzrow, int64_t(vec) * EPV + e, d[e]);
+          done = true;
+        }
+      }
+      if (!done) st_stream(dst + g * kConsumers * 16, Vec<T>::pack(d));
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void phase2_row_a(const Slice& sl, RingIt it, const RingBase& rb,
+                                             char* dzrow, int vy, int ye, float s_t,
+                                             uint64_t nl2, uint64_t av2, uint64_t hz2,
+                                             uint64_t nca2, int tid) {
+  int vbase = sl.v0;
+  for (int j = 0; j < sl.nchunk; ++j) {
+    const int vend = vbase + kVecPerChunk;
+    const bool check = (vend > sl.v1) || (sl.tail_vec >= vbase && sl.tail_vec < vend) ||
+                       (vy >= vbase && vy < vend);
+    if (check)
+      phase2_chunk_a<T, true>(it, rb, vbase, sl, dzrow, vy, ye, s_t, nl2, av2, hz2, nca2, tid);
+    else
+      phase2_chunk_a<T, false>(it, rb, vbase, sl, dzrow, vy, ye, s_t, nl2, av2, hz2, nca2, tid);
+    it.advance(2);
+    vbase = vend;
+  }
+}
+
 // waits of the producer / epilogue warps back off with nanosleep so their
 // polling does not steal issue slots from the consumer warps on the same SMSP
 // Back-off (ns) of the producer's slot waits, the epilogue's partial waits and
@@ -521,9 +777,76 @@ __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
   }
 }
 
+// Consumer warps of the fused anchor path: the same row loop as the default
+// consumers (first row's prefix, phase 1, partial post to every CTA of the
+// cluster, next row's prefix, phase 2), over chunk pairs.
 template <typename T, int CL>
+__device__ __forceinline__ void consumer_rows_a(const KParams& P, FusedSmemTail* tail,
+                                                const RingBase& rb, const Slice& sl, int pre,
+                                                int64_t cid, int64_t ncl, uint32_t rank,
+                                                int warp, int lane, int tid) {
+  constexpr int EPV = Vec<T>::N;
+  constexpr int ESZ = elem_bytes<T>();
+  const int64_t NR = P.n_rows;
+  const int V = int(P.vocab);
+  RingIt pos0 = {0u};
+  AccA acc = acc_init_a();
+  int vtid = tid;
+  if constexpr (kConsumerWarps == 16) {  // sub-partitions 2 / 3 first (see the default path)
+    const int q = warp & 3, grp = warp >> 2;
+    const int vw = (q >= 2) ? (grp * 2 + (q - 2)) : (8 + grp * 2 + q);
+    vtid = vw * 32 + lane;
+  }
+  if (cid < NR) phase1_range_a<T>(acc, pos0, rb, sl, 0, pre, vtid);
+  int64_t k = 0;
+  for (int64_t row = cid; row < NR; row += ncl, ++k) {
+    const int64_t nrow = row + ncl;
+    const int y = __ldg(&P.target[row]);
+    const int vy = (y >= 0 && y < V) ? (y / EPV) : -1;
+    const int ye = (vy >= 0) ? y - vy * EPV : 0;
+    const int par = int(k & 1);
+    phase1_range_a<T>(acc, pos0, rb, sl, pre, sl.nchunk, vtid);
+    float lq;
+    const float4 o = warp_partial_a(acc, lq);
+    if (lane == 0) {
+      const int slot = int(rank) * kConsumerWarps + warp;
+      tail->wpart[par][slot] = o;
+      tail->wpart_q[par][slot] = lq;
+      if constexpr (CL > 1) {
+        const uint32_t la = smem_u32(&tail->wpart[par][slot]);
+        const uint32_t lqa = smem_u32(&tail->wpart_q[par][slot]);
+        const uint32_t lb = smem_u32(&tail->pbar[par]);
+#pragma unroll
+        for (int r = 0; r < CL; ++r)
+          if (r != int(rank)) {
+            st_async_v4(map_to_rank(la, r), o.x, o.y, o.z, o.w, map_to_rank(lb, r));
+            st_async_f32(map_to_rank(lqa, r), lq, map_to_rank(lb, r));
+          }
+      }
+      arrive_u32(smem_u32(&tail->pbar[par]));
+    }
+    RingIt npos = pos0;
+    npos.advance(2 * sl.nchunk);
+    acc_new_row_a(acc);
+    if (nrow < NR) phase1_range_a<T>(acc, npos, rb, sl, 0, pre, vtid);
+    mbar_wait_u32<TG_SLEEP_BCAST>(smem_u32(&tail->bbar[par]), uint32_t((k >> 1) & 1));
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    const float4 bc = tail->bcast[par];
+    const float ca = tail->bcast_ca[par];
+    const float lseL = bc.z * kLog2e;
+    const uint64_t nl2 = pk2(-lseL, -lseL), av2 = pk2(bc.x, bc.x), hz2 = pk2(bc.y, bc.y);
+    const uint64_t nca2 = pk2(-ca, -ca);
+    char* dzrow = reinterpret_cast<char*>(P.dz) + row * P.ld_out * ESZ;
+    phase2_row_a<T>(sl, pos0, rb, dzrow, vy, ye, bc.w, nl2, av2, hz2, nca2, vtid);
+    pos0 = npos;
+  }
+}
+
+template <typename T, int CL, bool kA = false>
 __global__ void __launch_bounds__(kFusedThreads, 1)
     k_fused_tma(const KParams P, const RowMeta* __restrict__ meta, int prefetch_rows) {
+  static_assert(!kA || kStash, "the fused anchor path keeps z and za in the TMEM stash");
+  constexpr int kRing = kA ? 2 : 1;  // ring slots per logical chunk (z [, za])
   constexpr int EPV = Vec<T>::N;  // elements per 16-byte vector
   constexpr int ESZ = elem_bytes<T>();
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -549,7 +872,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   sl.tail_vec = (V % EPV) ? nvec - 1 : -1;  // global vector holding columns >= V
   sl.tail_valid = V - (nvec - 1) * EPV;
   // next-row phase-1 chunks that fit in the ring beside this row's slice
-  const int pre = min(min(kMaxPrefixChunks, (kStash ? kTSlots : kSlots) - sl.nchunk), sl.nchunk);
+  const int pre =
+      min(min(kMaxPrefixChunks, (kStash ? kTSlots : kSlots) / kRing - sl.nchunk), sl.nchunk);
 
   if (tid == 0) {
     for (int i = 0; i < kSlots; ++i) {
@@ -629,6 +953,22 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
               "l"(src + off), "r"(bytes), "r"(it.full(rb)), "l"(pol)
               : "memory");
           it.next();
+          if constexpr (kA) {  // the same columns of the anchor row, into the next slot
+            const char* qsrc = reinterpret_cast<const char*>(P.anchor) +
+                               row * P.ld_anchor * ESZ + int64_t(sl.v0) * 16;
+            mbar_wait_u32<TG_SLEEP_PROD>(it.empty(rb), it.phase() ^ 1u);
+            asm volatile(
+                "mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                    it.full(rb)),
+                "r"(bytes)
+                : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+                " [%0], [%1], %2, [%3], %4;" ::"r"(it.addr(rb)),
+                "l"(qsrc + off), "r"(bytes), "r"(it.full(rb)), "l"(pol)
+                : "memory");
+            it.next();
+          }
         }
       }
     }
@@ -641,6 +981,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     double sd[15];
 #pragma unroll
     for (int i = 0; i < 15; ++i) sd[i] = 0.0;
+    double sd_a[2] = {0.0, 0.0};  // kA: anchor loss, Sigma KL(p || q)
     // the row's metadata and target logit are fetched one row ahead (after the
     // previous row's broadcast), so their dependent loads stay off the path
     int seq_cur = (lane == 0 && cid < NR) ? seq_of_row(P, cid) : 0;
@@ -663,7 +1004,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       const float tzy = nzy;
       if (lane == 0) {
         if constexpr (CL > 1)
-          mbar_arrive_expect_tx(&tail->pbar[par], (CL - 1) * kConsumerWarps * 16);
+          mbar_arrive_expect_tx(&tail->pbar[par], (CL - 1) * kConsumerWarps * (kA ? 20 : 16));
       }
       {
         TG_PROF_T0();
@@ -698,10 +1039,29 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         }
       }
       const Online tot = warp_merge_first<(NP < 32 ? NP : 32)>(acc_p);
+      // kA: Sigma p (z - za) merges with the same scale factors as Sigma p z, the
+      // anchor's per-warp log-sum-exps as a log-sum-exp
+      Online tot_u = {kNegInf, 0.f, 0.f}, tot_q = {kNegInf, 0.f, 0.f};
+      if constexpr (kA) {
+        Online acc_u = {kNegInf, 0.f, 0.f}, acc_q = {kNegInf, 0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < (NP + 31) / 32; ++i) {
+          const int j = lane + 32 * i;
+          if (j < NP) {
+            const float4 v = tail->wpart[par][j];
+            acc_u = online_merge(acc_u, Online{v.x, v.y, v.w});
+            const float lq = tail->wpart_q[par][j];
+            acc_q = online_merge(acc_q, Online{lq, lq > kNegInf ? 1.f : 0.f, 0.f});
+          }
+        }
+        tot_u = warp_merge_first<(NP < 32 ? NP : 32)>(acc_u);
+        tot_q = warp_merge_first<(NP < 32 ? NP : 32)>(acc_q);
+      }
       if (lane == 0) {
         // fast log / divide on the critical path; full precision when the row's
-        // lp feeds sequence sums that couple the gradient (route 4), as in k_fwd_tma
-        const bool precise = (P.flags & TG_FLAG_UNSCALED_GRAD) != 0;
+        // lp feeds sequence sums that couple the gradient (route 4) or the
+        // anchor KL takes a difference of log-sum-exps, as in k_fwd / k_fwd_tma
+        const bool precise = kA || (P.flags & TG_FLAG_UNSCALED_GRAD) != 0;
         const float lse = tot.m + (precise ? logf(tot.s) : __logf(tot.s));
         const float H = lse - (precise ? tot.t / tot.s : __fdividef(tot.t, tot.s));
         const bool bad_target = (cur.flags & 2u) != 0;
@@ -716,7 +1076,15 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
           o.s = 0.f;
           o.h = 0.f;
         }
-        tail->bcast[par] = make_float4(o.s + o.h * (H - lse), o.h, lse, o.s);
+        float ca = 0.f, akl = 0.f, a_anchor = 0.f;
+        if constexpr (kA) {  // k_rowcoef's anchor terms: KL(p || q) = Sigma p (z - za) - lse + lse_q
+          const float lseq = tot_q.m + logf(tot_q.s);
+          akl = tot_u.t / tot_u.s - lse + lseq;
+          ca = bad_target ? 0.f : cur.ca;
+          a_anchor = ca * (lse - lseq + akl);
+          tail->bcast_ca[par] = ca;
+        }
+        tail->bcast[par] = make_float4(o.s + o.h * (H - lse) - a_anchor, o.h + ca, lse, o.s);
         arrive_u32(smem_u32(&tail->bbar[par]));
         if (row + ncl < NR) fetch(row + ncl);
 #ifdef TG_FUSED_PROF
@@ -728,7 +1096,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
           P.ent[row] = H;
           P.lse[row] = lse;
           const bool nonfin = !(finite_f(lse) && finite_f(lp) && finite_f(H) && finite_f(o.s) &&
-                                finite_f(o.h));
+                                finite_f(o.h) && finite_f(a_anchor));
+          if constexpr (kA) {
+            sd_a[0] += double(ca) * double(akl);
+            sd_a[1] += akl;
+          }
           sd[0] += o.l_pg;
           sd[1] += o.l_kl;
           sd[2] += o.l_ent;
@@ -768,7 +1140,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       dst[TG_S_N_TOK_RL] = sd[12];
       dst[TG_S_INVALID] = sd[13];
       dst[TG_S_N_TOK] = sd[14];
+      dst[TG_S_ANCHOR_LOSS] = sd_a[0];
+      dst[TG_S_SUM_ANCHOR_KL] = sd_a[1];
     }
+  } else if (kA && warp < kConsumerWarps) {
+    consumer_rows_a<T, CL>(P, tail, rb, sl, pre, cid, ncl, rank, warp, lane, tid);
   } else if (warp < kConsumerWarps) {
     // ===================== consumer warps =====================
     RingIt pos0 = {0u};  // the current row's first chunk
@@ -1049,11 +1425,11 @@ cudaError_t launch_fwd_tma(const KParams& P, int n_sms, cudaStream_t stream) {
 
 size_t fused_smem_bytes(int n_slots) { return size_t(n_slots) * kChunk + sizeof(FusedSmemTail); }
 
-template <typename T, int CL>
+template <typename T, int CL, bool kA = false>
 static cudaError_t launch_fused_t(const KParams& P, const RowMeta* meta, int n_ctas,
                                   int prefetch_rows, cudaStream_t stream) {
   const size_t smem = fused_smem_bytes(kSlots);
-  cudaError_t e = cudaFuncSetAttribute(k_fused_tma<T, CL>,
+  cudaError_t e = cudaFuncSetAttribute(k_fused_tma<T, CL, kA>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -1068,13 +1444,20 @@ static cudaError_t launch_fused_t(const KParams& P, const RowMeta* meta, int n_c
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_fused_tma<T, CL>, P, meta, prefetch_rows);
+  return cudaLaunchKernelEx(&cfg, k_fused_tma<T, CL, kA>, P, meta, prefetch_rows);
 }
 
 cudaError_t launch_fused(const KParams& P, const void* meta, int cl, int n_slots, int n_ctas,
                          int prefetch_rows, cudaStream_t stream) {
   if (n_slots != kSlots) return cudaErrorInvalidValue;
   const RowMeta* m = reinterpret_cast<const RowMeta*>(meta);
+  if (P.anchor && P.anchor_beta > 0.f) {  // fused anchor KL: bf16 only (fused_anchor_plan)
+    if (P.dtype != TG_DTYPE_BF16) return cudaErrorInvalidValue;
+    if (cl == 1) return launch_fused_t<bf16_t, 1, true>(P, m, n_ctas, prefetch_rows, stream);
+    if (cl == 2) return launch_fused_t<bf16_t, 2, true>(P, m, n_ctas, prefetch_rows, stream);
+    if (cl == 4) return launch_fused_t<bf16_t, 4, true>(P, m, n_ctas, prefetch_rows, stream);
+    return cudaErrorInvalidValue;
+  }
   if (P.dtype == TG_DTYPE_BF16) {
     if (cl == 1) return launch_fused_t<bf16_t, 1>(P, m, n_ctas, prefetch_rows, stream);
     if (cl == 2) return launch_fused_t<bf16_t, 2>(P, m, n_ctas, prefetch_rows, stream);

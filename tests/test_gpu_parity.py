@@ -152,6 +152,48 @@ def test_anchor_kl_regularizer(dtype):
     compare(out, ref, dtype)
 
 
+@pytest.mark.parametrize("shape,case_kw", [
+    ("v1000", {}), ("v32000", {}), ("v151936", {}), ("v1000", dict(ld=1008)),
+], ids=["v1000", "v32000", "v151936", "v1000_tail_vector"])
+def test_fused_anchor_kl_route_matches_oracle(shape, case_kw):
+    """regularizer_g in one pass (route 1 with the anchor rows on the fused
+    kernel's ring, 6V bytes per row) against the oracle; forced two-pass
+    (10V) on the same inputs agrees too."""
+    if shape == "v1000" and "ld" in case_kw:
+        V, lens, gs = 1001, SHAPES["v1000"][1], SHAPES["v1000"][2]
+    else:
+        V, lens, gs = SHAPES[shape]
+    cfg = RFTLossConfig.from_variant("OPMD_SIMPLE", tau=0.4, beta=0.9)
+    batch, packed = make_case(3, V, lens, gs, dtype=torch.bfloat16, anchor=True, **case_kw)
+    assert RFTLoss(cfg).route(packed) == 1
+    out = RFTLoss(cfg)(packed, dlogits="new")
+    ref = O.general_loss(batch, oracle_cfg(cfg))
+    compare(out, ref, torch.bfloat16)
+    two = RFTLoss(cfg.with_(force_two_pass=True))(packed, dlogits="new")
+    a, b = out.stats_dict(), two.stats_dict()
+    assert a["anchor_loss"] == pytest.approx(b["anchor_loss"], rel=1e-4, abs=1e-6)
+    assert a["sum_anchor_kl"] == pytest.approx(b["sum_anchor_kl"], rel=1e-4, abs=1e-5)
+
+
+def test_fused_anchor_kl_with_masked_vocabulary_matches_two_pass():
+    """-inf logits (masked vocabulary, in both the policy and the anchor rows)
+    take the fused anchor path's checked branch; the oracle cannot evaluate
+    KL(p || q) there (inf - inf), so the two-pass route -- which clamps -inf
+    the same way -- is the reference."""
+    V, lens, gs = SHAPES["v32000"]
+    cfg = RFTLossConfig.from_variant("OPMD_SIMPLE", tau=0.4, beta=0.9)
+    _, packed = make_case(4, V, lens, gs, dtype=torch.bfloat16, anchor=True, neg_inf=0.02)
+    assert RFTLoss(cfg).route(packed) == 1
+    out = RFTLoss(cfg)(packed, dlogits="new")
+    two = RFTLoss(cfg.with_(force_two_pass=True))(packed, dlogits="new")
+    a, b = out.stats_dict(), two.stats_dict()
+    assert a["nonfinite"] == 0
+    for k in ("loss", "anchor_loss", "sum_anchor_kl", "sum_lp", "sum_entropy"):
+        assert a[k] == pytest.approx(b[k], rel=1e-4, abs=1e-5), k
+    d, r = out.dlogits.float(), two.dlogits.float()
+    assert bool(((d - r).abs() <= 2.0 ** -8 * float(r.abs().max()) + 1e-2 * r.abs()).all())
+
+
 def test_mixed_rl_sft_batch():
     cfg = RFTLossConfig(advantage_fn="grpo", policy_loss_fn="ppo_clip",
                         loss_agg_mode="token-mean", sft_weight=0.5)
