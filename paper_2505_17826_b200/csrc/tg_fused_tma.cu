@@ -84,9 +84,13 @@ struct FusedSmemTail {
 #ifdef TG_FUSED_PROF
   unsigned long long prof[16];
   unsigned long long post_first[2], post_last[2];
-  unsigned long long post_t[2][kConsumerWarps];
+  uint32_t post_t[2][kConsumerWarps];  // low 32 bits of clock64 (differences within a row)
 #endif
 };
+
+// the ring + tail must fit the 227 KB per-CTA opt-in shared memory of sm_100
+static_assert(size_t(kSlots) * kChunk + sizeof(FusedSmemTail) <= 232448,
+              "fused kernel shared memory exceeds 227 KB");
 
 // ---- optional cycle accounting (profiling build only: -DTG_FUSED_PROF) -------
 // prof[0] consumer cycles waiting for ring data (summed over consumer warps)
@@ -495,6 +499,98 @@ __device__ __forceinline__ Acc1 acc_init() {
   return acc;
 }
 
+// ---- the epilogue's merge of the CL x warps row partials ----------------------
+// REDUX form: one warp max of the partials' reference maxima, each partial
+// scaled once, then plain butterfly sums -- a short dependency chain instead of
+// log2(NP) levels of online merges.  Measured: +10.5 % for the fused anchor
+// path at CL = 4 (64 partials, three merges: critical path 5.1k -> 3.9k cycles
+// per row), but -0.4 % (headline, CL = 2) and -2.3 % (CL = 1) for one merge of
+// <= 32 partials, so it is used only for the former.
+#ifndef TG_MERGE_REDUX
+#define TG_MERGE_REDUX 1
+#endif
+template <int NP, bool kU>
+__device__ __forceinline__ float4 merge_partials(const float4* wp, int lane) {
+  constexpr int K = (NP + 31) / 32;
+  float4 v[K];
+  float mloc = kNegInf;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    const int j = lane + 32 * i;
+    v[i] = j < NP ? wp[j] : make_float4(kNegInf, 0.f, 0.f, 0.f);
+    mloc = fmaxf(mloc, v[i].x);
+  }
+  const float M = warp_max_f(mloc);
+  float S = 0.f, Tt = 0.f, U = 0.f;
+  if (M != kNegInf) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const float f = v[i].x == kNegInf ? 0.f : ex2((v[i].x - M) * kLog2e);
+      S = fmaf(v[i].y, f, S);
+      Tt = fmaf(v[i].z, f, Tt);
+      if (kU) U = fmaf(v[i].w, f, U);
+    }
+  }
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) {
+    S += __shfl_xor_sync(0xffffffffu, S, d);
+    Tt += __shfl_xor_sync(0xffffffffu, Tt, d);
+    if (kU) U += __shfl_xor_sync(0xffffffffu, U, d);
+  }
+  return make_float4(M, S, Tt, U);
+}
+
+// the previous form: online merges (kept for A/B: -DTG_MERGE_REDUX=0)
+template <int NP, bool kU>
+__device__ __forceinline__ float4 merge_partials_online(const float4* wp, int lane) {
+  Online a = {kNegInf, 0.f, 0.f}, b = {kNegInf, 0.f, 0.f};
+#pragma unroll
+  for (int i = 0; i < (NP + 31) / 32; ++i) {
+    const int j = lane + 32 * i;
+    if (j < NP) {
+      const float4 v = wp[j];
+      a = online_merge(a, Online{v.x, v.y, v.z});
+      if (kU) b = online_merge(b, Online{v.x, v.y, v.w});
+    }
+  }
+  a = warp_merge_first<(NP < 32 ? NP : 32)>(a);
+  if (kU) b = warp_merge_first<(NP < 32 ? NP : 32)>(b);
+  return make_float4(a.m, a.s, a.t, b.t);
+}
+
+// log-sum-exp of NP per-warp log-sum-exps by online merges (lane 0 gets it)
+template <int NP>
+__device__ __forceinline__ float merge_lse_online(const float* lq, int lane) {
+  Online q = {kNegInf, 0.f, 0.f};
+#pragma unroll
+  for (int i = 0; i < (NP + 31) / 32; ++i) {
+    const int j = lane + 32 * i;
+    if (j < NP) q = online_merge(q, Online{lq[j], lq[j] > kNegInf ? 1.f : 0.f, 0.f});
+  }
+  q = warp_merge_first<(NP < 32 ? NP : 32)>(q);
+  return q.m + logf(q.s);
+}
+
+// log-sum-exp of NP per-warp log-sum-exps (all lanes get it)
+template <int NP>
+__device__ __forceinline__ float merge_lse(const float* lq, int lane) {
+  constexpr int K = (NP + 31) / 32;
+  float v[K];
+  float mloc = kNegInf;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    const int j = lane + 32 * i;
+    v[i] = j < NP ? lq[j] : kNegInf;
+    mloc = fmaxf(mloc, v[i]);
+  }
+  const float M = warp_max_f(mloc);
+  if (M == kNegInf) return kNegInf;
+  float S = 0.f;
+#pragma unroll
+  for (int i = 0; i < K; ++i) S += v[i] == kNegInf ? 0.f : ex2((v[i] - M) * kLog2e);
+  return M + logf(warp_sum_f(S));
+}
+
 // ---- fused anchor KL (regularizer_g, algorithms.py:193-217) -------------------
 // kA: the row's anchor logits za ride the same ring -- every logical chunk is a
 // z chunk followed by the za chunk of the same columns (two consecutive ring
@@ -553,7 +649,11 @@ __device__ __forceinline__ void phase1_chunk_a(AccA& acc, RingIt& it, const Ring
   bool valid[kVecPerThread];
   RingIt iq = it;
   iq.next();
-  wait_full(it.full(rb), it.phase());
+  {
+    TG_PROF_T0();
+    wait_full(it.full(rb), it.phase());
+    TG_PROF_ADD(prof_tail(), 0);
+  }
   const uint32_t az = it.addr(rb) + tid * 16;
 #pragma unroll
   for (int g = 0; g < kVecPerThread; ++g) {
@@ -789,6 +889,9 @@ __device__ __forceinline__ void consumer_rows_a(const KParams& P, FusedSmemTail*
   constexpr int ESZ = elem_bytes<T>();
   const int64_t NR = P.n_rows;
   const int V = int(P.vocab);
+#ifdef TG_FUSED_PROF
+  const long long t_start = clock64();
+#endif
   RingIt pos0 = {0u};
   AccA acc = acc_init_a();
   int vtid = tid;
@@ -829,7 +932,11 @@ __device__ __forceinline__ void consumer_rows_a(const KParams& P, FusedSmemTail*
     npos.advance(2 * sl.nchunk);
     acc_new_row_a(acc);
     if (nrow < NR) phase1_range_a<T>(acc, npos, rb, sl, 0, pre, vtid);
-    mbar_wait_u32<TG_SLEEP_BCAST>(smem_u32(&tail->bbar[par]), uint32_t((k >> 1) & 1));
+    {
+      TG_PROF_T0();
+      mbar_wait_u32<TG_SLEEP_BCAST>(smem_u32(&tail->bbar[par]), uint32_t((k >> 1) & 1));
+      TG_PROF_ADD(tail, 1);
+    }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     const float4 bc = tail->bcast[par];
     const float ca = tail->bcast_ca[par];
@@ -839,7 +946,13 @@ __device__ __forceinline__ void consumer_rows_a(const KParams& P, FusedSmemTail*
     char* dzrow = reinterpret_cast<char*>(P.dz) + row * P.ld_out * ESZ;
     phase2_row_a<T>(sl, pos0, rb, dzrow, vy, ye, bc.w, nl2, av2, hz2, nca2, vtid);
     pos0 = npos;
+#ifdef TG_FUSED_PROF
+    if (tid == 0) tail->prof[6] += 1;
+#endif
   }
+#ifdef TG_FUSED_PROF
+  if (tid == 0) tail->prof[2] = (unsigned long long)(clock64() - t_start);
+#endif
 }
 
 template <typename T, int CL, bool kA = false>
@@ -1021,7 +1134,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         tail->prof[9] += (unsigned long long)t_crit - tail->post_first[par];
         tail->prof[10] += tail->post_last[par] - tail->post_first[par];
         for (int w = 0; w < kConsumerWarps; ++w)
-          tail->prof[11 + (w & 3)] += tail->post_t[par][w] - tail->post_first[par];
+          tail->prof[11 + (w & 3)] += uint32_t(tail->post_t[par][w] - uint32_t(tail->post_first[par]));
         tail->post_first[par] = ~0ull;
         tail->post_last[par] = 0ull;
       }
@@ -1029,34 +1142,16 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       // all CL x warps partials, merged in a fixed lane order: lane 0 holds the
       // same bits on every CTA of the cluster
       constexpr int NP = CL * kConsumerWarps;
-      Online acc_p = {kNegInf, 0.f, 0.f};
-#pragma unroll
-      for (int i = 0; i < (NP + 31) / 32; ++i) {
-        const int j = lane + 32 * i;
-        if (j < NP) {
-          const float4 v = tail->wpart[par][j];
-          acc_p = online_merge(acc_p, Online{v.x, v.y, v.z});
-        }
-      }
-      const Online tot = warp_merge_first<(NP < 32 ? NP : 32)>(acc_p);
-      // kA: Sigma p (z - za) merges with the same scale factors as Sigma p z, the
-      // anchor's per-warp log-sum-exps as a log-sum-exp
-      Online tot_u = {kNegInf, 0.f, 0.f}, tot_q = {kNegInf, 0.f, 0.f};
-      if constexpr (kA) {
-        Online acc_u = {kNegInf, 0.f, 0.f}, acc_q = {kNegInf, 0.f, 0.f};
-#pragma unroll
-        for (int i = 0; i < (NP + 31) / 32; ++i) {
-          const int j = lane + 32 * i;
-          if (j < NP) {
-            const float4 v = tail->wpart[par][j];
-            acc_u = online_merge(acc_u, Online{v.x, v.y, v.w});
-            const float lq = tail->wpart_q[par][j];
-            acc_q = online_merge(acc_q, Online{lq, lq > kNegInf ? 1.f : 0.f, 0.f});
-          }
-        }
-        tot_u = warp_merge_first<(NP < 32 ? NP : 32)>(acc_u);
-        tot_q = warp_merge_first<(NP < 32 ? NP : 32)>(acc_q);
-      }
+      // (m, Sigma e, Sigma e z[, Sigma e (z - za)]) of the row; kA: the anchor's
+      // log-sum-exp from the per-warp ones
+      constexpr bool kRedux = TG_MERGE_REDUX && kA && NP > 32;
+      const float4 tot4 = kRedux ? merge_partials<NP, kA>(tail->wpart[par], lane)
+                                 : merge_partials_online<NP, kA>(tail->wpart[par], lane);
+      const Online tot = {tot4.x, tot4.y, tot4.z};
+      float lseq = 0.f;
+      if constexpr (kA)
+        lseq = kRedux ? merge_lse<NP>(tail->wpart_q[par], lane)
+                      : merge_lse_online<NP>(tail->wpart_q[par], lane);
       if (lane == 0) {
         // fast log / divide on the critical path; full precision when the row's
         // lp feeds sequence sums that couple the gradient (route 4) or the
@@ -1078,8 +1173,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         }
         float ca = 0.f, akl = 0.f, a_anchor = 0.f;
         if constexpr (kA) {  // k_rowcoef's anchor terms: KL(p || q) = Sigma p (z - za) - lse + lse_q
-          const float lseq = tot_q.m + logf(tot_q.s);
-          akl = tot_u.t / tot_u.s - lse + lseq;
+          akl = tot4.w / tot.s - lse + lseq;
           ca = bad_target ? 0.f : cur.ca;
           a_anchor = ca * (lse - lseq + akl);
           tail->bcast_ca[par] = ca;
@@ -1190,7 +1284,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         const unsigned long long tpost = clock64();
         atomicMin(&tail->post_first[par], tpost);
         atomicMax(&tail->post_last[par], tpost);
-        tail->post_t[par][warp] = tpost;
+        tail->post_t[par][warp] = uint32_t(tpost);
 #endif
         tail->wpart[par][slot] = make_float4(o.m, o.s, o.t, 0.f);
         if constexpr (CL > 1) {

@@ -2,7 +2,7 @@
 OPMD_SIMPLE + beta * anchor KL, route 2 = forward + backward streaming over the
 logits and the anchor logits, 10V bytes per row): 16,384 rows at V = 151,936.
 
-    python scripts/bench_anchor.py
+    python scripts/bench_anchor.py [V] [rows]
 """
 import json
 import sys
@@ -13,7 +13,10 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2505_17826_b200 import RFTLoss, RFTLossConfig, pack_arrays
-V=151936; T=16384; K=8; L=T//K
+V = int(sys.argv[1]) if len(sys.argv) > 1 else 151936
+T = int(sys.argv[2]) if len(sys.argv) > 2 else 16384
+K = 8
+L = T // K
 z=(torch.randn(T,V,device='cuda')*2).to(torch.bfloat16)
 q=(z.float()+0.3*torch.randn(T,V,device='cuda')).to(torch.bfloat16)
 y=np.random.default_rng(0).integers(0,V,T)
@@ -27,4 +30,13 @@ a.record()
 for _ in range(5): loss(b,dlogits=dz)
 e.record(); torch.cuda.synchronize()
 ms=a.elapsed_time(e)/5
+prof_out = __import__("os").environ.get("TG_FUSED_PROF_OUT")
+if prof_out:  # instrumented library (--variant=prof): per-CTA cycle counters
+    import ctypes
+    from paper_2505_17826_b200 import _native as N
+    L = N.lib()
+    buf = (ctypes.c_ulonglong * (1024 * 16))()
+    L.tg_debug_fused_prof(buf, 1024)
+    arr = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 16)
+    np.save(prof_out, arr[:int((arr[:, 6] > 0).sum()) or 1024])
 print(json.dumps({"route":loss.route(b),"rows":T,"ms":ms,"rows_per_s":T/ms*1e3,"GBs_10V":T*10*V/ms/1e6,"GBs_6V":T*6*V/ms/1e6}))
