@@ -32,6 +32,11 @@
 //    dz = p (s + h((z - lse) + H)) - s[v = y] with 128-bit streaming stores.
 //  * Persistent grid: one CTA per SM (18 warps), as many clusters as can be
 //    co-resident, striding over rows.
+//  * kA (anchor KL, regularizer_g): the anchor row's chunks ride the ring
+//    behind the logits' (chunk pairs), both stay in the TMEM stash, and the
+//    epilogue adds KL(p || q) -- 6V bytes per row instead of the two-pass 10V.
+//  * Route 4 (TG_FLAG_UNSCALED_GRAD): unit row coefficients, dz = p - e_y for
+//    the sequence-coupled losses; the per-row scale comes afterwards.
 //  * k_fwd_tma (below) is the forward-only sibling: same ring and phase 1,
 //    chunks released after phase 1, no resident rows, no cluster.
 #include "tg_common.cuh"
