@@ -43,6 +43,9 @@ def loss_paths():
             torch.cuda.synchronize()
             assert torch.equal(out.dlogits, b.logits), "in-place dlogits differ"
             out.metrics()
+            if loss.cfg.coupled:  # route 4: one pass, unscaled gradient + row scales
+                loss(pack_arrays(z.clone(), y, lens, groups, rew, old_lp=old, ref_lp=old),
+                     dlogits="new", unscaled=True).metrics()
         logprob_fwd(pack_arrays(z, y, lens, groups, rew))
     # anchor KL (regularizer_g)
     V = 4096
