@@ -74,7 +74,8 @@ VARIANT_WORKLOAD = {
 _BASE_LOSS = "grpo adv + ppo_clip(0.2,0.28) + low_var_kl(0.001) + token-mean"
 VARIANT_LOSS = {"grpo": _BASE_LOSS, "c1": _BASE_LOSS, "c3": _BASE_LOSS + " + entropy(0.001)",
                 "c4": _BASE_LOSS + " on RL seqs + SFT NLL (weight 1) on expert seqs",
-                "c5": _BASE_LOSS}
+                "c5": _BASE_LOSS,
+                "anchor": "opmd_simple(tau 1) + regularizer_g anchor KL (beta 0.1), fused (6V)"}
 
 
 def parse():
@@ -95,7 +96,7 @@ def parse():
     p.add_argument("--quiet", action="store_true")
     p.add_argument("--variant", default="grpo",
                    choices=["grpo", "grpo_two_pass", "opmd_kimi", "opmd_pairwise", "sft",
-                            "opmd_kimi_unscaled", "opmd_pairwise_unscaled",
+                            "opmd_kimi_unscaled", "opmd_pairwise_unscaled", "anchor",
                             "c1", "c3", "c4", "c5"],
                    help="loss variant (the headline metric is 'grpo' = configs[1]; c3 / c4 / c5 "
                         "are the per-GPU shards of BASELINE configs[2..4]; the others measure "
@@ -324,6 +325,8 @@ def main():
         cfg = RFTLossConfig(policy_loss_fn=args.variant.replace("_unscaled", ""), tau=1.0)
     elif args.variant == "sft":
         cfg = RFTLossConfig.from_variant("SFT")
+    elif args.variant == "anchor":  # regularizer_g: OPMD_SIMPLE + beta * KL(p || anchor)
+        cfg = RFTLossConfig.from_variant("OPMD_SIMPLE", tau=1.0, beta=0.1)
     elif args.variant == "c3":  # PPO clip + low_var_kl + entropy bonus
         cfg = cfg.with_(entropy_loss_fn="default", entropy_coef=0.001)
     elif args.variant == "c4":  # GRPO + SFT NLL on expert sequences in the same batch
@@ -332,7 +335,7 @@ def main():
     two_pass = args.variant in ("grpo_two_pass", "opmd_kimi", "opmd_pairwise")
     # coupled loss in one pass (TG_FLAG_UNSCALED_GRAD, route 4): p - e_y rows + row scales
     unscaled = args.variant.endswith("_unscaled")
-    algo_bytes_row = (6 * V + 24) if two_pass else ALGO_BYTES_PER_ROW
+    algo_bytes_row = (6 * V + 24) if (two_pass or args.variant == "anchor") else ALGO_BYTES_PER_ROW
 
     # ---- resident synthetic inputs (outside timing) ----
     gen = torch.Generator(device=dev)
@@ -345,6 +348,12 @@ def main():
     tgt_d = torch.as_tensor(tgt, device=dev)
     logits[torch.arange(mb_rows, device=dev), tgt_d] += BUMP
     dz = torch.empty_like(logits)
+    anchor = None
+    if args.variant == "anchor":  # the anchor policy's logits: the same rows + N(0, 0.3^2)
+        anchor = torch.empty_like(logits)
+        for r0 in range(0, mb_rows, 8192):
+            anchor[r0:r0 + 8192].normal_(0.0, 0.3, generator=gen)
+            anchor[r0:r0 + 8192] += logits[r0:r0 + 8192]
     lens = [Lr] * (mbg * K)
     gsz = [K] * mbg
     probe = pack_arrays(logits, tgt, lens, gsz, np.zeros(mbg * K, np.float32))
@@ -387,7 +396,7 @@ def main():
         old = (lp_true[rows] + rng.normal(0, OLD_LP_SIGMA, rows.size)).astype(np.float32)
         ref = (lp_true[rows] + rng.normal(0, 0.1, rows.size)).astype(np.float32)
         b = pack_arrays(logits, tgt[rows], lens_m, gsz, rew, old_lp=old, ref_lp=ref,
-                        seq_kind=kind, row_index=ridx)
+                        seq_kind=kind, row_index=ridx, anchor_logits=anchor)
         batches.append(b)
         outs.append(None)
         T += int(rows.size)
@@ -395,6 +404,7 @@ def main():
     route = loss.route(batches[0], unscaled=unscaled)
     assert route == (4 if unscaled else
                      1 if not two_pass else (2 if args.variant == "grpo_two_pass" else 3)), route
+    # (anchor: route 1 = the fused anchor path, 6V bytes per row)
     n_tok_g, n_seq_g, n_sft_g = world * T, world * B, world * n_sft
     stats_all = torch.zeros((n_mb, N.NSTAT), dtype=torch.float64, device=dev)
 
@@ -505,7 +515,8 @@ def main():
                        "parallelism": f"dp{world} (groups sharded by rank; stats allreduce)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_fused_tma" if not two_pass else "k_fwd..k_bwd (two-pass)",
+                         "kernel": ("k_fused_tma<anchor>" if args.variant == "anchor" else
+                                    "k_fused_tma" if not two_pass else "k_fwd..k_bwd (two-pass)"),
                          "kernel_ms": f_ms,
                          "algorithmic_bytes_per_launch": rows_per_launch * algo_bytes_row,
                          "peak_source": peak_src,
