@@ -169,6 +169,8 @@ def test_fused_anchor_kl_route_matches_oracle(shape, case_kw):
     out = RFTLoss(cfg)(packed, dlogits="new")
     ref = O.general_loss(batch, oracle_cfg(cfg))
     compare(out, ref, torch.bfloat16)
+    again = RFTLoss(cfg)(packed, dlogits="new")  # fixed-order reductions: bitwise rerun
+    assert torch.equal(again.stats, out.stats) and torch.equal(again.dlogits, out.dlogits)
     two = RFTLoss(cfg.with_(force_two_pass=True))(packed, dlogits="new")
     a, b = out.stats_dict(), two.stats_dict()
     assert a["anchor_loss"] == pytest.approx(b["anchor_loss"], rel=1e-4, abs=1e-6)
