@@ -318,7 +318,7 @@ FusedPlan fused_plan(const TgBatch* b, const TgOut* o, bool anchor = false) {
   if (b->ld < nvec * epv) return fp;  // TMA reads whole 16-byte vectors
   if (anchor) {  // the anchor rows ride the same ring: bf16, aligned, whole vectors
     if (b->dtype != TG_DTYPE_BF16 || !aligned16(b->anchor_logits) ||
-        (b->ld_anchor * esz) % 16 != 0 || b->ld_anchor < nvec * epv || b->row_index)
+        (b->ld_anchor * esz) % 16 != 0 || b->ld_anchor < nvec * epv)
       return fp;
     if (env_int("TG_FUSED_ANCHOR", 1) == 0) return fp;
   }
