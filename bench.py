@@ -26,8 +26,11 @@ copy / compute overlap).
 `--variant c1|c3|c4|c5` runs the per-GPU workloads of BASELINE configs[0],
 [2], [3], [4] (V = 32,000; PPO + k3 + entropy at 4,096 tokens; GRPO + SFT mix;
 ragged long-CoT through row_index); `grpo_two_pass`, `opmd_kimi`,
-`opmd_pairwise` measure the two-pass / sequence-coupled routes.  Kernel A/B:
-TG_LOSS_LIB selects a library build (scripts/gpu_libab.sh).
+`opmd_pairwise` measure the two-pass / sequence-coupled routes,
+`opmd_kimi_unscaled` / `opmd_pairwise_unscaled` the single-pass coupled route
+(unscaled gradient + per-row scales) and `anchor` the fused regularizer_g path
+(6V bytes per row).  Kernel A/B: TG_LOSS_LIB selects a library build
+(scripts/gpu_libab.sh).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--variant V]
