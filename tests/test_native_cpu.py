@@ -50,6 +50,8 @@ int main(void) {
   printf("%zu %zu %zu %zu %zu %zu\n", sizeof(TgConfig), sizeof(TgBatch), sizeof(TgOut),
          offsetof(TgBatch, seq_kind), offsetof(TgConfig, n_sft_seq_global), offsetof(TgOut, stats));
   printf("%d %d %d\n", TG_NSTAT, TG_S_INVALID, TG_S_SUM_ANCHOR_KL);
+  printf("%zu %d %d %d %d\n", offsetof(TgOut, row_coef), TG_FLAG_FORCE_TWO_PASS,
+         TG_FLAG_ROWS_GIVEN, TG_FLAG_UNSCALED_GRAD, TG_ABI_VERSION);
   return 0;
 }'''
     with tempfile.TemporaryDirectory() as d:
@@ -69,6 +71,10 @@ int main(void) {
     assert sizes[7] == N.STAT["invalid"] == O.STAT["invalid"]
     assert sizes[8] == N.STAT["sum_anchor_kl"]
     assert N.STAT_NAMES == O.STAT_NAMES
+    assert sizes[9] == N.TgOut.row_coef.offset
+    assert (sizes[10], sizes[11], sizes[12]) == (N.TG_FLAG_FORCE_TWO_PASS, N.TG_FLAG_ROWS_GIVEN,
+                                                 N.TG_FLAG_UNSCALED_GRAD)
+    assert sizes[13] == N.ABI_VERSION
 
 
 @pytest.mark.parametrize("name", ["simple_tau05", "kimi", "pairwise", "simple_bf16_v512",
