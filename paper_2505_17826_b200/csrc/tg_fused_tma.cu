@@ -33,7 +33,7 @@
 //  * Persistent grid: one CTA per SM (18 warps), as many clusters as can be
 //    co-resident, striding over rows.
 //  * kA (anchor KL, regularizer_g): the anchor row's chunks ride the ring
-//    behind the logits' (chunk pairs), both stay in the TMEM stash, and the
+//    beside the logits' (a z + za half-chunk pair per ring / TMEM slot), and the
 //    epilogue adds KL(p || q) -- 6V bytes per row instead of the two-pass 10V.
 //  * Route 4 (TG_FLAG_UNSCALED_GRAD): unit row coefficients, dz = p - e_y for
 //    the sequence-coupled losses; the per-row scale comes afterwards.
@@ -597,13 +597,19 @@ __device__ __forceinline__ float merge_lse(const float* lq, int lane) {
 }
 
 // ---- fused anchor KL (regularizer_g, algorithms.py:193-217) -------------------
-// kA: the row's anchor logits za ride the same ring -- every logical chunk is a
-// z chunk followed by the za chunk of the same columns (two consecutive ring
-// slots, two consecutive TMEM stash slots) -- so each row costs 6V bytes
-// (z and za read once, dz written once) instead of the two-pass route's 10V.
+// kA: the row's anchor logits za ride the same ring -- every ring slot holds a
+// half chunk of z (kVA vectors per consumer thread) followed by the za half
+// chunk of the same columns, and one TMEM stash slot keeps both -- so each
+// row costs 6V bytes (z and za read once, dz written once) instead of the
+// two-pass route's 10V, with the same look-ahead in columns as the default
+// path.
 // Phase 1 adds Sigma p (z - za) (aligned with z's reference max) and the
 // anchor's own online sum; the epilogue forms lse_q and KL(p || q); phase 2
 // writes dz = p (a + hz z - ca za) - s [v = y] (k_bwd's formula).
+constexpr int kVA = kVecPerThread / 2;           // z (and za) vectors per thread per slot
+constexpr int kVecPerChunkA = kConsumers * kVA;   // z vectors per slot
+constexpr uint32_t kHalf = uint32_t(kVecPerChunkA) * 16u;  // bytes of z (or za) per slot
+
 struct AccA {
   Acc1 z;         // (m, nm2, s2, t2, fresh) of the logits
   uint64_t u2;    // Sigma p (z - za), p = 2^((z - m) log2e)
@@ -650,48 +656,39 @@ __device__ __forceinline__ void accumulate_a(const uint4& uz, const uint4& uq, u
 template <typename T, bool kPartial, bool kMaskTail>
 __device__ __forceinline__ void phase1_chunk_a(AccA& acc, RingIt& it, const RingBase& rb,
                                                int vbase, const Slice& sl, int tid) {
-  uint4 uz[kVecPerThread], uq[kVecPerThread];
-  bool valid[kVecPerThread];
-  RingIt iq = it;
-  iq.next();
+  uint4 u[2 * kVA];  // [0, kVA): z vectors, [kVA, 2 kVA): za vectors of the same columns
+  bool valid[kVA];
   {
     TG_PROF_T0();
     wait_full(it.full(rb), it.phase());
     TG_PROF_ADD(prof_tail(), 0);
   }
-  const uint32_t az = it.addr(rb) + tid * 16;
+  const uint32_t a = it.addr(rb) + tid * 16;
 #pragma unroll
-  for (int g = 0; g < kVecPerThread; ++g) {
+  for (int g = 0; g < kVA; ++g) {
     const int vec = vbase + g * kConsumers + tid;
     valid[g] = !kPartial || vec < sl.v1;
-    uz[g] = valid[g] ? lds128(az + g * kConsumers * 16) : Pk<T>::neutral();
+    u[g] = valid[g] ? lds128(a + g * kConsumers * 16) : Pk<T>::neutral();
+    u[kVA + g] = valid[g] ? lds128(a + kHalf + g * kConsumers * 16) : Pk<T>::neutral();
   }
-  tmem_st16(stash_addr(rb, it.c), uz);
-  wait_full(iq.full(rb), iq.phase());
-  const uint32_t aq = iq.addr(rb) + tid * 16;
-#pragma unroll
-  for (int g = 0; g < kVecPerThread; ++g)
-    uq[g] = valid[g] ? lds128(aq + g * kConsumers * 16) : Pk<T>::neutral();
-  tmem_st16(stash_addr(rb, iq.c), uq);
+  static_assert(2 * kVA == 4, "one 16-column stash slot per z + za pair");
+  tmem_st16(stash_addr(rb, it.c), u);
   __syncwarp();
-  if ((tid & 31) == 0) {
-    arrive_u32(it.empty(rb));
-    arrive_u32(iq.empty(rb));
-  }
-  it.advance(2);
+  if ((tid & 31) == 0) arrive_u32(it.empty(rb));
+  it.next();
   if constexpr (kMaskTail) {
 #pragma unroll
-    for (int g = 0; g < kVecPerThread; ++g)
+    for (int g = 0; g < kVA; ++g)
       if (vbase + g * kConsumers + tid == sl.tail_vec) {
-        Pk<T>::mask_from(uz[g], sl.tail_valid);
-        Pk<T>::mask_from(uq[g], sl.tail_valid);
+        Pk<T>::mask_from(u[g], sl.tail_valid);
+        Pk<T>::mask_from(u[kVA + g], sl.tail_valid);
       }
   }
   {  // speculative: the current reference maxima, accepted when the sums are safe
     uint64_t s2 = pk2(0.f, 0.f), t2 = s2, u2 = s2, sq2 = s2;
 #pragma unroll
-    for (int g = 0; g < kVecPerThread; ++g)
-      accumulate_a<T>(uz[g], uq[g], acc.z.a.nm2, acc.nmq2, s2, t2, u2, sq2);
+    for (int g = 0; g < kVA; ++g)
+      accumulate_a<T>(u[g], u[kVA + g], acc.z.a.nm2, acc.nmq2, s2, t2, u2, sq2);
     float a0, a1;
     upk2(s2, a0, a1);
     const float sc = a0 + a1;
@@ -715,8 +712,11 @@ __device__ __forceinline__ void phase1_chunk_a(AccA& acc, RingIt& it, const Ring
     }
   }
   // checked: clamp -inf, exact warp maxima, rescale, sums
+  uint4 uz[kVA], uq[kVA];
 #pragma unroll
-  for (int g = 0; g < kVecPerThread; ++g) {
+  for (int g = 0; g < kVA; ++g) {
+    uz[g] = u[g];
+    uq[g] = u[kVA + g];
     Pk<T>::clamp(uz[g]);
     Pk<T>::clamp(uq[g]);
   }
@@ -744,7 +744,7 @@ __device__ __forceinline__ void phase1_chunk_a(AccA& acc, RingIt& it, const Ring
   acc.z.a.nm2 = pk2(nmL, nmL);
   acc.nmq2 = pk2(nqL, nqL);
 #pragma unroll
-  for (int g = 0; g < kVecPerThread; ++g)
+  for (int g = 0; g < kVA; ++g)
     if (!kPartial || valid[g])
       accumulate_a<T>(uz[g], uq[g], acc.z.a.nm2, acc.nmq2, acc.z.a.s2, acc.z.a.t2, acc.u2,
                       acc.sq2);
@@ -756,10 +756,10 @@ template <typename T>
 __device__ __forceinline__ void phase1_range_a(AccA& acc, RingIt row_it, const RingBase& rb,
                                                const Slice& sl, int c0, int c1, int tid) {
   RingIt it = row_it;
-  it.advance(2 * c0);
-  int vbase = sl.v0 + c0 * kVecPerChunk;
+  it.advance(c0);
+  int vbase = sl.v0 + c0 * kVecPerChunkA;
   for (int c = c0; c < c1; ++c) {
-    const int vend = vbase + kVecPerChunk;
+    const int vend = vbase + kVecPerChunkA;
     const bool has_tail = sl.tail_vec >= vbase && sl.tail_vec < vend;
     if (vend <= sl.v1 && !has_tail)
       phase1_chunk_a<T, false, false>(acc, it, rb, vbase, sl, tid);
@@ -798,15 +798,14 @@ __device__ __forceinline__ void phase2_chunk_a(const RingIt& it, const RingBase&
                                                uint64_t hz2, uint64_t nca2, int tid) {
   constexpr int EPV = Vec<T>::N;
   char* dst = dzrow + int64_t(vbase + tid) * 16;
-  uint4 sz[kVecPerThread], sq[kVecPerThread];
-  tmem_ld16(stash_addr(rb, it.c), sz);
-  tmem_ld16(stash_addr(rb, it.c + 1u), sq);
+  uint4 su[2 * kVA];
+  tmem_ld16(stash_addr(rb, it.c), su);
   const uint64_t l2e2 = pk2(kLog2e, kLog2e);
 #pragma unroll
-  for (int g = 0; g < kVecPerThread; ++g) {
+  for (int g = 0; g < kVA; ++g) {
     const int vec = vbase + g * kConsumers + tid;
     if (!kCheck || vec < sl.v1) {
-      uint4 uz = sz[g], uq = sq[g];
+      uint4 uz = su[g], uq = su[kVA + g];
       Pk<T>::clamp(uz);
       Pk<T>::clamp(uq);
       float d[EPV];
@@ -843,14 +842,14 @@ __device__ __forceinline__ void phase2_row_a(const Slice& sl, RingIt it, const R
                                              uint64_t nca2, int tid) {
   int vbase = sl.v0;
   for (int j = 0; j < sl.nchunk; ++j) {
-    const int vend = vbase + kVecPerChunk;
+    const int vend = vbase + kVecPerChunkA;
     const bool check = (vend > sl.v1) || (sl.tail_vec >= vbase && sl.tail_vec < vend) ||
                        (vy >= vbase && vy < vend);
     if (check)
       phase2_chunk_a<T, true>(it, rb, vbase, sl, dzrow, vy, ye, s_t, nl2, av2, hz2, nca2, tid);
     else
       phase2_chunk_a<T, false>(it, rb, vbase, sl, dzrow, vy, ye, s_t, nl2, av2, hz2, nca2, tid);
-    it.advance(2);
+    it.next();
     vbase = vend;
   }
 }
@@ -884,7 +883,7 @@ __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
 
 // Consumer warps of the fused anchor path: the same row loop as the default
 // consumers (first row's prefix, phase 1, partial post to every CTA of the
-// cluster, next row's prefix, phase 2), over chunk pairs.
+// cluster, next row's prefix, phase 2), over z + za half-chunk pairs.
 template <typename T, int CL>
 __device__ __forceinline__ void consumer_rows_a(const KParams& P, FusedSmemTail* tail,
                                                 const RingBase& rb, const Slice& sl, int pre,
@@ -934,7 +933,7 @@ __device__ __forceinline__ void consumer_rows_a(const KParams& P, FusedSmemTail*
       arrive_u32(smem_u32(&tail->pbar[par]));
     }
     RingIt npos = pos0;
-    npos.advance(2 * sl.nchunk);
+    npos.advance(sl.nchunk);
     acc_new_row_a(acc);
     if (nrow < NR) phase1_range_a<T>(acc, npos, rb, sl, 0, pre, vtid);
     {
@@ -964,7 +963,7 @@ template <typename T, int CL, bool kA = false>
 __global__ void __launch_bounds__(kFusedThreads, 1)
     k_fused_tma(const KParams P, const RowMeta* __restrict__ meta, int prefetch_rows) {
   static_assert(!kA || kStash, "the fused anchor path keeps z and za in the TMEM stash");
-  constexpr int kRing = kA ? 2 : 1;  // ring slots per logical chunk (z [, za])
+  // kA: a ring / stash slot holds a z + za half-chunk pair
   constexpr int EPV = Vec<T>::N;  // elements per 16-byte vector
   constexpr int ESZ = elem_bytes<T>();
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -986,12 +985,12 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   sl.v0 = int((int64_t(rank) * nvec) / CL);
   sl.v1 = int((int64_t(rank + 1) * nvec) / CL);
   const uint32_t slice_bytes = uint32_t(sl.v1 - sl.v0) * 16u;
-  sl.nchunk = int((slice_bytes + kChunk - 1) / kChunk);
+  sl.nchunk = int((slice_bytes + (kA ? kHalf : kChunk) - 1) / (kA ? kHalf : kChunk));
   sl.tail_vec = (V % EPV) ? nvec - 1 : -1;  // global vector holding columns >= V
   sl.tail_valid = V - (nvec - 1) * EPV;
   // next-row phase-1 chunks that fit in the ring beside this row's slice
   const int pre =
-      min(min(kMaxPrefixChunks, (kStash ? kTSlots : kSlots) / kRing - sl.nchunk), sl.nchunk);
+      min(min(kMaxPrefixChunks, (kStash ? kTSlots : kSlots) - sl.nchunk), sl.nchunk);
 
   if (tid == 0) {
     for (int i = 0; i < kSlots; ++i) {
@@ -1059,34 +1058,29 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
             mbar_wait_u32<TG_SLEEP_PROD>(it.empty(rb), it.phase() ^ 1u);
             TG_PROF_ADD(tail, 3);
           }
-          const uint32_t off = uint32_t(j) * kChunk;
-          const uint32_t bytes = min(uint32_t(kChunk), slice_bytes - off);
+          // kA: a half chunk of z and the same columns of the anchor row in one slot
+          const uint32_t step = kA ? kHalf : uint32_t(kChunk);
+          const uint32_t off = uint32_t(j) * step;
+          const uint32_t bytes = min(step, slice_bytes - off);
           asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
                            it.full(rb)),
-                       "r"(bytes)
+                       "r"(kA ? 2 * bytes : bytes)
                        : "memory");
           asm volatile(
               "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
               " [%0], [%1], %2, [%3], %4;" ::"r"(it.addr(rb)),
               "l"(src + off), "r"(bytes), "r"(it.full(rb)), "l"(pol)
               : "memory");
-          it.next();
-          if constexpr (kA) {  // the same columns of the anchor row, into the next slot
+          if constexpr (kA) {
             const char* qsrc = reinterpret_cast<const char*>(P.anchor) +
                                row * P.ld_anchor * ESZ + int64_t(sl.v0) * 16;
-            mbar_wait_u32<TG_SLEEP_PROD>(it.empty(rb), it.phase() ^ 1u);
-            asm volatile(
-                "mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
-                    it.full(rb)),
-                "r"(bytes)
-                : "memory");
             asm volatile(
                 "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-                " [%0], [%1], %2, [%3], %4;" ::"r"(it.addr(rb)),
+                " [%0], [%1], %2, [%3], %4;" ::"r"(it.addr(rb) + kHalf),
                 "l"(qsrc + off), "r"(bytes), "r"(it.full(rb)), "l"(pol)
                 : "memory");
-            it.next();
           }
+          it.next();
         }
       }
     }
