@@ -332,14 +332,14 @@ FusedPlan fused_plan(const TgBatch* b, const TgOut* o, bool anchor = false) {
   for (int oi = 0; oi < 4; ++oi) {
     const int cl = kOrder[oi];
     if (force_cl ? cl != force_cl : cl == 3) continue;  // CL = 3 only on request
-    if (anchor && cl == 3) continue;
     const int64_t slice_vec = (nvec + cl - 1) / cl;
     const int64_t nchunk = (slice_vec * 16 + fused_chunk_bytes() - 1) / fused_chunk_bytes();
     // resident TMEM chunks: the slice + >= 2 prefix chunks (anchor: a stash
     // slot holds a z + za half-chunk pair)
     const int64_t half = fused_chunk_bytes() / 2;
     const int64_t nslot = anchor ? (slice_vec * 16 + half - 1) / half : nchunk;
-    if (nslot + 2 <= fused_resident_chunks()) {
+    // (a forced cluster size may run with a single slot of look-ahead)
+    if (nslot + ((force_cl && anchor) ? 1 : 2) <= fused_resident_chunks()) {
       // persistent grid: as many clusters as can be co-resident, at most one per row
       int64_t clusters_max = fused_max_clusters(b->dtype, cl);
       if (clusters_max <= 0) clusters_max = d.sms / cl;

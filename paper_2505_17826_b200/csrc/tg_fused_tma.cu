@@ -1548,6 +1548,7 @@ cudaError_t launch_fused(const KParams& P, const void* meta, int cl, int n_slots
     if (P.dtype != TG_DTYPE_BF16) return cudaErrorInvalidValue;
     if (cl == 1) return launch_fused_t<bf16_t, 1, true>(P, m, n_ctas, prefetch_rows, stream);
     if (cl == 2) return launch_fused_t<bf16_t, 2, true>(P, m, n_ctas, prefetch_rows, stream);
+    if (cl == 3) return launch_fused_t<bf16_t, 3, true>(P, m, n_ctas, prefetch_rows, stream);
     if (cl == 4) return launch_fused_t<bf16_t, 4, true>(P, m, n_ctas, prefetch_rows, stream);
     return cudaErrorInvalidValue;
   }
