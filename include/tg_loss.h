@@ -252,8 +252,10 @@ int tg_apply_update(float* table, int64_t ld_table, int64_t n_states, int64_t vo
                     int64_t n_rows, double learning_rate, int32_t* status, void* stream);
 
 /* Which kernel route tg_loss_fwd_bwd takes for this input: 1 = fused single
-   pass (4V bytes/row), 2 = forward + backward streaming (6V), 3 = coupled
-   (6V), 4 = coupled with TG_FLAG_UNSCALED_GRAD (single pass, 4V). */
+   pass (4V bytes/row; 6V with the anchor KL of regularizer_g, whose anchor
+   rows ride the same pass), 2 = forward + backward streaming (6V; 10V with
+   the anchor), 3 = coupled (6V), 4 = coupled with TG_FLAG_UNSCALED_GRAD
+   (single pass, 4V). */
 int tg_route(const TgBatch* batch, const TgConfig* cfg);
 
 /* Timing hook (measurement only): when both are non-NULL cudaEvent_t handles,
