@@ -1122,8 +1122,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         TG_PROF_T0();
         if constexpr (CL > 1)
           mbar_wait_cluster_sleep<TG_SLEEP_EPI>(smem_u32(&tail->pbar[par]), parity);
-        else
-          mbar_wait_u32<TG_SLEEP_EPI>(smem_u32(&tail->pbar[par]), parity);
+        else  // short rows (CL = 1): spin, the waits are frequent and short (+0.65 %)
+          mbar_wait_u32<0>(smem_u32(&tail->pbar[par]), parity);
         TG_PROF_ADD(tail, 4);
       }
 #ifdef TG_FUSED_PROF
@@ -1304,7 +1304,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       // ---------------- phase 2: dz from the resident slice ----------------
       {
         TG_PROF_T0();
-        mbar_wait_u32<TG_SLEEP_BCAST>(smem_u32(&tail->bbar[par]), uint32_t((k >> 1) & 1));
+        mbar_wait_u32<(CL == 1 ? 0 : TG_SLEEP_BCAST)>(smem_u32(&tail->bbar[par]),
+                                                      uint32_t((k >> 1) & 1));
         TG_PROF_ADD(tail, 1);
       }
       if constexpr (kStash) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
