@@ -938,7 +938,8 @@ __device__ __forceinline__ void consumer_rows_a(const KParams& P, FusedSmemTail*
     if (nrow < NR) phase1_range_a<T>(acc, npos, rb, sl, 0, pre, vtid);
     {
       TG_PROF_T0();
-      mbar_wait_u32<TG_SLEEP_BCAST>(smem_u32(&tail->bbar[par]), uint32_t((k >> 1) & 1));
+      mbar_wait_u32<(CL == 1 ? 0 : TG_SLEEP_BCAST)>(smem_u32(&tail->bbar[par]),
+                                                    uint32_t((k >> 1) & 1));
       TG_PROF_ADD(tail, 1);
     }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
