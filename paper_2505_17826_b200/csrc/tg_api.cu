@@ -316,8 +316,8 @@ FusedPlan fused_plan(const TgBatch* b, const TgOut* o, bool anchor = false) {
   if (!aligned16(o->dlogits) || (o->ld_out * esz) % 16 != 0 || o->ld_out < b->vocab) return fp;
   const int64_t nvec = (b->vocab + epv - 1) / epv;
   if (b->ld < nvec * epv) return fp;  // TMA reads whole 16-byte vectors
-  if (anchor) {  // the anchor rows ride the same ring: bf16, aligned, whole vectors
-    if (b->dtype != TG_DTYPE_BF16 || !aligned16(b->anchor_logits) ||
+  if (anchor) {  // the anchor rows ride the same ring: aligned, whole vectors
+    if (!aligned16(b->anchor_logits) ||
         (b->ld_anchor * esz) % 16 != 0 || b->ld_anchor < nvec * epv)
       return fp;
     if (env_int("TG_FUSED_ANCHOR", 1) == 0) return fp;
@@ -332,6 +332,7 @@ FusedPlan fused_plan(const TgBatch* b, const TgOut* o, bool anchor = false) {
   for (int oi = 0; oi < 4; ++oi) {
     const int cl = kOrder[oi];
     if (force_cl ? cl != force_cl : cl == 3) continue;  // CL = 3 only on request
+    if (anchor && cl == 3 && b->dtype != TG_DTYPE_BF16) continue;  // not instantiated
     const int64_t slice_vec = (nvec + cl - 1) / cl;
     const int64_t nchunk = (slice_vec * 16 + fused_chunk_bytes() - 1) / fused_chunk_bytes();
     // resident TMEM chunks: the slice + >= 2 prefix chunks (anchor: a stash

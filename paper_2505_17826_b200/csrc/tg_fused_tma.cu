@@ -1546,12 +1546,17 @@ cudaError_t launch_fused(const KParams& P, const void* meta, int cl, int n_slots
                          int prefetch_rows, cudaStream_t stream) {
   if (n_slots != kSlots) return cudaErrorInvalidValue;
   const RowMeta* m = reinterpret_cast<const RowMeta*>(meta);
-  if (P.anchor && P.anchor_beta > 0.f) {  // fused anchor KL: bf16 only (fused_anchor_plan)
-    if (P.dtype != TG_DTYPE_BF16) return cudaErrorInvalidValue;
-    if (cl == 1) return launch_fused_t<bf16_t, 1, true>(P, m, n_ctas, prefetch_rows, stream);
-    if (cl == 2) return launch_fused_t<bf16_t, 2, true>(P, m, n_ctas, prefetch_rows, stream);
-    if (cl == 3) return launch_fused_t<bf16_t, 3, true>(P, m, n_ctas, prefetch_rows, stream);
-    if (cl == 4) return launch_fused_t<bf16_t, 4, true>(P, m, n_ctas, prefetch_rows, stream);
+  if (P.anchor && P.anchor_beta > 0.f) {  // fused anchor KL (fused_plan's anchor rules)
+    if (P.dtype == TG_DTYPE_BF16) {
+      if (cl == 1) return launch_fused_t<bf16_t, 1, true>(P, m, n_ctas, prefetch_rows, stream);
+      if (cl == 2) return launch_fused_t<bf16_t, 2, true>(P, m, n_ctas, prefetch_rows, stream);
+      if (cl == 3) return launch_fused_t<bf16_t, 3, true>(P, m, n_ctas, prefetch_rows, stream);
+      if (cl == 4) return launch_fused_t<bf16_t, 4, true>(P, m, n_ctas, prefetch_rows, stream);
+    } else {  // fp32 rows: the slices fit the stash up to V ~ 65 k (CL <= 4)
+      if (cl == 1) return launch_fused_t<float, 1, true>(P, m, n_ctas, prefetch_rows, stream);
+      if (cl == 2) return launch_fused_t<float, 2, true>(P, m, n_ctas, prefetch_rows, stream);
+      if (cl == 4) return launch_fused_t<float, 4, true>(P, m, n_ctas, prefetch_rows, stream);
+    }
     return cudaErrorInvalidValue;
   }
   if (P.dtype == TG_DTYPE_BF16) {

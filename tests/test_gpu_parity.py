@@ -177,6 +177,18 @@ def test_fused_anchor_kl_route_matches_oracle(shape, case_kw):
     assert a["sum_anchor_kl"] == pytest.approx(b["sum_anchor_kl"], rel=1e-4, abs=1e-5)
 
 
+@pytest.mark.parametrize("shape,route", [("v1000", 1), ("v32000", 1), ("v151936", 2)])
+def test_fp32_anchor_kl_routes_match_oracle(shape, route):
+    """fp32 rows take the fused anchor path while both slices fit the TMEM
+    stash (V up to ~65 k), else the two-pass route; both against the oracle."""
+    V, lens, gs = SHAPES[shape]
+    cfg = RFTLossConfig.from_variant("OPMD_SIMPLE", tau=0.4, beta=0.9)
+    batch, packed = make_case(7, V, lens, gs, dtype=torch.float32, anchor=True)
+    assert RFTLoss(cfg).route(packed) == route
+    out = RFTLoss(cfg)(packed, dlogits="new")
+    compare(out, O.general_loss(batch, oracle_cfg(cfg)), torch.float32)
+
+
 def test_fused_anchor_kl_with_masked_vocabulary_matches_two_pass():
     """-inf logits (masked vocabulary, in both the policy and the anchor rows)
     take the fused anchor path's checked branch; the oracle cannot evaluate
