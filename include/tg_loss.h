@@ -112,7 +112,9 @@ enum {
                                   third block, d loss / d z_t = s_t (p_t - e_y) -- the
                                   caller folds diag(s) into its LM-head backward
                                   (d hidden rows and the hidden rows of d W scale by s_t;
-                                  SURVEY.md 7, hard part 3).  No anchor KL.          */
+                                  SURVEY.md 7, hard part 3).  No anchor KL.  Layouts
+                                  the single pass cannot take (unaligned pitch, forced
+                                  two-pass) give the same outputs over two passes.   */
 };
 
 /* stats[] layout (double).  Sums are over this call's rows / groups; the

@@ -452,6 +452,8 @@ int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspa
       return fail(TG_EINVAL, "TG_FLAG_UNSCALED_GRAD needs out.dlogits and out.row_coef");
     if (c->flags & TG_FLAG_ROWS_GIVEN)
       return fail(TG_EINVAL, "TG_FLAG_UNSCALED_GRAD and TG_FLAG_ROWS_GIVEN exclude each other");
+    if (c->anchor_beta > 0)
+      return fail(TG_EINVAL, "TG_FLAG_UNSCALED_GRAD cannot describe the anchor-KL gradient");
   }
   if (o->row_coef && c->anchor_beta > 0)
     return fail(TG_EINVAL, "out.row_coef cannot describe the anchor-KL gradient (anchor_beta > 0)");
@@ -469,10 +471,9 @@ int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspa
   KParams P;
   fill_params(P, b, c, o, ws, L);
   void* meta = ws + L.meta;
-  int route = route_of(b, c, o);
-  if (route == 3 && (c->flags & TG_FLAG_UNSCALED_GRAD))
-    return fail(TG_EUNSUPPORTED, "TG_FLAG_UNSCALED_GRAD: no single-pass plan for this batch "
-                                 "(dtype / pitch / anchor / forced two-pass)");
+  // TG_FLAG_UNSCALED_GRAD without a single-pass plan (pitch / dtype / forced
+  // two-pass) runs route 3 with a unit-coefficient backward: same outputs, 6V bytes
+  const int route = route_of(b, c, o);
   const bool coupled = route == 3 || route == 4;
   const bool anchor = c->anchor_beta > 0;
   const int esz = esz_of(b->dtype);

@@ -263,7 +263,10 @@ __global__ void __launch_bounds__(kStreamThreads) k_bwd(const KParams P) {
     char* drow = reinterpret_cast<char*>(P.dz) + row * P.ld_out * ESZ;
     const int64_t y = P.target[row];
     const float lseL = P.lse[row] * kLog2e;
-    const float a = P.rA[row], hz = P.rHz[row], ca = P.rCa[row], s = P.rS[row];
+    // TG_FLAG_UNSCALED_GRAD (coupled losses): p - e_y; the true row scale is in rS
+    const bool unit = (P.flags & TG_FLAG_UNSCALED_GRAD) != 0;
+    const float a = unit ? 1.f : P.rA[row], hz = unit ? 0.f : P.rHz[row];
+    const float ca = unit ? 0.f : P.rCa[row], s = unit ? 1.f : P.rS[row];
     if (VEC) {
       const int64_t nvec = (V + EPV - 1) / EPV;
       const int64_t vy = (y >= 0 && y < V) ? y / EPV : -1;
@@ -388,7 +391,9 @@ __global__ void __launch_bounds__(kStreamThreads) k_bwd_fast(const KParams P) {
     const int vy = (y >= 0 && y < V) ? y / EPV : -1;
     const int ye = (vy >= 0) ? y - vy * EPV : 0;
     const float lseL = P.lse[row] * kLog2e;
-    const float a = P.rA[row], hz = P.rHz[row], s = P.rS[row];
+    const bool unit = (P.flags & TG_FLAG_UNSCALED_GRAD) != 0;  // p - e_y (see k_bwd)
+    const float a = unit ? 1.f : P.rA[row], hz = unit ? 0.f : P.rHz[row];
+    const float s = unit ? 1.f : P.rS[row];
     const uint64_t nl2 = pk2(-lseL, -lseL), av2 = pk2(a, a), hz2 = pk2(hz, hz);
     for (int base = 0; base < nvec; base += kStreamThreads * kFastVec) {
       uint4 u[kFastVec];

@@ -1,4 +1,4 @@
-"""Randomised parity sweep: 96 seeded combinations of the registry components
+"""Randomised parity sweep: 160 seeded combinations of the registry components
 (advantage x policy loss x KL x entropy x aggregation), anchor KL, mixed SFT
 sequences, dtype, vocabulary size, padded pitch and the unscaled coupled
 route, each against the oracle with the tolerances of test_gpu_parity.py.
@@ -56,7 +56,7 @@ def draw(seed):
     return kw, anchor, dtype, V, K, G, lens, seq_kind, ld, unscaled
 
 
-@pytest.mark.parametrize("seed", range(96))
+@pytest.mark.parametrize("seed", range(160))
 def test_random_configuration_matches_oracle(seed):
     kw, anchor, dtype, V, K, G, lens, seq_kind, ld, unscaled = draw(seed)
     cfg = RFTLossConfig(**kw)
@@ -68,4 +68,9 @@ def test_random_configuration_matches_oracle(seed):
         out.dlogits = out.dlogits.float() * out.row_scale[:, None]
     else:
         out = loss(packed, dlogits="new")
-    compare(out, O.general_loss(batch, oracle_cfg(cfg)), dtype)
+    # sequence-coupled coefficients are differences of sequence sums of fp32 row
+    # logprobs (pairwise: a_i - a_j), so near-cancelling groups carry ~1e-4
+    # relative error in fp32; per-row losses keep the parity-matrix bar
+    coupled = cfg.policy_loss_fn in ("opmd_kimi", "opmd_pairwise")
+    compare(out, O.general_loss(batch, oracle_cfg(cfg)), dtype,
+            rtol_dz=1e-3 if coupled and dtype == torch.float32 else None)

@@ -33,7 +33,7 @@ def _close_loss(a, b, floor):
     assert abs(a - b) <= 1e-3 * max(abs(b), floor), (a, b, floor)
 
 
-def compare(out, ref, dtype, dz=True):
+def compare(out, ref, dtype, dz=True, rtol_dz=None):
     st = out.stats_dict()
     rs = O.stats_dict(ref["stats"])
     floor = 1e-3 * float(np.sum(np.abs(ref["s"] * ref["lp"]))) + 1e-6
@@ -57,9 +57,9 @@ def compare(out, ref, dtype, dz=True):
         r = ref["dz"]
         scale = float(np.max(np.abs(r))) if r.size else 0.0
         if dtype == torch.bfloat16:
-            tol = 2.0 ** -8 * scale + 1e-2 * np.abs(r)
+            tol = 2.0 ** -8 * scale + (rtol_dz or 1e-2) * np.abs(r)
         else:
-            tol = 1e-5 * scale + 1e-4 * np.abs(r)
+            tol = 1e-5 * scale + (rtol_dz or 1e-4) * np.abs(r)
         err = np.abs(d[:, : r.shape[1]] - r)
         assert np.all(err <= tol), float(np.max(err - tol))
 

@@ -87,3 +87,21 @@ def test_unscaled_in_place_and_errors():
         grpo(b2, dlogits="new", unscaled=True)  # not a coupled loss
     with pytest.raises(NativeError):
         kimi(b2, dlogits=None, unscaled=True)  # needs dlogits
+
+
+def test_unscaled_on_a_layout_without_single_pass_plan():
+    """An unaligned row pitch has no fused plan: the unscaled gradient still
+    comes out (route 3 with a unit-coefficient backward), matching the scaled
+    two-pass result row by row."""
+    lens = [21, 13, 30, 8]
+    _, batch = make_case(9, 4097, lens, [2, 2])  # 4,097 x 2 B rows: not 16-byte aligned
+    kimi = RFTLoss(RFTLossConfig(policy_loss_fn="opmd_kimi", tau=0.6))
+    assert kimi.route(batch, unscaled=True) == 3
+    ref = kimi(batch, dlogits="new")
+    got = kimi(batch, dlogits="new", unscaled=True)
+    torch.cuda.synchronize()
+    assert torch.equal(got.stats, ref.stats)
+    scaled = got.dlogits.float() * got.row_scale[:, None]
+    want = ref.dlogits.float()
+    assert bool(((scaled - want).abs() <= 2.0 ** -8 * float(want.abs().max())
+                 + 1e-2 * want.abs()).all())
