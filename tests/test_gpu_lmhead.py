@@ -228,3 +228,32 @@ def test_lmhead_backward_in_both_cta_modes(pair):
                         "no:cacheprovider", "-k", "matches_torch_fp32 or backward_from_hidden or matches_formula"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_lmhead_random_shapes(seed):
+    """Seeded random shapes for both LM-head kernels: row counts off the tile
+    grid (including 1), vocabularies off the 256-column tile, several d, and a
+    random vocabulary chunk for the backward -- forward lse / entropy against
+    torch fp32 and dz against the formula."""
+    from paper_2505_17826_b200 import lmhead_dlogits
+    r = np.random.default_rng(500 + seed)
+    T = int(r.choice([1, 7, 128, 129, 300, 777]))
+    V = int(r.integers(64, 5000))
+    d = int(r.choice([64, 128, 256, 512]))
+    h, w, y = make(T, V, d, seed=seed)
+    lp, ent, lse = lmhead_logprob_fwd(h, w, y)
+    rlp, rent, rlse = reference(h, w, y)
+    torch.testing.assert_close(lse, rlse, atol=2e-4, rtol=1e-5)
+    torch.testing.assert_close(ent, rent, atol=2e-4, rtol=1e-4)
+    col0 = int(r.integers(0, V - 1))
+    n = int(r.integers(1, V - col0 + 1))
+    coef = (torch.randn(3, T, device="cuda", generator=torch.Generator(device="cuda")
+                        .manual_seed(seed)) * 0.3).contiguous()
+    got = lmhead_dlogits(h, w, y, rlse.contiguous(), coef, col0, n).float()
+    z = (h.float() @ w.float().T)[:, col0:col0 + n]
+    want = torch.exp(z - rlse[:, None]) * (coef[0][:, None] + coef[1][:, None] * z)
+    want -= coef[2][:, None] * (y.long()[:, None] ==
+                                torch.arange(col0, col0 + n, device="cuda")).float()
+    tol = 2.0 ** -8 * float(want.abs().max()) + 1e-2 * want.abs()
+    assert bool(((got - want).abs() <= tol).all())
