@@ -1,5 +1,9 @@
 # A/B of the fused anchor path and the epilogue merge (scripts/bench_anchor.py),
-# plus instrumented per-row cycle accounting of both merge forms.
+# plus instrumented per-row cycle accounting of both merge forms.  Build the
+# variants first:
+#   python -m paper_2505_17826_b200._build --variant=mergeold --define=-DTG_MERGE_REDUX=0
+#   python -m paper_2505_17826_b200._build --variant=prof
+#   python -m paper_2505_17826_b200._build --variant=profold --define=-DTG_FUSED_PROF --define=-DTG_MERGE_REDUX=0
 mkdir -p gpurun_out
 L=$PWD/paper_2505_17826_b200/_lib
 for rep in 1 2; do
