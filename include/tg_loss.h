@@ -80,6 +80,10 @@ enum {
   TG_PG_OPMD_PAIRWISE = 4,  /* sum_{i<j} (a_i - a_j)^2                    :156-190       */
   TG_PG_DPO = 5             /* mean softplus(-beta margin); groups are (chosen, rejected) */
 };
+/* The sequence-coupled losses (OPMD_KIMI, OPMD_PAIRWISE, DPO) are whole-sequence
+   objectives: with them kl_fn / kl_coef, the entropy bonus, a loss_agg_mode other
+   than TG_AGG_SEQ_SUM and a seq_kind array (SFT rows) are refused with TG_EINVAL
+   instead of being silently dropped.  The anchor KL (anchor_beta) is allowed. */
 
 /* kl_fn registry: token-level penalty kl_coef * kl(lp, ref_lp) */
 enum { TG_KL_NONE = 0, TG_KL_K1 = 1, TG_KL_K2 = 2, TG_KL_K3 = 3 /* low_var_kl */, TG_KL_ABS = 4 };
@@ -259,6 +263,11 @@ int tg_apply_update(float* table, int64_t ld_table, int64_t n_states, int64_t vo
    the anchor), 3 = coupled (6V), 4 = coupled with TG_FLAG_UNSCALED_GRAD
    (single pass, 4V). */
 int tg_route(const TgBatch* batch, const TgConfig* cfg);
+
+/* Thread-block cluster size of the fused single-pass kernel (k_fused_tma<T, CL>)
+   that tg_loss_fwd_bwd launches for this input on the current device (routes 1
+   and 4), or 0 when the call takes a streaming route.  Introspection only. */
+int tg_fused_cluster_size(const TgBatch* batch, const TgConfig* cfg);
 
 /* Timing hook (measurement only): when both are non-NULL cudaEvent_t handles,
    the next tg_loss_fwd_bwd call on this thread records ev_begin on its stream

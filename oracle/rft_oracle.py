@@ -519,13 +519,15 @@ def general_loss(batch: Batch, cfg: Config, want_dz: bool = True) -> Dict[str, o
             pg_t = -At * lp
             s_pg = At.copy()
         elif pg == "ppo_clip":
-            logr = np.clip(lp - old, -20.0, 20.0)
+            dlr = lp - old
+            logr = np.clip(dlr, -20.0, 20.0)
             rho = np.exp(logr)
             l1 = -At * rho
             l2 = -At * np.clip(rho, 1.0 - cfg.clip_lo, 1.0 + cfg.clip_hi)
             pg_t = np.maximum(l1, l2)
             clipped = l2 > l1
-            s_pg = np.where(clipped, 0.0, At * rho)
+            # the log-ratio clamp is a torch.clamp (verl): zero gradient when active
+            s_pg = np.where(clipped | (logr != dlr), 0.0, At * rho)
             if cfg.clip_c > 0:
                 l3 = -At * cfg.clip_c
                 dual = (At < 0) & (l3 < pg_t)
@@ -699,11 +701,13 @@ def single_pass_blocked(batch: Batch, cfg: Config, dz_out: Optional[np.ndarray] 
         At, wt, rl = A[row_seq[a:b]], w[row_seq[a:b]], is_rl[a:b]
         if cfg.policy_loss_fn == "ppo_clip":
             old = batch.old_lp[a:b] if batch.old_lp is not None else lpb
-            rho = np.exp(np.clip(lpb - old, -20.0, 20.0))
+            dlr = lpb - old
+            logr = np.clip(dlr, -20.0, 20.0)
+            rho = np.exp(logr)
             l1 = -At * rho
             l2 = -At * np.clip(rho, 1.0 - cfg.clip_lo, 1.0 + cfg.clip_hi)
             pg = np.maximum(l1, l2)
-            s_pg = np.where(l2 > l1, 0.0, At * rho)
+            s_pg = np.where((l2 > l1) | (logr != dlr), 0.0, At * rho)
             if cfg.clip_c > 0:
                 l3 = -At * cfg.clip_c
                 dual = (At < 0) & (l3 < pg)

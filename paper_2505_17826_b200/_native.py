@@ -75,7 +75,7 @@ EXPORTED = [
     "tg_workspace_size", "tg_loss_fwd_bwd", "tg_logprob_fwd", "tg_route", "tg_strerror",
     "tg_last_error", "tg_abi_version", "tg_scored_states", "tg_group_by_task",
     "tg_set_timing_events", "tg_launch_count", "tg_pack_rows", "tg_lmhead_logprob_fwd",
-    "tg_lmhead_workspace_size", "tg_apply_update", "tg_lmhead_dlogits",
+    "tg_lmhead_workspace_size", "tg_apply_update", "tg_lmhead_dlogits", "tg_fused_cluster_size",
 ]
 
 ABI_VERSION = 2  # include/tg_loss.h TG_ABI_VERSION
@@ -115,6 +115,8 @@ def lib() -> ctypes.CDLL:
     L.tg_logprob_fwd.argtypes = [POINTER(TgBatch), POINTER(TgOut), c_void_p, c_size_t, c_void_p]
     L.tg_route.restype = c_int
     L.tg_route.argtypes = [POINTER(TgBatch), POINTER(TgConfig)]
+    L.tg_fused_cluster_size.restype = c_int
+    L.tg_fused_cluster_size.argtypes = [POINTER(TgBatch), POINTER(TgConfig)]
     L.tg_strerror.restype = c_char_p
     L.tg_strerror.argtypes = [c_int]
     L.tg_last_error.restype = c_char_p

@@ -6,6 +6,7 @@ from __future__ import annotations
 import enum
 import math
 from dataclasses import dataclass, replace
+from typing import Optional
 
 from . import _native as N
 from .registry import (ADVANTAGE_FNS, ENTROPY_LOSS_FNS, KL_FNS, LOSS_AGG_MODES,
@@ -35,7 +36,7 @@ class RFTLossConfig:
     policy_loss_fn: str = "ppo_clip"
     kl_fn: str = "none"
     entropy_loss_fn: str = "none"
-    loss_agg_mode: str = "token-mean"
+    loss_agg_mode: Optional[str] = None   # None: "seq-sum" for coupled losses, else "token-mean"
     tau: float = 0.0
     clip_lo: float = 0.2
     clip_hi: float = 0.2
@@ -56,6 +57,8 @@ class RFTLossConfig:
         self.kl_fn = lookup(KL_FNS, self.kl_fn, "kl_fn").name
         self.entropy_loss_fn = lookup(ENTROPY_LOSS_FNS, self.entropy_loss_fn,
                                       "entropy_loss_fn").name
+        if self.loss_agg_mode is None:
+            self.loss_agg_mode = "seq-sum" if self.policy_loss_fn in COUPLED else "token-mean"
         self.loss_agg_mode = lookup(LOSS_AGG_MODES, self.loss_agg_mode, "loss_agg_mode").name
         # scalar rules (algorithms.py:47-56 and the north_star pieces)
         if not self.tau >= 0:
@@ -77,6 +80,18 @@ class RFTLossConfig:
             raise AlgorithmError("sft_weight must be >= 0")
         if self.loss_agg_mode == "seq-mean-token-sum-norm" and not self.agg_norm > 0:
             raise AlgorithmError("agg_norm must be > 0")
+        if self.policy_loss_fn in COUPLED:
+            # the sequence-coupled losses are whole-sequence objectives (algorithms.py:
+            # 118-190, 277-315): a token KL, an entropy bonus or a token aggregation
+            # would have no defined gradient there -- refuse instead of dropping them
+            if self.kl_fn != "none" and self.kl_coef != 0:
+                raise AlgorithmError(f"{self.policy_loss_fn} takes no token KL penalty "
+                                     f"(kl_fn={self.kl_fn!r}, kl_coef={self.kl_coef})")
+            if self.entropy_loss_fn != "none" and self.entropy_coef != 0:
+                raise AlgorithmError(f"{self.policy_loss_fn} takes no entropy bonus")
+            if self.loss_agg_mode != "seq-sum":
+                raise AlgorithmError(f"{self.policy_loss_fn} sums over groups; loss_agg_mode "
+                                     f"{self.loss_agg_mode!r} does not apply")
         for k in ("tau", "clip_lo", "clip_hi", "clip_c", "kl_coef", "entropy_coef", "std_eps",
                   "sft_weight", "anchor_beta", "dpo_beta", "agg_norm"):
             if not math.isfinite(getattr(self, k)):

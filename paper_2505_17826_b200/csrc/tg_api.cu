@@ -209,6 +209,17 @@ int validate_cfg(const TgBatch* b, const TgConfig* c) {
   if (!(c->sft_weight >= 0)) return fail(TG_EINVAL, "sft_weight must be >= 0");
   if (c->loss_agg_mode == TG_AGG_SEQ_MEAN_TOKEN_SUM_NORM && !(c->agg_norm > 0))
     return fail(TG_EINVAL, "agg_norm must be > 0");
+  if (coupled_pg(c->policy_loss_fn)) {
+    // whole-sequence objectives: no per-token penalty, bonus, aggregation or SFT rows
+    if (c->kl_fn != TG_KL_NONE && c->kl_coef != 0)
+      return fail(TG_EINVAL, "sequence-coupled losses take no token KL penalty");
+    if (c->entropy_loss_fn != TG_ENT_NONE && c->entropy_coef != 0)
+      return fail(TG_EINVAL, "sequence-coupled losses take no entropy bonus");
+    if (c->loss_agg_mode != TG_AGG_SEQ_SUM)
+      return fail(TG_EINVAL, "sequence-coupled losses sum over groups (loss_agg_mode SEQ_SUM)");
+    if (b->seq_kind || c->n_sft_seq_global > 0)
+      return fail(TG_EINVAL, "sequence-coupled losses take no SFT rows (seq_kind must be NULL)");
+  }
   if (c->advantage_fn == TG_ADV_GIVEN &&
       (c->policy_loss_fn == TG_PG_VANILLA || c->policy_loss_fn == TG_PG_PPO_CLIP) &&
       b->n_seqs > 0 && !b->advantage)
@@ -427,6 +438,16 @@ int tg_route(const TgBatch* batch, const TgConfig* cfg) {
   probe.dlogits = const_cast<void*>(batch->logits);
   probe.ld_out = batch->ld;
   return route_of(batch, cfg, &probe);
+}
+
+int tg_fused_cluster_size(const TgBatch* batch, const TgConfig* cfg) {
+  if (!batch || !cfg) return 0;
+  TgOut probe = {};
+  probe.dlogits = const_cast<void*>(batch->logits);
+  probe.ld_out = batch->ld;
+  const int r = route_of(batch, cfg, &probe);
+  if (r != 1 && r != 4) return 0;
+  return fused_plan(batch, &probe, r == 1 && cfg->anchor_beta > 0).cl;
 }
 
 int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspace,

@@ -67,13 +67,15 @@ __device__ __forceinline__ RowTerms meta_terms(const KParams& P, const RowMeta& 
   float pg, s_pg;
   if (P.pg == TG_PG_PPO_CLIP) {
     const float old = P.old_lp ? m.old : lp;
-    const float logr = fminf(fmaxf(lp - old, -20.f), 20.f);
+    const float dlr = lp - old;
+    const float logr = fminf(fmaxf(dlr, -20.f), 20.f);
     const float rho = TG_EXPF(logr);
     const float l1 = -A * rho;
     const float l2 = -A * fminf(fmaxf(rho, 1.f - P.clip_lo), 1.f + P.clip_hi);
     pg = fmaxf(l1, l2);
     const bool clipped = l2 > l1;
-    s_pg = clipped ? 0.f : A * rho;
+    // the log-ratio clamp is a torch.clamp: no gradient through a clamped ratio
+    s_pg = (clipped || logr != dlr) ? 0.f : A * rho;
     if (P.clip_c > 0.f) {
       const float l3 = -A * P.clip_c;
       const bool dual = (A < 0.f) && (l3 < pg);

@@ -81,6 +81,17 @@ def c_batch(b: PackedBatch) -> N.TgBatch:
     return c
 
 
+def _coupled_rows(cfg: RFTLossConfig, batch: PackedBatch, cb: N.TgBatch) -> None:
+    """Sequence-coupled losses take RL rollouts only (the C ABI refuses a
+    seq_kind array for them): SFT sequences are an error, an all-RL seq_kind
+    is dropped."""
+    if cfg.coupled:
+        if batch.n_sft_seqs > 0:
+            raise AlgorithmError(f"{cfg.policy_loss_fn} takes no SFT sequences "
+                                 f"({batch.n_sft_seqs} in the batch)")
+        cb.seq_kind = None
+
+
 @dataclass
 class LossOutput:
     stats: torch.Tensor                   # [32] float64 (layout _native.STAT_NAMES)
@@ -134,14 +145,20 @@ def stats_to_metrics(s: Dict[str, float], check: bool = True) -> Dict[str, float
 
 
 class _Workspace:
-    def __init__(self):
-        self.buf: Dict[int, torch.Tensor] = {}
+    """One workspace per (device, stream), allocated ON that stream: the caching
+    allocator then only recycles it (or a grown-out buffer) for work ordered
+    after the kernels that use it on the same stream."""
 
-    def get(self, dev: torch.device, nbytes: int) -> torch.Tensor:
-        key = dev.index if dev.index is not None else torch.cuda.current_device()
+    def __init__(self):
+        self.buf: Dict[tuple, torch.Tensor] = {}
+
+    def get(self, dev: torch.device, nbytes: int, stream: torch.cuda.Stream) -> torch.Tensor:
+        key = (dev.index if dev.index is not None else torch.cuda.current_device(),
+               stream.cuda_stream)
         t = self.buf.get(key)
         if t is None or t.numel() < nbytes:
-            t = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
+            with torch.cuda.stream(stream):
+                t = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
             self.buf[key] = t
         return t
 
@@ -166,6 +183,14 @@ class RFTLoss:
             cc.flags |= N.TG_FLAG_UNSCALED_GRAD
         return N.lib().tg_route(ctypes.byref(c_batch(batch)), ctypes.byref(cc))
 
+    def cluster_size(self, batch: PackedBatch, unscaled: bool = False) -> int:
+        """CL of the k_fused_tma<T, CL> instantiation this batch runs on (0 = a
+        streaming route); introspection for tests and benchmarks."""
+        cc = self.cfg.to_c()
+        if unscaled:
+            cc.flags |= N.TG_FLAG_UNSCALED_GRAD
+        return N.lib().tg_fused_cluster_size(ctypes.byref(c_batch(batch)), ctypes.byref(cc))
+
     def __call__(self, batch: PackedBatch, dlogits: Union[str, torch.Tensor, None] = "new", *,
                  n_tok_global: int = 0, n_seq_global: int = 0, n_sft_seq_global: int = 0,
                  out: Optional[LossOutput] = None, stream: Optional[torch.cuda.Stream] = None,
@@ -185,25 +210,31 @@ class RFTLoss:
         cc = cfg.to_c(n_tok_global, n_seq_global, n_sft_seq_global)
         if unscaled:
             cc.flags |= N.TG_FLAG_UNSCALED_GRAD
+        _coupled_rows(cfg, batch, cb)
         dev = batch.device
         T, B = batch.n_rows, batch.n_seqs
-        if out is None:
-            f32 = dict(dtype=torch.float32, device=dev)
-            out = LossOutput(stats=torch.empty(N.NSTAT, dtype=torch.float64, device=dev),
-                             lp=torch.empty(T, **f32), entropy=torch.empty(T, **f32),
-                             lse=torch.empty(T, **f32), seq_lp=torch.empty(B, **f32),
-                             seq_adv=torch.empty(B, **f32))
-        if isinstance(dlogits, str):
-            if dlogits == "inplace":
-                if batch.row_index is not None:
-                    raise ValueError("in-place dlogits needs logits rows == trainable rows")
-                dz = batch.logits
-            elif dlogits == "new":
-                dz = torch.empty((T, batch.vocab), dtype=batch.logits.dtype, device=dev)
+        # outputs and workspace are allocated on the launch stream (see _Workspace)
+        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        with torch.cuda.stream(s):
+            if out is None:
+                f32 = dict(dtype=torch.float32, device=dev)
+                out = LossOutput(stats=torch.empty(N.NSTAT, dtype=torch.float64, device=dev),
+                                 lp=torch.empty(T, **f32), entropy=torch.empty(T, **f32),
+                                 lse=torch.empty(T, **f32), seq_lp=torch.empty(B, **f32),
+                                 seq_adv=torch.empty(B, **f32))
+            if isinstance(dlogits, str):
+                if dlogits == "inplace":
+                    if batch.row_index is not None:
+                        raise ValueError("in-place dlogits needs logits rows == trainable rows")
+                    dz = batch.logits
+                elif dlogits == "new":
+                    dz = torch.empty((T, batch.vocab), dtype=batch.logits.dtype, device=dev)
+                else:
+                    raise ValueError(f"dlogits must be 'inplace', 'new', None or a tensor")
             else:
-                raise ValueError(f"dlogits must be 'inplace', 'new', None or a tensor")
-        else:
-            dz = dlogits
+                dz = dlogits
+            if unscaled and (out.row_coef is None or out.row_coef.shape != (3, T)):
+                out.row_coef = torch.empty(3, T, dtype=torch.float32, device=dev)
         co = N.TgOut()
         if dz is not None:
             if dz.dtype != batch.logits.dtype or dz.device != dev or dz.stride(1) != 1:
@@ -215,12 +246,9 @@ class RFTLoss:
         co.seq_lp, co.seq_adv, co.stats = (out.seq_lp.data_ptr(), out.seq_adv.data_ptr(),
                                            out.stats.data_ptr())
         if unscaled:
-            if out.row_coef is None or out.row_coef.shape != (3, T):
-                out.row_coef = torch.empty(3, T, dtype=torch.float32, device=dev)
             co.row_coef = out.row_coef.data_ptr()
         nbytes = L.tg_workspace_size(ctypes.byref(cb), ctypes.byref(cc))
-        ws = self._ws.get(dev, nbytes)
-        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        ws = self._ws.get(dev, nbytes, s)
         with torch.cuda.device(dev):
             N.check(L.tg_loss_fwd_bwd(ctypes.byref(cb), ctypes.byref(cc), ctypes.byref(co),
                                       ws.data_ptr(), ws.numel(), s.cuda_stream))
@@ -244,6 +272,7 @@ class RFTLoss:
             n_seq_global = batch.n_seqs
         cc = cfg.to_c(n_tok_global, n_seq_global, n_sft_seq_global)
         cc.flags |= N.TG_FLAG_ROWS_GIVEN
+        _coupled_rows(cfg, batch, cb)
         dev = batch.device
         T, B = batch.n_rows, batch.n_seqs
         for name, t in (("lp", lp), ("entropy", entropy), ("lse", lse)):
@@ -251,19 +280,21 @@ class RFTLoss:
                     not t.is_contiguous():
                 raise ValueError(f"{name} must be a contiguous float32 [{T}] tensor on {dev}")
         f32 = dict(dtype=torch.float32, device=dev)
-        out = LossOutput(stats=torch.empty(N.NSTAT, dtype=torch.float64, device=dev), lp=lp,
-                         entropy=entropy, lse=lse, seq_lp=torch.empty(B, **f32),
-                         seq_adv=torch.empty(B, **f32))
+        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        with torch.cuda.stream(s):
+            out = LossOutput(stats=torch.empty(N.NSTAT, dtype=torch.float64, device=dev), lp=lp,
+                             entropy=entropy, lse=lse, seq_lp=torch.empty(B, **f32),
+                             seq_adv=torch.empty(B, **f32))
+            if row_coef:
+                out.row_coef = torch.empty(3, T, **f32)
         co = N.TgOut()
         co.lp, co.entropy, co.lse = lp.data_ptr(), entropy.data_ptr(), lse.data_ptr()
         co.seq_lp, co.seq_adv, co.stats = (out.seq_lp.data_ptr(), out.seq_adv.data_ptr(),
                                            out.stats.data_ptr())
         if row_coef:
-            out.row_coef = torch.empty(3, T, **f32)
             co.row_coef = out.row_coef.data_ptr()
         nbytes = L.tg_workspace_size(ctypes.byref(cb), ctypes.byref(cc))
-        ws = self._ws.get(dev, nbytes)
-        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        ws = self._ws.get(dev, nbytes, s)
         with torch.cuda.device(dev):
             N.check(L.tg_loss_fwd_bwd(ctypes.byref(cb), ctypes.byref(cc), ctypes.byref(co),
                                       ws.data_ptr(), ws.numel(), s.cuda_stream))
@@ -278,14 +309,15 @@ def logprob_fwd(batch: PackedBatch, stream: Optional[torch.cuda.Stream] = None):
     cb = c_batch(batch)
     dev = batch.device
     f32 = dict(dtype=torch.float32, device=dev)
-    lp, ent, lse = (torch.empty(batch.n_rows, **f32) for _ in range(3))
-    seq_lp = torch.empty(batch.n_seqs, **f32)
+    nbytes = L.tg_workspace_size(ctypes.byref(cb), None)
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    with torch.cuda.stream(s):  # outputs + workspace belong to the launch stream
+        lp, ent, lse = (torch.empty(batch.n_rows, **f32) for _ in range(3))
+        seq_lp = torch.empty(batch.n_seqs, **f32)
+        ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
     co = N.TgOut()
     co.lp, co.entropy, co.lse, co.seq_lp = (lp.data_ptr(), ent.data_ptr(), lse.data_ptr(),
                                             seq_lp.data_ptr())
-    nbytes = L.tg_workspace_size(ctypes.byref(cb), None)
-    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
-    s = stream if stream is not None else torch.cuda.current_stream(dev)
     with torch.cuda.device(dev):
         N.check(L.tg_logprob_fwd(ctypes.byref(cb), ctypes.byref(co), ws.data_ptr(), ws.numel(),
                                  s.cuda_stream))
@@ -307,17 +339,18 @@ def lmhead_logprob_fwd(hidden: torch.Tensor, weight: torch.Tensor,
     T, d = hidden.shape
     V = weight.shape[0]
     f32 = dict(dtype=torch.float32, device=dev)
-    ent, lse = torch.empty(T, **f32), torch.empty(T, **f32)
-    lp = tgt = None
-    if target is not None:
-        tgt = target.to(device=dev, dtype=torch.int32).contiguous()
-        if tgt.shape != (T,):
-            raise ValueError(f"target must have shape ({T},)")
-        lp = torch.empty(T, **f32)
     s = stream if stream is not None else torch.cuda.current_stream(dev)
+    with torch.cuda.stream(s):  # outputs + workspace belong to the launch stream
+        ent, lse = torch.empty(T, **f32), torch.empty(T, **f32)
+        lp = tgt = None
+        if target is not None:
+            tgt = target.to(device=dev, dtype=torch.int32).contiguous()
+            if tgt.shape != (T,):
+                raise ValueError(f"target must have shape ({T},)")
+            lp = torch.empty(T, **f32)
+        ws = torch.empty(max(L.tg_lmhead_workspace_size(T, V), 16), dtype=torch.uint8,
+                         device=dev)
     with torch.cuda.device(dev):
-        nbytes = L.tg_lmhead_workspace_size(T, V)
-        ws = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
         N.check(L.tg_lmhead_logprob_fwd(
             hidden.data_ptr(), hidden.stride(0), weight.data_ptr(), weight.stride(0), T, V, d,
             tgt.data_ptr() if tgt is not None else None, lp.data_ptr() if lp is not None else None,
@@ -352,16 +385,18 @@ def lmhead_dlogits(hidden: torch.Tensor, weight: torch.Tensor, target: torch.Ten
     dev = hidden.device
     T, d = hidden.shape
     V = weight.shape[0]
-    if out is None:  # row pitch a multiple of 8 elements (16-byte vector stores)
-        out = torch.empty(T, (n_cols + 7) // 8 * 8, dtype=torch.bfloat16, device=dev)[:, :n_cols]
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    with torch.cuda.stream(s):
+        if out is None:  # row pitch a multiple of 8 elements (16-byte vector stores)
+            out = torch.empty(T, (n_cols + 7) // 8 * 8, dtype=torch.bfloat16,
+                              device=dev)[:, :n_cols]
+        tgt = target.to(device=dev, dtype=torch.int32).contiguous()
     if out.dtype != torch.bfloat16 or out.shape != (T, n_cols) or out.stride(1) != 1:
         raise ValueError(f"out must be a bf16 [{T}, {n_cols}] tensor with unit column stride")
-    tgt = target.to(device=dev, dtype=torch.int32).contiguous()
     for name, t, shape in (("lse", lse, (T,)), ("row_coef", row_coef, (3, T))):
         if t.dtype != torch.float32 or t.shape != shape or not t.is_contiguous() or \
                 t.device != dev:
             raise ValueError(f"{name} must be a contiguous float32 {list(shape)} tensor on {dev}")
-    s = stream if stream is not None else torch.cuda.current_stream(dev)
     with torch.cuda.device(dev):
         N.check(L.tg_lmhead_dlogits(
             hidden.data_ptr(), hidden.stride(0), weight.data_ptr(), weight.stride(0), T, V, d,

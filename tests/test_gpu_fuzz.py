@@ -37,6 +37,9 @@ def draw(seed):
               tau=float(r.choice([0.5, 1.0])) if coupled else float(r.choice([0.0, 0.5])),
               clip_lo=0.2, clip_hi=float(r.choice([0.2, 0.28])),
               clip_c=float(r.choice([0.0, 3.0])) if pg == "ppo_clip" else 0.0)
+    if coupled:  # the coupled losses take no token KL / entropy bonus / aggregation
+        kw.update(kl_fn="none", kl_coef=0.0, entropy_loss_fn="none", entropy_coef=0.0,
+                  loss_agg_mode="seq-sum")
     anchor = bool(r.random() < 0.3)
     if anchor:
         kw["anchor_beta"] = float(r.choice([0.1, 0.5]))

@@ -119,6 +119,17 @@ def _dummy_batch():
     (lambda b, c: setattr(b, "dtype", 7), N.TG_EINVAL),
     (lambda b, c: setattr(c, "clip_c", 0.5), N.TG_EINVAL),
     (lambda b, c: None, N.TG_EWORKSPACE),                             # workspace too small
+    # sequence-coupled losses refuse token-level terms instead of dropping them
+    (lambda b, c: (setattr(c, "policy_loss_fn", N.TG_PG_OPMD_KIMI), setattr(c, "tau", 1.0),
+                   setattr(c, "loss_agg_mode", 0), setattr(c, "kl_fn", N.TG_KL_K3),
+                   setattr(c, "kl_coef", 0.1)), N.TG_EINVAL),
+    (lambda b, c: (setattr(c, "policy_loss_fn", N.TG_PG_DPO), setattr(c, "loss_agg_mode", 0),
+                   setattr(c, "entropy_loss_fn", N.TG_ENT_DEFAULT),
+                   setattr(c, "entropy_coef", 0.01)), N.TG_EINVAL),
+    (lambda b, c: (setattr(c, "policy_loss_fn", N.TG_PG_OPMD_PAIRWISE), setattr(c, "tau", 1.0),
+                   setattr(c, "loss_agg_mode", N.TG_AGG_TOKEN_MEAN)), N.TG_EINVAL),
+    (lambda b, c: (setattr(c, "policy_loss_fn", N.TG_PG_OPMD_PAIRWISE), setattr(c, "tau", 1.0),
+                   setattr(c, "loss_agg_mode", 0), setattr(b, "seq_kind", 0x1000)), N.TG_EINVAL),
 ])
 def test_validation_mirrors_reference_errors(mut, code):
     L = N.lib()
@@ -147,6 +158,16 @@ def test_config_validation_and_registry():
         ("opmd", "vanilla", "seq-sum", 0.2)
     assert RFTLossConfig.from_variant("SFT").loss_agg_mode == "seq-mean-token-sum"
     assert RFTLossConfig.from_variant("DPO").coupled
+    # coupled losses: aggregation defaults to the reference's group sum, and
+    # token-level terms are refused rather than silently dropped
+    assert RFTLossConfig(policy_loss_fn="opmd_kimi", tau=1.0).loss_agg_mode == "seq-sum"
+    assert RFTLossConfig().loss_agg_mode == "token-mean"
+    for bad in (dict(kl_fn="k3", kl_coef=0.1), dict(entropy_loss_fn="default", entropy_coef=0.01),
+                dict(loss_agg_mode="token-mean")):
+        for pg in ("opmd_kimi", "opmd_pairwise", "dpo"):
+            with pytest.raises(AlgorithmError):
+                RFTLossConfig(policy_loss_fn=pg, tau=1.0, **bad)
+    RFTLossConfig(policy_loss_fn="dpo", kl_fn="k3", kl_coef=0.0)  # a zero coefficient is no term
 
 
 def test_lmhead_and_update_argument_validation():

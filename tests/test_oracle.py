@@ -314,6 +314,22 @@ def test_dual_clip_counts_and_zero_gradient():
     _fd_check(b, cfg)
 
 
+def test_ppo_log_ratio_clamp_has_no_gradient():
+    """|lp - old| > 20: the ratio is clamped like torch.clamp, so the row has
+    no policy gradient even on the unclipped (A < 0, rho >> 1) branch."""
+    b = _small_batch(4)
+    b.old_lp = b.old_lp - 25.0
+    b.reward = -np.abs(b.reward) - 1.0  # reinforce: A < 0 everywhere
+    cfg = O.Config(advantage_fn="reinforce", policy_loss_fn="ppo_clip", loss_agg_mode="seq-sum")
+    out = O.general_loss(b, cfg)
+    assert np.all(out["s"] == 0.0) and np.all(out["dz"] == 0.0)
+    assert out["stats"][O.STAT["clip_count"]] == 0
+    _fd_check(b, cfg)
+    dz = np.zeros_like(b.logits)
+    O.single_pass_blocked(b, cfg, dz_out=dz)
+    assert np.all(dz == 0.0)
+
+
 @pytest.mark.parametrize("cfg", [
     O.Config(advantage_fn="grpo", policy_loss_fn="ppo_clip", kl_fn="k3", kl_coef=0.1,
              entropy_loss_fn="default", entropy_coef=0.05, loss_agg_mode="token-mean"),
