@@ -60,6 +60,20 @@ def c_batch(b: PackedBatch) -> N.TgBatch:
         _check_dev(getattr(b, name), dev, name, torch.float32)
     _check_dev(b.seq_kind, dev, "seq_kind", torch.uint8)
     _check_dev(b.row_index, dev, "row_index", torch.int64)
+    # element counts the C ABI cannot see (plain pointers; ranges of device
+    # values are the packer's job -- checking them here would sync)
+    T, B, G = b.n_rows, b.n_seqs, b.n_groups
+    for name, n in (("target", T), ("seq_offsets", B + 1), ("group_offsets", G + 1),
+                    ("reward", B), ("old_lp", T), ("ref_lp", T), ("seq_ref_lp", B),
+                    ("advantage", B), ("seq_kind", B), ("row_index", T)):
+        t = getattr(b, name)
+        if t is not None and t.numel() != n:
+            raise ValueError(f"{name} has {t.numel()} entries, expected {n}")
+    if b.row_index is None and lg.numel() and lg.shape[0] < T:
+        raise ValueError(f"logits has {lg.shape[0]} rows for {T} trainable rows")
+    if b.anchor_logits is not None and (b.anchor_logits.shape[0] < T or
+                                        b.anchor_logits.shape[1] < b.vocab):
+        raise ValueError("anchor_logits must hold one row of >= vocab columns per trainable row")
     c = N.TgBatch()
     c.dtype = _DTYPES[lg.dtype]
     c.n_seqs, c.n_groups = b.n_seqs, b.n_groups

@@ -99,6 +99,27 @@ def pack_arrays(logits: torch.Tensor, target, seq_lengths, group_sizes, reward, 
     if T and (target.min() < 0 or target.max() >= V):
         bad = int(target[(target < 0) | (target >= V)][0])
         raise PolicyError(f"token {bad} outside vocabulary of size {V}")
+    # shapes the C ABI cannot check (plain pointers): a short array would be
+    # read out of bounds on the device, a long one silently misaligned
+    for name, arr, n in (("reward", reward, B), ("seq_ref_lp", seq_ref_lp, B),
+                         ("advantage", advantage, B), ("seq_kind", kind, B),
+                         ("old_lp", old_lp, T), ("ref_lp", ref_lp, T)):
+        if arr is not None and int(np.size(arr)) != n:
+            raise AlgorithmError(f"{name} has {int(np.size(arr))} entries, expected {n} "
+                                 f"({'one per sequence' if n == B else 'one per trainable row'})")
+    n_logit_rows = int(logits.shape[0]) if logits.dim() == 2 else 0
+    if row_index is not None:
+        row_index = np.asarray(row_index, dtype=np.int64)
+        if row_index.shape != (T,):
+            raise AlgorithmError(f"row_index has {row_index.size} entries, expected {T}")
+        if T and logits.numel() and (row_index.min() < 0 or row_index.max() >= n_logit_rows):
+            raise AlgorithmError(f"row_index outside the {n_logit_rows} logits rows")
+    elif logits.numel() and n_logit_rows < T:
+        raise AlgorithmError(f"{n_logit_rows} logits rows for {T} trainable rows")
+    if anchor_logits is not None:
+        if anchor_logits.dim() != 2 or anchor_logits.shape[0] < T or anchor_logits.shape[1] < V:
+            raise AlgorithmError(f"anchor_logits {tuple(anchor_logits.shape)} must cover "
+                                 f"[{T}, {V}] (one row per trainable row)")
     return PackedBatch(
         logits=logits, target=_i32(target, dev), seq_offsets=_i32(so, dev),
         group_offsets=_i32(go, dev), reward=_f32(reward, dev), old_lp=_f32(old_lp, dev),

@@ -220,3 +220,32 @@ def test_rows_given_flag_validation():
     o.dlogits, o.ld_out = 16, 100
     rc = L.tg_loss_fwd_bwd(ctypes.byref(b), ctypes.byref(cfg), ctypes.byref(o), None, 0, None)
     assert rc == N.TG_EINVAL and b"forward-only" in L.tg_last_error()
+
+
+def test_pack_arrays_rejects_misshaped_side_inputs():
+    """Host-side shape checks the C ABI cannot do: short arrays
+    would be read out of bounds on the device, long ones silently misaligned."""
+    import torch
+    from paper_2505_17826_b200 import pack_arrays
+
+    logits = torch.zeros(10, 16)
+    tgt = np.arange(10) % 16
+    ok = dict(old_lp=np.zeros(10), ref_lp=np.zeros(10), seq_ref_lp=np.zeros(3),
+              advantage=np.zeros(3), seq_kind=[0, 0, 1])
+    b = pack_arrays(logits, tgt, [4, 3, 3], [3], np.zeros(3), **ok)
+    assert (b.n_rows, b.n_seqs, b.n_sft_seqs) == (10, 3, 1)
+    for name, bad in (("old_lp", np.zeros(30)), ("ref_lp", np.zeros(9)),
+                      ("seq_ref_lp", np.zeros(2)), ("advantage", np.zeros(10)),
+                      ("seq_kind", [0, 1])):
+        with pytest.raises(AlgorithmError, match=name):
+            pack_arrays(logits, tgt, [4, 3, 3], [3], np.zeros(3), **{**ok, name: bad})
+    with pytest.raises(AlgorithmError, match="reward"):
+        pack_arrays(logits, tgt, [4, 3, 3], [3], np.zeros(4))
+    with pytest.raises(AlgorithmError, match="row_index"):
+        pack_arrays(logits, tgt, [4, 3, 3], [3], np.zeros(3), row_index=np.arange(10) + 1)
+    with pytest.raises(AlgorithmError, match="row_index"):
+        pack_arrays(logits, tgt, [4, 3, 3], [3], np.zeros(3), row_index=np.arange(9))
+    with pytest.raises(AlgorithmError, match="logits rows"):
+        pack_arrays(logits[:8], tgt, [4, 3, 3], [3], np.zeros(3))
+    with pytest.raises(AlgorithmError, match="anchor_logits"):
+        pack_arrays(logits, tgt, [4, 3, 3], [3], np.zeros(3), anchor_logits=torch.zeros(10, 8))
