@@ -54,7 +54,7 @@
 extern "C" {
 #endif
 
-#define TG_ABI_VERSION 2
+#define TG_ABI_VERSION 3
 
 /* return codes */
 enum { TG_OK = 0, TG_EINVAL = 1, TG_ECUDA = 2, TG_EUNSUPPORTED = 3, TG_EWORKSPACE = 4 };
@@ -78,7 +78,12 @@ enum {
   TG_PG_SFT = 2,            /* -lp (NLL)                          algorithms.py:256-274  */
   TG_PG_OPMD_KIMI = 3,      /* sum_i (r_i - zeta - tau(LP_i - ref_i))^2   :118-153       */
   TG_PG_OPMD_PAIRWISE = 4,  /* sum_{i<j} (a_i - a_j)^2                    :156-190       */
-  TG_PG_DPO = 5             /* mean softplus(-beta margin); groups are (chosen, rejected) */
+  TG_PG_DPO = 5,            /* mean softplus(-beta margin); groups are (chosen, rejected) */
+  TG_PG_GIVEN = 6           /* caller-supplied per-row policy loss l_t (TgBatch.pg_loss) and
+                               coefficient -d l_t / d lp_t (TgBatch.pg_coef): a policy loss
+                               registered from Python, evaluated on the rows' lp before the
+                               call; weighted by the aggregation weight like the built-ins,
+                               token KL / entropy / SFT rows / anchor KL unchanged      */
 };
 /* The sequence-coupled losses (OPMD_KIMI, OPMD_PAIRWISE, DPO) are whole-sequence
    objectives: with them kl_fn / kl_coef, the entropy bonus, a loss_agg_mode other
@@ -179,6 +184,8 @@ typedef struct TgBatch {
                                     (records.py:119-121)                                 */
   const float* advantage;        /* [B] for TG_ADV_GIVEN                                 */
   const uint8_t* seq_kind;       /* optional [B]: 0 RL rollout, 1 SFT / expert           */
+  const float* pg_coef;          /* [T] for TG_PG_GIVEN: -d l_t / d lp_t (unweighted)     */
+  const float* pg_loss;          /* [T] for TG_PG_GIVEN: l_t (unweighted)                 */
 } TgBatch;
 
 typedef struct TgOut {

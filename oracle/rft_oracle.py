@@ -56,6 +56,8 @@ class Batch:
     seq_kind: Optional[np.ndarray] = None     # [B] 0 = RL rollout, 1 = SFT / expert
     anchor_logits: Optional[np.ndarray] = None  # [T, V] frozen anchor policy rows
     advantage: Optional[np.ndarray] = None    # [B] precomputed (advantage_fn "given")
+    pg_coef: Optional[np.ndarray] = None      # [T] -d l_t / d lp_t (policy_loss_fn "given")
+    pg_loss: Optional[np.ndarray] = None      # [T] l_t (policy_loss_fn "given")
 
     @property
     def n_rows(self) -> int:
@@ -80,6 +82,7 @@ class Batch:
 class Config:
     advantage_fn: str = "grpo"        # grpo | rloo | opmd | reinforce | given
     policy_loss_fn: str = "ppo_clip"  # vanilla | ppo_clip | sft | opmd_kimi | opmd_pairwise | dpo
+    #                                   | given (a caller-registered per-row loss + coefficient)
     kl_fn: str = "none"               # none | k1 | k2 | k3 (low_var_kl) | abs
     entropy_loss_fn: str = "none"     # none | default
     loss_agg_mode: str = "token-mean"  # seq-sum | token-mean | seq-mean-token-sum |
@@ -540,6 +543,9 @@ def general_loss(batch: Batch, cfg: Config, want_dz: bool = True) -> Dict[str, o
         elif pg == "sft":
             pg_t = -lp
             s_pg = np.ones(T)
+        elif pg == "given":  # a registered Python policy loss, evaluated by the caller
+            pg_t = np.asarray(batch.pg_loss, np.float64)
+            s_pg = np.asarray(batch.pg_coef, np.float64)
         else:
             raise ValueError(f"unknown policy_loss_fn {pg}")
         kl_t = np.zeros(T)

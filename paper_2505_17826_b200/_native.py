@@ -18,7 +18,7 @@ TG_OK, TG_EINVAL, TG_ECUDA, TG_EUNSUPPORTED, TG_EWORKSPACE = 0, 1, 2, 3, 4
 TG_DTYPE_BF16, TG_DTYPE_F32 = 0, 1
 TG_ADV_GIVEN, TG_ADV_GRPO, TG_ADV_RLOO, TG_ADV_OPMD, TG_ADV_REINFORCE = 0, 1, 2, 3, 4
 (TG_PG_VANILLA, TG_PG_PPO_CLIP, TG_PG_SFT, TG_PG_OPMD_KIMI, TG_PG_OPMD_PAIRWISE,
- TG_PG_DPO) = 0, 1, 2, 3, 4, 5
+ TG_PG_DPO, TG_PG_GIVEN) = 0, 1, 2, 3, 4, 5, 6
 TG_KL_NONE, TG_KL_K1, TG_KL_K2, TG_KL_K3, TG_KL_ABS = 0, 1, 2, 3, 4
 TG_ENT_NONE, TG_ENT_DEFAULT = 0, 1
 (TG_AGG_SEQ_SUM, TG_AGG_TOKEN_MEAN, TG_AGG_SEQ_MEAN_TOKEN_SUM, TG_AGG_SEQ_MEAN_TOKEN_MEAN,
@@ -60,6 +60,7 @@ class TgBatch(ctypes.Structure):
         ("target", c_void_p), ("old_lp", c_void_p), ("ref_lp", c_void_p),
         ("seq_offsets", c_void_p), ("group_offsets", c_void_p), ("reward", c_void_p),
         ("seq_ref_lp", c_void_p), ("advantage", c_void_p), ("seq_kind", c_void_p),
+        ("pg_coef", c_void_p), ("pg_loss", c_void_p),
     ]
 
 
@@ -78,7 +79,7 @@ EXPORTED = [
     "tg_lmhead_workspace_size", "tg_apply_update", "tg_lmhead_dlogits", "tg_fused_cluster_size",
 ]
 
-ABI_VERSION = 2  # include/tg_loss.h TG_ABI_VERSION
+ABI_VERSION = 3  # include/tg_loss.h TG_ABI_VERSION
 
 _lib = None
 

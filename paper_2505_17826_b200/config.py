@@ -101,6 +101,16 @@ class RFTLossConfig:
     def coupled(self) -> bool:
         return self.policy_loss_fn in COUPLED
 
+    @property
+    def advantage_callable(self):
+        """The registered Python advantage function, or None for a built-in."""
+        return ADVANTAGE_FNS[self.advantage_fn].fn
+
+    @property
+    def policy_loss_callable(self):
+        """The registered Python policy loss, or None for a built-in."""
+        return POLICY_LOSS_FNS[self.policy_loss_fn].fn
+
     @classmethod
     def from_variant(cls, variant, tau: float = 1.0, beta: float = 0.0,
                      dpo_beta: float = 0.1) -> "RFTLossConfig":

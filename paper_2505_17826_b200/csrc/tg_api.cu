@@ -185,7 +185,7 @@ int validate_cfg(const TgBatch* b, const TgConfig* c) {
   if (!c) return fail(TG_EINVAL, "config is NULL");
   if (c->advantage_fn < TG_ADV_GIVEN || c->advantage_fn > TG_ADV_REINFORCE)
     return fail(TG_EINVAL, "unknown advantage_fn %d", c->advantage_fn);
-  if (c->policy_loss_fn < TG_PG_VANILLA || c->policy_loss_fn > TG_PG_DPO)
+  if (c->policy_loss_fn < TG_PG_VANILLA || c->policy_loss_fn > TG_PG_GIVEN)
     return fail(TG_EINVAL, "unknown policy_loss_fn %d", c->policy_loss_fn);
   if (c->kl_fn < TG_KL_NONE || c->kl_fn > TG_KL_ABS)
     return fail(TG_EINVAL, "unknown kl_fn %d", c->kl_fn);
@@ -220,6 +220,8 @@ int validate_cfg(const TgBatch* b, const TgConfig* c) {
     if (b->seq_kind || c->n_sft_seq_global > 0)
       return fail(TG_EINVAL, "sequence-coupled losses take no SFT rows (seq_kind must be NULL)");
   }
+  if (c->policy_loss_fn == TG_PG_GIVEN && b->n_rows > 0 && (!b->pg_coef || !b->pg_loss))
+    return fail(TG_EINVAL, "policy_loss_fn GIVEN requires batch.pg_coef and batch.pg_loss");
   if (c->advantage_fn == TG_ADV_GIVEN &&
       (c->policy_loss_fn == TG_PG_VANILLA || c->policy_loss_fn == TG_PG_PPO_CLIP) &&
       b->n_seqs > 0 && !b->advantage)
@@ -250,6 +252,8 @@ void fill_params(KParams& P, const TgBatch* b, const TgConfig* c, const TgOut* o
   P.seq_ref_lp = b->seq_ref_lp;
   P.advantage = b->advantage;
   P.seq_kind = b->seq_kind;
+  P.pg_coef = b->pg_coef;
+  P.pg_loss = b->pg_loss;
   P.dz = o ? o->dlogits : nullptr;
   P.lp = (o && o->lp) ? o->lp : reinterpret_cast<float*>(ws + L.lp);
   P.ent = (o && o->entropy) ? o->entropy : reinterpret_cast<float*>(ws + L.ent);

@@ -40,6 +40,8 @@ struct KParams {
   const float* seq_ref_lp;
   const float* advantage;
   const uint8_t* seq_kind;
+  const float* pg_coef;  // TG_PG_GIVEN: caller's per-row -d l / d lp and l
+  const float* pg_loss;
   // outputs (never null after tg_api resolves them to workspace)
   void* dz;
   float* lp;

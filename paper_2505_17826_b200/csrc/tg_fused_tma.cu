@@ -233,6 +233,10 @@ __device__ __forceinline__ RowMeta row_meta(const KParams& P, int64_t row, int& 
   m.w = P.sW[seq];
   m.old = P.old_lp ? P.old_lp[row] : 0.f;
   m.ref = P.ref_lp ? P.ref_lp[row] : 0.f;
+  if (P.pg == TG_PG_GIVEN) {  // the caller's per-row coefficient / loss (see k_rowmeta)
+    m.A = P.pg_coef[row];
+    m.old = P.pg_loss[row];
+  }
   const bool rl = P.seq_kind == nullptr || P.seq_kind[seq] == 0;
   const bool bad = m.y < 0 || int64_t(m.y) >= P.vocab;
   m.flags = (rl ? 1u : 0u) | (bad ? 2u : 0u);

@@ -3,8 +3,9 @@
 //  k_counts     batch-wide RL row / sequence counts (token-mean denominators)
 //               and group-shape validation (pairwise K >= 2, DPO K == 2)
 //  k_prep       K2: group-relative advantage + aggregation weight per sequence,
-//               one thread per group (K is small; f64 arithmetic like the
-//               reference's Python floats):
+//               a warp-per-group segmented reduction (lanes stride over the
+//               group's sequences, f64 butterfly sums -- the same bits on every
+//               lane and every run; f64 like the reference's Python floats):
 //                 OPMD   (r - rbar) / (1 + tau)            algorithms.py:234-242
 //                 GRPO   (r - mean) / (std + eps)          north_star
 //                 RLOO   r_i - mean_{j != i} r_j           north_star
@@ -14,7 +15,7 @@
 //               algorithms.py:81-85) and the resolved reference logprob
 //               (records.py:119-121 default)
 //  k_coupled    K3: group-coupled coefficients of OPMD_KIMI (algorithms.py:139-146),
-//               OPMD_PAIRWISE (172-183) and DPO (299-308)
+//               OPMD_PAIRWISE (172-183) and DPO (299-308), warp per group
 //  k_finalize   deterministic fixed-order reduction of the per-CTA partial
 //               stats + group metrics (combine_reports, algorithms.py:368-379)
 #include <math.h>
@@ -57,29 +58,41 @@ __global__ void k_counts(const KParams P) {
   if (threadIdx.x < 4) P.counts[threadIdx.x] = int64_t(c[threadIdx.x]);
 }
 
-// group g's advantages and aggregation weights (per sequence) and metrics
-__device__ void prep_group(const KParams& P, int g, int64_t n_tok, int64_t n_seq,
-                           int64_t n_sft) {
+__device__ __forceinline__ int warp_sum_i(int v) { return __reduce_add_sync(0xffffffffu, v); }
+
+__device__ __forceinline__ double warp_max_d(double v) {
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, d));
+  return v;
+}
+
+// K2, warp per group: group g's advantages and aggregation weights (per
+// sequence) and metrics.  All 32 lanes call it for the same g; the group's
+// RL rewards are reduced with f64 butterflies (identical on every lane).
+__device__ void prep_group_warp(const KParams& P, int g, int lane, int64_t n_tok, int64_t n_seq,
+                                int64_t n_sft) {
   const int a = P.grp_off[g], b = P.grp_off[g + 1];
   double sum = 0.0;
   int k = 0;
-  for (int i = a; i < b; ++i)
+  for (int i = a + lane; i < b; i += 32)
     if (is_rl(P, i)) {
       sum += double(P.reward[i]);
       ++k;
     }
+  sum = warp_sum_d(sum);
+  k = warp_sum_i(k);
   const double mean = k > 0 ? sum / k : 0.0;
   double var = 0.0;
   if (P.adv == TG_ADV_GRPO && k > 1) {
-    for (int i = a; i < b; ++i)
+    for (int i = a + lane; i < b; i += 32)
       if (is_rl(P, i)) {
         const double d = double(P.reward[i]) - mean;
         var += d * d;
       }
-    var /= double(k - 1);
+    var = warp_sum_d(var) / double(k - 1);
   }
   const double sd = sqrt(var);
-  for (int i = a; i < b; ++i) {
+  for (int i = a + lane; i < b; i += 32) {
     const double r = double(P.reward[i]);
     double A = 0.0, w;
     const int n_i = P.seq_off[i + 1] - P.seq_off[i];
@@ -108,22 +121,26 @@ __device__ void prep_group(const KParams& P, int g, int64_t n_tok, int64_t n_seq
     P.sK[i] = float(b - a);
     if (P.seq_adv) P.seq_adv[i] = float(A);
   }
-  P.gF[4 * g + 0] = mean;
-  P.gF[4 * g + 1] = mean;
-  P.gF[4 * g + 2] = 0.0;
-  P.gF[4 * g + 3] = double(k);
+  if (lane == 0) {
+    P.gF[4 * g + 0] = mean;
+    P.gF[4 * g + 1] = mean;
+    P.gF[4 * g + 2] = 0.0;
+    P.gF[4 * g + 3] = double(k);
+  }
 }
 
+// multi-CTA form (batches beyond one CTA's 32 warps x 64 groups): warp per group
 __global__ void k_prep(const KParams P) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (g >= P.n_groups) return;
-  prep_group(P, g, P.n_tok_g > 0 ? P.n_tok_g : P.counts[0],
-             P.n_seq_g > 0 ? P.n_seq_g : P.counts[1], P.n_sft_g > 0 ? P.n_sft_g : P.counts[2]);
+  prep_group_warp(P, g, threadIdx.x & 31, P.n_tok_g > 0 ? P.n_tok_g : P.counts[0],
+                  P.n_seq_g > 0 ? P.n_seq_g : P.counts[1],
+                  P.n_sft_g > 0 ? P.n_sft_g : P.counts[2]);
 }
 
 // k_counts + k_prep in one CTA (one launch instead of two on every call):
-// the batch counts are reduced in shared memory, then the threads stride over
-// the groups.
+// the batch counts are reduced in shared memory, then the 32 warps take the
+// groups one warp per group.
 __global__ void __launch_bounds__(1024) k_counts_prep(const KParams P) {
   __shared__ unsigned long long c[4];
   if (threadIdx.x < 4) c[threadIdx.x] = 0;
@@ -154,7 +171,9 @@ __global__ void __launch_bounds__(1024) k_counts_prep(const KParams P) {
   const int64_t n_tok = P.n_tok_g > 0 ? P.n_tok_g : int64_t(c[0]);
   const int64_t n_seq = P.n_seq_g > 0 ? P.n_seq_g : int64_t(c[1]);
   const int64_t n_sft = P.n_sft_g > 0 ? P.n_sft_g : int64_t(c[2]);
-  for (int g = threadIdx.x; g < P.n_groups; g += blockDim.x) prep_group(P, g, n_tok, n_seq, n_sft);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int g = warp; g < P.n_groups; g += blockDim.x >> 5)
+    prep_group_warp(P, g, lane, n_tok, n_seq, n_sft);
 }
 
 // one warp per sequence
@@ -169,8 +188,10 @@ __global__ void k_rowmeta(const KParams P, RowMeta* __restrict__ meta) {
   for (int r = a + lane; r < b; r += 32) {
     const int32_t y = P.target[r];
     const bool bad = (y < 0) || (int64_t(y) >= P.vocab);
-    int4 m0 = make_int4(y, i, __float_as_int(A), __float_as_int(w));
-    int4 m1 = make_int4(__float_as_int(P.old_lp ? P.old_lp[r] : 0.f),
+    // TG_PG_GIVEN: the caller's per-row coefficient / loss ride in the A / old slots
+    const bool given = P.pg == TG_PG_GIVEN;
+    int4 m0 = make_int4(y, i, __float_as_int(given ? P.pg_coef[r] : A), __float_as_int(w));
+    int4 m1 = make_int4(__float_as_int(given ? P.pg_loss[r] : (P.old_lp ? P.old_lp[r] : 0.f)),
                         __float_as_int(P.ref_lp ? P.ref_lp[r] : 0.f),
                         int((rl ? 1u : 0u) | (bad ? 2u : 0u)), __float_as_int(ca));
     int4* dst = reinterpret_cast<int4*>(meta + r);
@@ -206,61 +227,72 @@ __device__ __forceinline__ double sigmoid_d(double x) {
   return e / (1.0 + e);
 }
 
-// one thread per group
+// K3, warp per group: lanes stride over the group's sequences, f64 butterflies
 __global__ void k_coupled(const KParams P) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (g >= P.n_groups) return;
   const int a = P.grp_off[g], b = P.grp_off[g + 1];
   const int k = b - a;
   const double tau = double(P.tau);
   double mean = 0.0;
-  for (int i = a; i < b; ++i) mean += double(P.reward[i]);
+  for (int i = a + lane; i < b; i += 32) mean += double(P.reward[i]);
+  mean = warp_sum_d(mean);
   mean = k > 0 ? mean / k : 0.0;
   double loss = 0.0, baseline = mean, aux = double(k);
   if (P.pg == TG_PG_OPMD_KIMI && k > 0) {
     double m = -INFINITY;
-    for (int i = a; i < b; ++i) m = fmax(m, double(P.reward[i]));
+    for (int i = a + lane; i < b; i += 32) m = fmax(m, double(P.reward[i]));
+    m = warp_max_d(m);
     double me = 0.0;
-    for (int i = a; i < b; ++i) me += exp((double(P.reward[i]) - m) / tau);
+    for (int i = a + lane; i < b; i += 32) me += exp((double(P.reward[i]) - m) / tau);
+    me = warp_sum_d(me);
     const double zhat = m + tau * log(me / k);  // tau_log_zhat, algorithms.py:93-101
     baseline = zhat;
-    for (int i = a; i < b; ++i) {
+    for (int i = a + lane; i < b; i += 32) {
       const double res = double(P.reward[i]) - zhat - tau * (P.sLP[i] - P.sRef[i]);
       loss += res * res;
       P.sA[i] = float(2.0 * tau * res);
     }
+    loss = warp_sum_d(loss);
   } else if (P.pg == TG_PG_OPMD_PAIRWISE && k >= 2) {
+    // sum_{i<j} (a_i - a_j)^2 = k sum_i (a_i - abar)^2 (centred: no cancellation)
     double tot = 0.0;
-    for (int i = a; i < b; ++i) tot += double(P.reward[i]) - tau * (P.sLP[i] - P.sRef[i]);
-    for (int i = a; i < b; ++i) {
+    for (int i = a + lane; i < b; i += 32) tot += double(P.reward[i]) - tau * (P.sLP[i] - P.sRef[i]);
+    tot = warp_sum_d(tot);
+    const double abar = tot / double(k);
+    for (int i = a + lane; i < b; i += 32) {
       const double ai = double(P.reward[i]) - tau * (P.sLP[i] - P.sRef[i]);
-      for (int j = i + 1; j < b; ++j) {
-        const double d = ai - (double(P.reward[j]) - tau * (P.sLP[j] - P.sRef[j]));
-        loss += d * d;
-      }
-      P.sA[i] = float(2.0 * tau * (double(k) * ai - tot));
+      loss += (ai - abar) * (ai - abar);
+      P.sA[i] = float(2.0 * tau * double(k) * (ai - abar));
     }
+    loss = double(k) * warp_sum_d(loss);
   } else if (P.pg == TG_PG_DPO && k == 2) {
     const double n = P.n_seq_g > 0 ? double(P.n_seq_g / 2) : double(P.n_groups);
     const double beta = double(P.dpo_beta);
     const double margin = beta * ((P.sLP[a] - P.sRef[a]) - (P.sLP[a + 1] - P.sRef[a + 1]));
     loss = softplus_d(-margin) / n;
     const double s = (1.0 - sigmoid_d(margin)) * beta / n;
-    P.sA[a] = float(s);
-    P.sA[a + 1] = float(-s);
+    if (lane == 0) {
+      P.sA[a] = float(s);
+      P.sA[a + 1] = float(-s);
+    }
     baseline = 0.0;
     aux = margin;
   } else {
-    for (int i = a; i < b; ++i) P.sA[i] = 0.f;
+    for (int i = a + lane; i < b; i += 32) P.sA[i] = 0.f;
   }
-  for (int i = a; i < b; ++i) {
+  __syncwarp();
+  for (int i = a + lane; i < b; i += 32) {
     P.sW[i] = 1.f;
     if (P.seq_adv) P.seq_adv[i] = P.sA[i];
   }
-  P.gF[4 * g + 0] = mean;
-  P.gF[4 * g + 1] = baseline;
-  P.gF[4 * g + 2] = loss;
-  P.gF[4 * g + 3] = aux;
+  if (lane == 0) {
+    P.gF[4 * g + 0] = mean;
+    P.gF[4 * g + 1] = baseline;
+    P.gF[4 * g + 2] = loss;
+    P.gF[4 * g + 3] = aux;
+  }
 }
 
 // single CTA of 256 threads; fixed reduction order => deterministic stats
@@ -339,16 +371,16 @@ __global__ void k_finalize(const KParams P, int coupled) {
 
 // ---------------------------------------------------------------------------
 
-// counts + group prep: one CTA for batches of up to 8,192 groups (every
+// counts + group prep: one CTA for batches of up to 2,048 groups (every
 // realistic micro-batch), two kernels beyond
 int launch_group_prep(const KParams& P, bool coupled, cudaStream_t st) {
   (void)coupled;  // coupled variants get neutral per-sequence values now, A after the forward
-  if (P.n_groups <= 8192) {
+  if (P.n_groups <= 2048) {  // <= 64 groups per warp of the single CTA
     k_counts_prep<<<1, 1024, 0, st>>>(P);
     return 1;
   }
   k_counts<<<1, 256, 0, st>>>(P);
-  k_prep<<<(P.n_groups + 127) / 128, 128, 0, st>>>(P);
+  k_prep<<<(P.n_groups + 7) / 8, 256, 0, st>>>(P);
   return 2;
 }
 
@@ -362,7 +394,7 @@ void launch_seq_reduce(const KParams& P, cudaStream_t st) {
 }
 
 void launch_coupled(const KParams& P, cudaStream_t st) {
-  if (P.n_groups > 0) k_coupled<<<(P.n_groups + 127) / 128, 128, 0, st>>>(P);
+  if (P.n_groups > 0) k_coupled<<<(P.n_groups + 7) / 8, 256, 0, st>>>(P);
 }
 
 void launch_finalize(const KParams& P, bool coupled, cudaStream_t st) {

@@ -30,7 +30,7 @@ struct RowTerms {
 struct __align__(16) RowMeta {
   int32_t y, seq;
   float A, w;
-  float old, ref;
+  float old, ref;   // TG_PG_GIVEN: A = caller's -d l / d lp, old = caller's l
   uint32_t flags;  // bit0: RL row, bit1: target outside [0, V)
   float ca;        // anchor KL coefficient beta / K of the row's group (0 = none)
 };
@@ -91,6 +91,9 @@ __device__ __forceinline__ RowTerms meta_terms(const KParams& P, const RowMeta& 
   } else if (P.pg == TG_PG_SFT) {
     pg = -lp;
     s_pg = 1.f;
+  } else if (P.pg == TG_PG_GIVEN) {  // RowMeta carries the caller's l_t in `old`, -dl/dlp in `A`
+    pg = m.old;
+    s_pg = A;
   } else {
     pg = -A * lp;
     s_pg = A;

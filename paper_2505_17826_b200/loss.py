@@ -56,7 +56,7 @@ def c_batch(b: PackedBatch) -> N.TgBatch:
     _check_dev(b.seq_offsets, dev, "seq_offsets", torch.int32)
     _check_dev(b.group_offsets, dev, "group_offsets", torch.int32)
     _check_dev(b.reward, dev, "reward", torch.float32)
-    for name in ("old_lp", "ref_lp", "seq_ref_lp", "advantage"):
+    for name in ("old_lp", "ref_lp", "seq_ref_lp", "advantage", "pg_coef", "pg_loss"):
         _check_dev(getattr(b, name), dev, name, torch.float32)
     _check_dev(b.seq_kind, dev, "seq_kind", torch.uint8)
     _check_dev(b.row_index, dev, "row_index", torch.int64)
@@ -65,7 +65,8 @@ def c_batch(b: PackedBatch) -> N.TgBatch:
     T, B, G = b.n_rows, b.n_seqs, b.n_groups
     for name, n in (("target", T), ("seq_offsets", B + 1), ("group_offsets", G + 1),
                     ("reward", B), ("old_lp", T), ("ref_lp", T), ("seq_ref_lp", B),
-                    ("advantage", B), ("seq_kind", B), ("row_index", T)):
+                    ("advantage", B), ("seq_kind", B), ("row_index", T), ("pg_coef", T),
+                    ("pg_loss", T)):
         t = getattr(b, name)
         if t is not None and t.numel() != n:
             raise ValueError(f"{name} has {t.numel()} entries, expected {n}")
@@ -92,6 +93,7 @@ def c_batch(b: PackedBatch) -> N.TgBatch:
     c.seq_offsets, c.group_offsets = b.seq_offsets.data_ptr(), b.group_offsets.data_ptr()
     c.reward = b.reward.data_ptr()
     c.seq_ref_lp, c.advantage, c.seq_kind = _ptr(b.seq_ref_lp), _ptr(b.advantage), _ptr(b.seq_kind)
+    c.pg_coef, c.pg_loss = _ptr(b.pg_coef), _ptr(b.pg_loss)
     return c
 
 
@@ -188,6 +190,63 @@ class RFTLoss:
     def __init__(self, cfg: Optional[RFTLossConfig] = None, **kw):
         self.cfg = cfg if cfg is not None else RFTLossConfig(**kw)
         self._ws = _Workspace()
+        self._probe: Optional["RFTLoss"] = None
+
+    # ---- registered Python components (registry.register_*) -------------------
+
+    def _plugins(self, batch: PackedBatch, s: torch.cuda.Stream, glob: dict,
+                 rows=None) -> PackedBatch:
+        """Run the config's registered Python components on the batch's device
+        and return the batch with their outputs attached: ``advantage``
+        (TG_ADV_GIVEN) and ``pg_coef`` / ``pg_loss`` (TG_PG_GIVEN)."""
+        from dataclasses import replace
+
+        from .registry import AdvantageInputs, PolicyLossInputs
+        adv_fn, pg_fn = self.cfg.advantage_callable, self.cfg.policy_loss_callable
+        if adv_fn is None and pg_fn is None:
+            return batch
+        dev, B, T = batch.device, batch.n_seqs, batch.n_rows
+        with torch.cuda.stream(s):
+            seq_len = (batch.seq_offsets[1:] - batch.seq_offsets[:-1]).to(torch.int32)
+            if adv_fn is not None:
+                grp = torch.repeat_interleave(
+                    torch.arange(batch.n_groups, device=dev),
+                    (batch.group_offsets[1:] - batch.group_offsets[:-1]).long(), output_size=B)
+                is_rl = (torch.ones(B, dtype=torch.bool, device=dev) if batch.seq_kind is None
+                         else batch.seq_kind == 0)
+                a = adv_fn(AdvantageInputs(reward=batch.reward, group_index=grp,
+                                           group_offsets=batch.group_offsets, seq_lengths=seq_len,
+                                           is_rl=is_rl, n_groups=batch.n_groups, config=self.cfg))
+                a = torch.as_tensor(a, device=dev).to(torch.float32).reshape(-1).contiguous()
+                if a.numel() != B:
+                    raise AlgorithmError(f"advantage_fn {self.cfg.advantage_fn!r} returned "
+                                         f"{a.numel()} values for {B} sequences")
+                batch = replace(batch, advantage=a)
+            if pg_fn is not None:
+                # forward pass (2V bytes / row): lp, entropy and the sequence advantages
+                if self._probe is None:
+                    self._probe = RFTLoss(self.cfg.with_(policy_loss_fn="vanilla", kl_fn="none",
+                                                         entropy_loss_fn="none", anchor_beta=0.0))
+                if rows is None:
+                    fwd = self._probe(batch, dlogits=None, stream=s, **glob)
+                else:  # per-row lp / entropy / lse given (LM-head path): no logits pass
+                    fwd = self._probe.from_rows(batch, *rows, stream=s, **glob)
+                seq = torch.repeat_interleave(torch.arange(B, device=dev), seq_len.long(),
+                                              output_size=T)
+                lp = fwd.lp.detach().clone().requires_grad_(True)
+                with torch.enable_grad():
+                    loss_t = pg_fn(PolicyLossInputs(
+                        lp=lp, old_lp=batch.old_lp, ref_lp=batch.ref_lp,
+                        advantage=fwd.seq_adv[seq], entropy=fwd.entropy, seq_index=seq,
+                        config=self.cfg))
+                    if not torch.is_tensor(loss_t) or loss_t.shape != (T,):
+                        raise AlgorithmError(f"policy_loss_fn {self.cfg.policy_loss_fn!r} must "
+                                             f"return one loss per row ([{T}])")
+                    (g,) = torch.autograd.grad(loss_t.sum(), lp, allow_unused=True)
+                coef = (torch.zeros_like(lp) if g is None else -g).detach().float().contiguous()
+                batch = replace(batch, pg_coef=coef,
+                                pg_loss=loss_t.detach().float().contiguous())
+        return batch
 
     def route(self, batch: PackedBatch, unscaled: bool = False) -> int:
         """1 = fused single pass, 2 = forward+backward streaming, 3 = sequence-coupled,
@@ -217,6 +276,12 @@ class RFTLoss:
         d loss / d z_t = row_scale[t] * dlogits[t] -- for a caller that folds
         the row scale into its LM-head backward."""
         L = N.lib()
+        dev = batch.device
+        # outputs and workspace are allocated on the launch stream (see _Workspace)
+        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        batch = self._plugins(batch, s, dict(n_tok_global=n_tok_global,
+                                             n_seq_global=n_seq_global,
+                                             n_sft_seq_global=n_sft_seq_global))
         cb = c_batch(batch)
         cfg = self.cfg
         if cfg.coupled and cfg.policy_loss_fn == "dpo" and n_seq_global == 0:
@@ -225,10 +290,7 @@ class RFTLoss:
         if unscaled:
             cc.flags |= N.TG_FLAG_UNSCALED_GRAD
         _coupled_rows(cfg, batch, cb)
-        dev = batch.device
         T, B = batch.n_rows, batch.n_seqs
-        # outputs and workspace are allocated on the launch stream (see _Workspace)
-        s = stream if stream is not None else torch.cuda.current_stream(dev)
         with torch.cuda.stream(s):
             if out is None:
                 f32 = dict(dtype=torch.float32, device=dev)
@@ -280,6 +342,11 @@ class RFTLoss:
         also returns the per-row gradient coefficients ``out.row_coef`` [3, T]
         (a, hz, s: dz = p (a + hz z) - s [v = y]) for ``lmhead_dlogits``."""
         L = N.lib()
+        s = stream if stream is not None else torch.cuda.current_stream(batch.device)
+        batch = self._plugins(batch, s, dict(n_tok_global=n_tok_global,
+                                             n_seq_global=n_seq_global,
+                                             n_sft_seq_global=n_sft_seq_global),
+                              rows=(lp, entropy, lse))
         cb = c_batch(batch)
         cfg = self.cfg
         if cfg.coupled and cfg.policy_loss_fn == "dpo" and n_seq_global == 0:
@@ -294,7 +361,6 @@ class RFTLoss:
                     not t.is_contiguous():
                 raise ValueError(f"{name} must be a contiguous float32 [{T}] tensor on {dev}")
         f32 = dict(dtype=torch.float32, device=dev)
-        s = stream if stream is not None else torch.cuda.current_stream(dev)
         with torch.cuda.stream(s):
             out = LossOutput(stats=torch.empty(N.NSTAT, dtype=torch.float64, device=dev), lp=lp,
                              entropy=entropy, lse=lse, seq_lp=torch.empty(B, **f32),

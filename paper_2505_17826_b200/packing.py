@@ -46,6 +46,8 @@ class PackedBatch:
     seq_kind: Optional[torch.Tensor] = None   # [B] uint8 (0 RL, 1 SFT)
     anchor_logits: Optional[torch.Tensor] = None  # [T, ld_a]
     row_index: Optional[torch.Tensor] = None  # [T] int64
+    pg_coef: Optional[torch.Tensor] = None    # [T] f32 (registered policy loss: -d l / d lp)
+    pg_loss: Optional[torch.Tensor] = None    # [T] f32 (registered policy loss: l)
     vocab: int = 0
     # host-side shape facts (known to the packer; no device sync needed)
     n_rows: int = 0

@@ -52,6 +52,7 @@ int main(void) {
   printf("%d %d %d\n", TG_NSTAT, TG_S_INVALID, TG_S_SUM_ANCHOR_KL);
   printf("%zu %d %d %d %d\n", offsetof(TgOut, row_coef), TG_FLAG_FORCE_TWO_PASS,
          TG_FLAG_ROWS_GIVEN, TG_FLAG_UNSCALED_GRAD, TG_ABI_VERSION);
+  printf("%zu %d\n", offsetof(TgBatch, pg_loss), TG_PG_GIVEN);
   return 0;
 }'''
     with tempfile.TemporaryDirectory() as d:
@@ -75,6 +76,7 @@ int main(void) {
     assert (sizes[10], sizes[11], sizes[12]) == (N.TG_FLAG_FORCE_TWO_PASS, N.TG_FLAG_ROWS_GIVEN,
                                                  N.TG_FLAG_UNSCALED_GRAD)
     assert sizes[13] == N.ABI_VERSION
+    assert (sizes[14], sizes[15]) == (N.TgBatch.pg_loss.offset, N.TG_PG_GIVEN)
 
 
 @pytest.mark.parametrize("name", ["simple_tau05", "kimi", "pairwise", "simple_bf16_v512",
@@ -249,3 +251,38 @@ def test_pack_arrays_rejects_misshaped_side_inputs():
         pack_arrays(logits[:8], tgt, [4, 3, 3], [3], np.zeros(3))
     with pytest.raises(AlgorithmError, match="anchor_logits"):
         pack_arrays(logits, tgt, [4, 3, 3], [3], np.zeros(3), anchor_logits=torch.zeros(10, 8))
+
+
+def test_registry_user_components_and_errors():
+    """Python components lower to the GIVEN codes; names are unique; built-ins
+    cannot be shadowed or removed (no silent aliasing)."""
+    from paper_2505_17826_b200.registry import (register_advantage_fn, register_policy_loss_fn,
+                                                unregister)
+
+    @register_policy_loss_fn("cpu_test_pg", aliases=("cpu_test_pg_alias",))
+    def pg(x):
+        """doc"""
+        return -x.advantage * x.lp
+
+    @register_advantage_fn("cpu_test_adv")
+    def adv(x):
+        return x.reward
+
+    try:
+        cfg = RFTLossConfig(advantage_fn="cpu_test_adv", policy_loss_fn="cpu_test_pg_alias")
+        assert cfg.policy_loss_fn == "cpu_test_pg" and cfg.policy_loss_callable is pg
+        assert cfg.advantage_callable is adv
+        c = cfg.to_c()
+        assert (c.policy_loss_fn, c.advantage_fn) == (N.TG_PG_GIVEN, N.TG_ADV_GIVEN)
+        assert RFTLossConfig().policy_loss_callable is None
+        with pytest.raises(ValueError, match="already registered"):
+            register_policy_loss_fn("ppo_clip")(pg)
+        with pytest.raises(ValueError, match="already registered"):
+            register_advantage_fn("x", aliases=("grpo",))(adv)
+        assert "x" not in ADVANTAGE_FNS  # nothing half-registered
+        with pytest.raises(ValueError, match="built-in"):
+            unregister(POLICY_LOSS_FNS, "ppo_clip")
+    finally:
+        unregister(POLICY_LOSS_FNS, "cpu_test_pg")
+        unregister(ADVANTAGE_FNS, "cpu_test_adv")
+    assert "cpu_test_pg_alias" not in POLICY_LOSS_FNS
