@@ -15,22 +15,30 @@ per-micro-batch targets are shared, rewards / old / ref logprobs differ.
 Every micro-batch still streams its full 2V bytes per row in and 2V out:
 the working set (80 GB) is ~600x the 126 MB L2, so no L2 flush is needed.
 
-One process per GPU (torchrun for N > 1); each rank processes its own
-1,048,576-row batch (weak scaling) and NCCL allreduces only the 32-double
-statistics vector per step.  `value` = rows of all ranks / max-over-ranks
-device time.  `e2e` = the same metric through the public API with pinned
-HOST logits: H2D of the logits + metadata and D2H of dlogits + stats inside
-the timed region, one e2e step = the same 1,048,576 rows (64 calls, 3-deep
-copy / compute overlap).
+One process per GPU.  `--gpus N` without a torchrun environment re-launches
+itself under `torch.distributed.run` with N ranks (NCCL; with fewer visible
+GPUs than ranks the ranks share devices over gloo -- plumbing only, and the
+line says so).  configs[1] / [0] / [3] are weak-scaled (each rank its own
+batch of that shape); configs[2] (`--variant c3`, 128 x 8 x 4096) and
+configs[4] (`--variant c5`, 256 x 16 ragged <= 8192) are ONE global batch
+whose whole groups are LPT-sharded over the ranks by row count
+(distributed.shard_groups), strong-scaled.  The only collective on the loss
+path is the 32-double statistics allreduce per step.  `value` = rows of all
+ranks / max-over-ranks device time.  `e2e` = the same metric through the public
+API with pinned HOST logits: H2D of the logits + metadata and D2H of dlogits
++ stats inside the timed region, one e2e step = the same 1,048,576 rows (64
+calls, 3-deep copy / compute overlap), its results checked against the
+device path.
 
-`--variant c1|c3|c4|c5` runs the per-GPU workloads of BASELINE configs[0],
-[2], [3], [4] (V = 32,000; PPO + k3 + entropy at 4,096 tokens; GRPO + SFT mix;
-ragged long-CoT through row_index); `grpo_two_pass`, `opmd_kimi`,
-`opmd_pairwise` measure the two-pass / sequence-coupled routes,
-`opmd_kimi_unscaled` / `opmd_pairwise_unscaled` the single-pass coupled route
-(unscaled gradient + per-row scales) and `anchor` the fused regularizer_g path
-(6V bytes per row).  Kernel A/B: TG_LOSS_LIB selects a library build
-(scripts/gpu_libab.sh).
+`--impl reference` times the reference's own CPU loss path -- triad's
+group_loss + combine_reports (OPMD_SIMPLE, its GRPO analogue) staged under
+oracle/_ref by oracle/stage_ref.sh -- on all host cores; `cpu_baseline` the
+same on one core (the numpy port when the reference is not staged).
+
+Other variants: `grpo_two_pass`, `opmd_kimi`, `opmd_pairwise` (two-pass /
+sequence-coupled routes), `opmd_kimi_unscaled` / `opmd_pairwise_unscaled`
+(single-pass coupled route), `anchor` (fused regularizer_g, 6V bytes per row),
+`sft`.  Kernel A/B: TG_LOSS_LIB selects a library build (scripts/gpu_libab.sh).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--variant V]
@@ -39,9 +47,9 @@ ragged long-CoT through row_index); `grpo_two_pass`, `opmd_kimi`,
 from __future__ import annotations
 
 import argparse
-import ctypes
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -59,26 +67,26 @@ UNIT = "tokens/s"
 V = 151936
 BUMP = 13.5
 # behaviour-policy logprob = lp + N(0, sigma^2).  SURVEY.md 8(d) asks for a PPO
-# clip fraction of about 5-20 % at eps = 0.2 / 0.28; its sigma = 0.05 gives
-# ~0 % (ratios within exp(+-0.15)), sigma = 0.15 gives ~6 %.
+# clip fraction of about 5-20 % at eps = 0.2 / 0.28; sigma = 0.15 gives ~6 %.
 OLD_LP_SIGMA = 0.15
-ALGO_BYTES_PER_ROW = 4 * V + 24  # 2V read + 2V write + 24 B side data
 WORKLOAD = "grpo_ppo_clip_k3_token_mean_qwen2.5_1.5b_shapes"
 VARIANT_WORKLOAD = {
     "grpo": WORKLOAD,
     "c1": "configs[0]: GRPO loss, 8 prompts x 8 x 512 tokens, vocab 32,000 (the CPU "
-          "reference's case) on 1 GPU",
-    "c3": "configs[2] per-GPU shard: ppo_clip_k3_entropy, 16 prompts x 8 x 4096 tokens "
-          "(128 x 8 over 8 GPUs)",
-    "c4": "configs[3]: mixed GRPO + SFT NLL (50/50 sequences) at configs[1] shapes",
-    "c5": "configs[4] per-GPU shard: long-CoT 32 groups x 16 ragged responses <= 8192, "
-          "10 % interior mask-false spans, row_index gather (256 x 16 over 8 GPUs)",
+          "reference's case) per GPU",
+    "c3": "configs[2]: ppo_clip_k3_entropy, ONE global batch of 128 prompts x 8 x 4096 tokens "
+          "sharded over the GPUs by whole groups",
+    "c4": "configs[3]: mixed GRPO + SFT NLL (50/50 sequences) at configs[1] shapes per GPU",
+    "c5": "configs[4]: long-CoT, ONE global batch of 256 groups x 16 ragged responses <= 8191, "
+          "10 % interior mask-false spans, LPT-sharded over the GPUs, packed on the device "
+          "(tg_pack_rows, HF shift) and read in place through row_index",
 }
 _BASE_LOSS = "grpo adv + ppo_clip(0.2,0.28) + low_var_kl(0.001) + token-mean"
 VARIANT_LOSS = {"grpo": _BASE_LOSS, "c1": _BASE_LOSS, "c3": _BASE_LOSS + " + entropy(0.001)",
                 "c4": _BASE_LOSS + " on RL seqs + SFT NLL (weight 1) on expert seqs",
                 "c5": _BASE_LOSS,
                 "anchor": "opmd_simple(tau 1) + regularizer_g anchor KL (beta 0.1), fused (6V)"}
+GLOBAL_SHARDED = ("c3", "c5")   # one global batch, LPT-sharded (strong scaling)
 
 
 def parse():
@@ -95,27 +103,35 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--e2e-groups", type=int, default=0,
                    help="groups per e2e step (0 = the whole step's groups, as the device metric)")
-    p.add_argument("--cpu-rows", type=int, default=256)
+    p.add_argument("--cpu-resp-len", type=int, default=384,
+                   help="response tokens per sequence of the 1-core reference sample (8 seqs)")
+    p.add_argument("--ref-resp-len", type=int, default=64,
+                   help="response tokens per sequence of each reference-arm worker's group")
     p.add_argument("--quiet", action="store_true")
     p.add_argument("--variant", default="grpo",
                    choices=["grpo", "grpo_two_pass", "opmd_kimi", "opmd_pairwise", "sft",
                             "opmd_kimi_unscaled", "opmd_pairwise_unscaled", "anchor",
                             "c1", "c3", "c4", "c5"],
-                   help="loss variant (the headline metric is 'grpo' = configs[1]; c3 / c4 / c5 "
-                        "are the per-GPU shards of BASELINE configs[2..4]; the others measure "
+                   help="loss variant (the headline metric is 'grpo' = configs[1]; c1 / c3 / "
+                        "c4 / c5 are BASELINE configs[0], [2], [3], [4]; the others measure "
                         "the two-pass / sequence-coupled routes)")
     a = p.parse_args()
-    global V, BUMP, ALGO_BYTES_PER_ROW
-    # per-GPU shards of the multi-GPU configs (weak scaling: fixed work per GPU)
+    global V, BUMP
     if a.variant == "c1":    # configs[0]: the CPU oracle's case, 8 x 8 x 512 at V = 32,000
         V, BUMP = 32000, 12.0
-        ALGO_BYTES_PER_ROW = 4 * V + 24
         a.groups, a.group_size, a.resp_len, a.mb_groups = 8, 8, 512, 8
-    elif a.variant == "c3":    # configs[2]: 128 x 8 rollouts x 4096 tokens over 8 GPUs
-        a.groups, a.group_size, a.resp_len, a.mb_groups = 16, 8, 4096, 4
-    elif a.variant == "c5":  # configs[4]: 256 x 16 rollouts, <= 8192 ragged tokens, 8 GPUs
-        a.groups, a.group_size, a.resp_len, a.mb_groups = 32, 16, 8192, 2
+    elif a.variant == "c3":  # configs[2]: 128 x 8 rollouts x 4096 tokens, one global batch
+        a.groups, a.group_size, a.resp_len, a.mb_groups = 128, 8, 4096, 4
+    elif a.variant == "c5":  # configs[4]: 256 x 16 rollouts, <= 8191 ragged tokens
+        a.groups, a.group_size, a.resp_len, a.mb_groups = 256, 16, 8192, 2
     return a
+
+
+def algo_bytes_per_row(variant: str) -> int:
+    """SURVEY.md 8(d): single pass 4V + 24 (2V read + 2V write + side data);
+    two-pass / anchor-KL 6V + 24."""
+    six = variant in ("grpo_two_pass", "opmd_kimi", "opmd_pairwise", "anchor")
+    return (6 if six else 4) * V + 24
 
 
 def log(*a):
@@ -131,6 +147,20 @@ def peaks():
         except Exception:
             pass
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def traffic_of(variant: str):
+    """DRAM bytes per row of THIS variant's dominant kernel from its committed
+    `ncu --set full` capture (profiles/traffic.json), or None when that kernel
+    was never captured -- never another kernel's number."""
+    f = ROOT / "profiles" / "traffic.json"
+    try:
+        d = json.loads(f.read_text())[variant]
+        if int(d["vocab"]) == V:
+            return d
+    except Exception:
+        pass
+    return None
 
 
 # ---------------------------------------------------------------------------
@@ -200,9 +230,9 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the oracle port (numpy float64), bounded sample
+# CPU: the reference's own loss path (oracle/_ref), else the numpy port
 
-def cpu_sample(seed: int, rows: int, group_size: int):
+def _port_sample(seed: int, rows: int, group_size: int):
     from oracle import rft_oracle as O
     rng = np.random.default_rng(seed)
     per = max(1, rows // group_size)
@@ -212,75 +242,137 @@ def cpu_sample(seed: int, rows: int, group_size: int):
     x[np.arange(T), tgt] += BUMP
     x = x.astype(np.float32).astype(np.float64)
     lp = O.row_forward(x, tgt)[1]
-    b = O.Batch(logits=x, target=tgt, seq_offsets=np.arange(0, T + 1, per),
-                group_offsets=np.array([0, group_size]),
-                reward=rng.integers(0, 2, group_size).astype(np.float64),
-                old_lp=lp + rng.normal(0, OLD_LP_SIGMA, T), ref_lp=lp + rng.normal(0, 0.1, T))
-    return b
+    return O.Batch(logits=x, target=tgt, seq_offsets=np.arange(0, T + 1, per),
+                   group_offsets=np.array([0, group_size]),
+                   reward=rng.integers(0, 2, group_size).astype(np.float64),
+                   old_lp=lp + rng.normal(0, OLD_LP_SIGMA, T), ref_lp=lp + rng.normal(0, 0.1, T))
 
 
-def oracle_cfg():
-    from oracle import rft_oracle as O
-    return O.Config(advantage_fn="grpo", policy_loss_fn="ppo_clip", kl_fn="k3", kl_coef=0.001,
-                    loss_agg_mode="token-mean", clip_lo=0.2, clip_hi=0.28)
-
-
-def cpu_run(args_tuple):
+def _port_run(args_tuple):
+    """The numpy port (oracle/rft_oracle.single_pass_blocked) on the GPU arm's
+    exact loss -- used when the reference is not staged."""
     seed, rows, gsize = args_tuple
     from oracle import rft_oracle as O
-    b = cpu_sample(seed, rows, gsize)
+    b = _port_sample(seed, rows, gsize)
     dz = np.empty((b.n_rows, V), np.float32)
+    cfg = O.Config(advantage_fn="grpo", policy_loss_fn="ppo_clip", kl_fn="k3", kl_coef=0.001,
+                   loss_agg_mode="token-mean", clip_lo=0.2, clip_hi=0.28)
     t0 = time.perf_counter()
-    O.single_pass_blocked(b, oracle_cfg(), dz_out=dz, block=32)
-    return b.n_rows, time.perf_counter() - t0
+    O.single_pass_blocked(b, cfg, dz_out=dz, block=32)
+    return b.n_rows, time.perf_counter() - t0, 0.0
 
 
-def cpu_baseline(rows: int, gsize: int):
-    n, dt = cpu_run((1234, rows, gsize))
+def cpu_baseline(args):
+    """One core, bounded sample (~10-30 s): triad's group_loss + combine_reports."""
+    from oracle import ref_timing as R
+    K = args.group_size
+    if R.available():
+        n, dt, _ = R.run(1234, V, K, args.cpu_resp_len)
+        return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "reference",
+                "sample": f"triad (oracle/_ref) group_loss + combine_reports, OPMD_SIMPLE tau=1 "
+                          f"(the reference's GRPO analogue; it has no PPO / k3), 1 group x {K} "
+                          f"x {args.cpu_resp_len} mask-true tokens, V={V}, 1 process; "
+                          f"{dt:.2f} s"}
+    n, dt, _ = _port_run((1234, K * 32, K))
     return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "port",
             "sample": f"oracle/rft_oracle.single_pass_blocked (numpy f64, 1 thread) on {n} rows "
-                      f"x V={V} (1 group x {gsize} seqs), same loss config; {dt:.2f} s"}
+                      f"x V={V}, same loss config (reference not staged); {dt:.2f} s"}
 
 
 def run_reference(args):
-    """--impl reference: the oracle port on all host cores (the reference is
-    pure Python and cannot run on the GPU box)."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    """--impl reference: the reference's own CPU path on all host cores, rank 0
+    only (the other ranks exit without work)."""
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    if int(os.environ.get("RANK", "0")) != 0:
         return 0
     import multiprocessing as mp
-    cores = os.cpu_count() or 1
-    try:
-        avail = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
-    except Exception:
-        avail = 64 << 30
-    per_worker = args.cpu_rows * V * 4 * 8  # rough peak bytes of one worker
-    workers = max(1, min(cores, int(0.5 * avail // per_worker), 64))
-    ctx = mp.get_context("fork")
-    rates = []
-    with ctx.Pool(workers) as pool:
+
+    from oracle import ref_timing as R
+    K, Lr = args.group_size, args.ref_resp_len
+    staged = R.available()
+    if staged:
+        workers = R.pool_size(V, 64, K, Lr)
+        fn, task = R._worker, (lambda step, i: (1000 + 7919 * step + i, V, K, Lr))
+    else:
+        workers = max(1, min(os.cpu_count() or 1, 32))
+        fn, task = _port_run, (lambda step, i: (1000 + 7919 * step + i, K * 32, K))
+    rates, losses = [], []
+    with mp.get_context("fork").Pool(workers) as pool:
         for step in range(args.warmup + args.steps):
             t0 = time.perf_counter()
-            res = pool.map(cpu_run, [(1000 + step * workers + i, args.cpu_rows, args.group_size)
-                                     for i in range(workers)])
+            res = pool.map(fn, [task(step, i) for i in range(workers)])
             dt = time.perf_counter() - t0
             if step >= args.warmup:
                 rates.append(sum(r[0] for r in res) / dt)
+                losses.append(sum(r[2] for r in res))
     value = statistics.median(rates)
-    rows = workers * (args.cpu_rows // args.group_size) * args.group_size
+    rows = sum(r[0] for r in res)
+    if staged:
+        sample = (f"{workers} processes x (triad group_loss + combine_reports, OPMD_SIMPLE tau=1, "
+                  f"1 group x {K} x {Lr} mask-true tokens, V={V}) per step; triad from "
+                  f"oracle/_ref (the reference has no PPO / k3: its GRPO analogue)")
+    else:
+        sample = (f"{workers} processes x {K * 32} rows x V={V} of the numpy port per step "
+                  "(reference not staged: run oracle/stage_ref.sh)")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * rows / value,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": WORKLOAD, "vocab": V,
-                                        "sample_rows_per_step": rows},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
-                         "sample": f"{workers} processes x {args.cpu_rows} rows x V={V} of the "
-                                   "oracle port (numpy f64) per step"},
+        "data": "synthetic",
+        "config": {"workload": VARIANT_WORKLOAD.get(args.variant, args.variant), "vocab": V,
+                   "sample_rows_per_step": rows},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers,
+                         "kind": "reference" if staged else "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "check": {"sum_loss_last_step": float(losses[-1]) if losses else None},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+# ---------------------------------------------------------------------------
+# launcher
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(args) -> int:
+    """`--gpus N` outside torchrun: re-run this script as N ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    log("launching:", " ".join(cmd))
+    return subprocess.call(cmd)
+
+
+# ---------------------------------------------------------------------------
+# workload layout
+
+def global_layout(args):
+    """(seq_lengths [B], group_sizes [G], keep-masks or None) of the global batch
+    (sharded variants) or of one rank's batch (weak-scaled variants).  c5:
+    lognormal(ln 3000, 0.8) response lengths in [64, 8191] and ~10 % of each
+    response's target rows in interior mask-false spans of 8..64 (seeded; the
+    same on every rank)."""
+    G, K, Lr = args.groups, args.group_size, args.resp_len
+    if args.variant != "c5":
+        return np.full(G * K, Lr, np.int64), np.full(G, K, np.int64), None
+    rng = np.random.default_rng(1236)
+    L = np.clip(np.exp(rng.normal(np.log(3000.0), 0.8, G * K)), 64, Lr - 1).astype(int)
+    masks = []
+    for n in L:
+        m = np.ones(n, bool)
+        masked = 0
+        while masked < 0.1 * n:
+            run = int(rng.integers(8, 65))
+            start = int(rng.integers(0, max(1, n - run)))
+            masked += int(m[start:start + run].sum())
+            m[start:start + run] = False
+        masks.append(m)
+    return np.array([int(m.sum()) for m in masks], np.int64), np.full(G, K, np.int64), masks
 
 
 # ---------------------------------------------------------------------------
@@ -288,6 +380,9 @@ def run_reference(args):
 
 def main():
     args = parse()
+    world_env = os.environ.get("WORLD_SIZE")
+    if args.gpus > 1 and world_env is None:
+        return self_launch(args)
     if args.impl == "reference":
         return run_reference(args)
     import torch
@@ -295,30 +390,45 @@ def main():
 
     from paper_2505_17826_b200 import RFTLoss, RFTLossConfig, logprob_fwd, pack_arrays
     from paper_2505_17826_b200 import _native as N
-    from paper_2505_17826_b200.distributed import allreduce_stats
+    from paper_2505_17826_b200.distributed import allreduce_stats, group_rows, shard_groups
+    from paper_2505_17826_b200.packing import pack_token_batch
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = int(world_env or "1")
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    # one process per GPU; TG_BENCH_BACKEND=gloo lets a multi-rank smoke run share
-    # a single GPU (NCCL refuses two ranks on one device) -- plumbing only
-    backend = os.environ.get("TG_BENCH_BACKEND", "nccl")
-    if backend != "nccl":
-        local = local % torch.cuda.device_count()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    n_dev = torch.cuda.device_count()
+    # one process per GPU over NCCL.  More ranks than visible GPUs (a 1-GPU
+    # lease) share devices over gloo: the multi-rank plumbing, not a speed claim
+    shared = world > n_dev
+    backend = "gloo" if shared else os.environ.get("TG_BENCH_BACKEND", "nccl")
+    local = local % n_dev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # rank / channel count in the log
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
     L = N.lib()
+    if shared:  # several ranks on one device: keep every rank's buffers within HBM / world
+        args.mb_groups = max(1, args.mb_groups // world)
+        args.no_e2e = True
 
-    G, K, Lr = args.groups, args.group_size, args.resp_len
-    mbg = min(args.mb_groups, G)
-    n_mb = G // mbg
-    mb_rows = mbg * K * Lr  # logits buffer rows (c5: padded layout of the ragged batch)
-    B = G * K
+    K, Lr = args.group_size, args.resp_len
+    sharded = args.variant in GLOBAL_SHARDED
+    seq_len_g, gsize_g, masks_g = global_layout(args)
+    Gg = len(gsize_g)
+    if sharded:
+        my_groups = shard_groups(group_rows(seq_len_g, gsize_g), world)[rank]
+    else:
+        my_groups = list(range(Gg))
+    mbg = max(1, min(args.mb_groups, len(my_groups)))
+    chunks = [my_groups[i:i + mbg] for i in range(0, len(my_groups), mbg)]
+    n_mb = len(chunks)
+    mb_rows = mbg * K * Lr  # logits buffer rows (c5: the padded [seqs, 8192] layout)
     cfg = RFTLossConfig(advantage_fn="grpo", policy_loss_fn="ppo_clip", kl_fn="low_var_kl",
                         kl_coef=0.001, loss_agg_mode="token-mean", clip_lo=0.2, clip_hi=0.28)
     if args.variant == "grpo_two_pass":
@@ -338,7 +448,7 @@ def main():
     two_pass = args.variant in ("grpo_two_pass", "opmd_kimi", "opmd_pairwise")
     # coupled loss in one pass (TG_FLAG_UNSCALED_GRAD, route 4): p - e_y rows + row scales
     unscaled = args.variant.endswith("_unscaled")
-    algo_bytes_row = (6 * V + 24) if (two_pass or args.variant == "anchor") else ALGO_BYTES_PER_ROW
+    algo_bytes_row = algo_bytes_per_row(args.variant)
 
     # ---- resident synthetic inputs (outside timing) ----
     gen = torch.Generator(device=dev)
@@ -357,66 +467,72 @@ def main():
         for r0 in range(0, mb_rows, 8192):
             anchor[r0:r0 + 8192].normal_(0.0, 0.3, generator=gen)
             anchor[r0:r0 + 8192] += logits[r0:r0 + 8192]
-    lens = [Lr] * (mbg * K)
-    gsz = [K] * mbg
-    probe = pack_arrays(logits, tgt, lens, gsz, np.zeros(mbg * K, np.float32))
-    lp_true = logprob_fwd(probe)[0].cpu().numpy().astype(np.float64)
-
-    def mb_layout(m):
-        """(lens, row_index, seq_kind) of micro-batch m.  c5: ragged long-CoT
-        responses (lognormal lengths, 64..8192) with ~10 % of rows in interior
-        mask-false spans of 8..64 rows, read in place from the padded buffer
-        through row_index; c4: the second half of the groups are SFT sequences."""
-        if args.variant == "c5":
-            lrng = np.random.default_rng(1236 + 1000 * rank + m)
-            L = np.clip(np.exp(lrng.normal(np.log(3000.0), 0.8, mbg * K)), 64, Lr).astype(int)
-            keep = []
-            off = 0
-            for n in L:
-                mask = np.ones(n, bool)
-                masked = 0
-                while masked < 0.1 * n:
-                    run = int(lrng.integers(8, 65))
-                    start = int(lrng.integers(0, max(1, n - run)))
-                    masked += int(mask[start:start + run].sum())
-                    mask[start:start + run] = False
-                keep.append(np.nonzero(mask)[0] + off)
-                off += n
-            return [len(k) for k in keep], np.concatenate(keep), None
-        kind = None
-        if args.variant == "c4":
-            kind = np.repeat((np.arange(mbg) >= mbg // 2).astype(np.uint8), K)
-        return lens, None, kind
-
+    so_g = np.concatenate([[0], np.cumsum(gsize_g)])
+    lp_true = None
+    if args.variant != "c5":
+        probe = pack_arrays(logits, tgt, [Lr] * (mbg * K), [K] * mbg, np.zeros(mbg * K))
+        lp_true = logprob_fwd(probe)[0].cpu().numpy().astype(np.float64)
     batches, outs = [], []
     T = n_sft = 0
-    for m in range(n_mb):
-        rew = rng.integers(0, 2, mbg * K).astype(np.float32)
-        if m == 0:
+    for m, grp in enumerate(chunks):
+        seqs = np.concatenate([np.arange(so_g[g], so_g[g + 1]) for g in grp])
+        lens = seq_len_g[seqs]
+        gsz = gsize_g[grp]
+        rew = np.random.default_rng(1235 + 1000 * rank + m).integers(0, 2, len(seqs)).astype(
+            np.float32)
+        if m == 0 and rank == 0:
             rew[:K] = 1.0  # an all-equal group (A = 0, std = 0)
-        lens_m, ridx, kind = mb_layout(m)
-        rows = np.arange(mb_rows) if ridx is None else ridx
-        old = (lp_true[rows] + rng.normal(0, OLD_LP_SIGMA, rows.size)).astype(np.float32)
-        ref = (lp_true[rows] + rng.normal(0, 0.1, rows.size)).astype(np.float32)
-        b = pack_arrays(logits, tgt[rows], lens_m, gsz, rew, old_lp=old, ref_lp=ref,
-                        seq_kind=kind, row_index=ridx, anchor_logits=anchor)
+        if args.variant == "c5":
+            # the LLM layout [seqs, 8192]: target position l >= 1 of sequence b is
+            # scored by logits row b * 8192 + l - 1; packed on the device
+            B_mb = len(seqs)
+            mask = np.zeros((B_mb, Lr), bool)
+            for j, i in enumerate(seqs):
+                full = masks_g[i]
+                mask[j, 1:1 + full.size] = full
+            ids = torch.randint(0, V, (B_mb, Lr), device=dev, generator=gen)
+            b = pack_token_batch(logits[:B_mb * Lr], ids, torch.as_tensor(mask, device=dev),
+                                 rew, list(gsz))
+            lp0 = logprob_fwd(b)[0]
+            noise = torch.randn((2, b.n_rows), device=dev, generator=gen)
+            b.old_lp = (lp0 + OLD_LP_SIGMA * noise[0]).contiguous()
+            b.ref_lp = (lp0 + 0.1 * noise[1]).contiguous()
+            assert b.n_rows == int(lens.sum())
+        else:
+            rows_m = int(lens.sum())
+            kind = None
+            if args.variant == "c4":
+                kind = np.repeat((np.arange(len(grp)) >= len(grp) // 2).astype(np.uint8), K)
+            old = (lp_true[:rows_m] + rng.normal(0, OLD_LP_SIGMA, rows_m)).astype(np.float32)
+            ref = (lp_true[:rows_m] + rng.normal(0, 0.1, rows_m)).astype(np.float32)
+            b = pack_arrays(logits, tgt[:rows_m], lens, gsz, rew, old_lp=old, ref_lp=ref,
+                            seq_kind=kind, anchor_logits=anchor)
+            n_sft += 0 if kind is None else int(kind.sum())
         batches.append(b)
         outs.append(None)
-        T += int(rows.size)
-        n_sft += 0 if kind is None else int(kind.sum())
+        T += b.n_rows
     route = loss.route(batches[0], unscaled=unscaled)
     assert route == (4 if unscaled else
                      1 if not two_pass else (2 if args.variant == "grpo_two_pass" else 3)), route
-    # (anchor: route 1 = the fused anchor path, 6V bytes per row)
-    n_tok_g, n_seq_g, n_sft_g = world * T, world * B, world * n_sft
-    stats_all = torch.zeros((n_mb, N.NSTAT), dtype=torch.float64, device=dev)
+    cl = loss.cluster_size(batches[0], unscaled=unscaled)
+    # global denominators (token-mean's N_tok, sequence means, SFT): host-side
+    if sharded:
+        n_tok_g, n_seq_g, n_sft_g = int(seq_len_g.sum()), len(seq_len_g), 0
+    else:
+        n_tok_g, n_seq_g, n_sft_g = world * T, world * int(len(seq_len_g)), world * n_sft
+    rows_rank = torch.zeros(world, dtype=torch.float64, device=dev)
+    rows_rank[rank] = T
+    if world > 1:
+        dist.all_reduce(rows_rank)
+    rows_rank = rows_rank.cpu().numpy()
+    T_all = float(rows_rank.sum())
 
     def step():
         for m in range(n_mb):
             outs[m] = loss(batches[m], dlogits=dz, n_tok_global=n_tok_g, n_seq_global=n_seq_g,
                            n_sft_seq_global=n_sft_g, out=outs[m], unscaled=unscaled)
-        st = torch.stack([o.stats for o in outs]).sum(0)
-        return allreduce_stats(st)
+        st = outs[0].stats if n_mb == 1 else torch.stack([o.stats for o in outs]).sum(0)
+        return allreduce_stats(st.clone())
 
     for _ in range(args.warmup):
         st = step()
@@ -449,7 +565,8 @@ def main():
             k += 1
             outs[m] = loss(batches[m], dlogits=dz, n_tok_global=n_tok_g, n_seq_global=n_seq_g,
                            n_sft_seq_global=n_sft_g, out=outs[m], unscaled=unscaled)
-        st = allreduce_stats(torch.stack([o.stats for o in outs]).sum(0))
+        st = allreduce_stats(outs[0].stats if n_mb == 1 else
+                             torch.stack([o.stats for o in outs]).sum(0))
     t_end.record()
     torch.cuda.synchronize()
     if world > 1:
@@ -470,58 +587,62 @@ def main():
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     ms = float(tmax.item())
     stats = st.cpu().numpy()
-    value = world * T * args.steps / (ms / 1000.0)
+    value = T_all * args.steps / (ms / 1000.0)
 
-    # ---- roofline of the dominant kernel (k_fused_tma) ----
+    # ---- roofline of the dominant kernel (k_fused_tma; the row kernels on the
+    # two-pass routes): algorithmic bytes / CUDA-event time of the loss calls
+    # (the library's timing hook spans the whole call: the group prologue, the
+    # row kernels and the tail, so this slightly understates the kernel)
     peak, peak_src = peaks()
     f_ms = statistics.mean(fused_ms)
+    achieved = T * args.steps * algo_bytes_row / (sum(fused_ms) / 1000.0) / 1e9
     rows_per_launch = T / n_mb
-    achieved = rows_per_launch * algo_bytes_row / (f_ms / 1000.0) / 1e9
-    # DRAM bytes per launch from the committed `ncu --set full` capture of the
-    # same kernel at this vocabulary, scaled from its row count to this launch's
-    # (the kernel streams rows independently, so bytes / row is size-invariant)
-    traffic = None
-    tf = ROOT / "profiles" / "fused_traffic.json"
-    if tf.exists():
-        try:
-            d = json.loads(tf.read_text())
-            if int(d.get("vocab", 0)) == V:
-                traffic = float(d["dram_bytes_per_row"]) * rows_per_launch
-        except Exception:
-            traffic = None
+    tr = traffic_of(args.variant)
+    traffic = None if tr is None else float(tr["dram_bytes_per_row"]) * rows_per_launch
 
     # ---- e2e: public API with pinned host buffers ----
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, loss, dev, world, rank, n_tok_g, n_seq_g)
+        e2e = run_e2e(args, loss, dev, world, rank, n_tok_g, n_seq_g, len(my_groups))
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cpu = cpu_baseline(args.cpu_rows, K)
+            cpu = cpu_baseline(args)
         except Exception as ex:  # pragma: no cover
-            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "port", "sample": repr(ex)}
+            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
+                   "sample": repr(ex)}
 
     if rank == 0:
+        kname = ("k_fused_tma<bf16,%d>%s" % (cl, " (anchor KL)" if args.variant == "anchor"
+                                              else "")) if cl else "k_fwd + k_bwd (two-pass)"
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
             "config": {"workload": VARIANT_WORKLOAD.get(args.variant,
                                                         f"{args.variant}_qwen2.5_1.5b_shapes"),
-                       "vocab": V, "prompts": G, "repeats": K,
-                       "response_len": Lr if args.variant != "c5" else f"ragged <= {Lr}",
-                       "rows_per_gpu_per_step": T,
-                       "micro_batches": n_mb, "rows_per_micro_batch": T // n_mb,
+                       "vocab": V, "prompts": Gg, "repeats": K,
+                       "response_len": Lr if args.variant != "c5" else f"ragged <= {Lr - 1}",
+                       "global_rows_per_step": T_all,
+                       "rows_per_rank": [int(x) for x in rows_rank],
+                       "load_imbalance": float(rows_rank.max() / rows_rank.mean()),
+                       "micro_batches_rank0": n_mb, "rows_per_micro_batch_rank0": T / n_mb,
                        "loss": VARIANT_LOSS.get(args.variant, args.variant),
                        "l2": f"inputs larger than L2 ({2 * mb_rows * V * 2 / 1e9:.1f} GB "
                              "working set)",
-                       "parallelism": f"dp{world} (groups sharded by rank; stats allreduce)"},
+                       "parallelism": (f"dp{world}: " + ("one global batch, whole groups "
+                                                         "LPT-sharded by rows" if sharded else
+                                                         "one batch per rank") +
+                                       f"; stats allreduce over {backend}" +
+                                       (" (ranks share a device: plumbing only)" if shared
+                                        else ""))},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": ("k_fused_tma<anchor>" if args.variant == "anchor" else
-                                    "k_fused_tma" if not two_pass else "k_fwd..k_bwd (two-pass)"),
-                         "kernel_ms": f_ms,
+                         "traffic_source": None if tr is None else tr.get("source"),
+                         "kernel": kname, "kernel_ms": f_ms,
                          "algorithmic_bytes_per_launch": rows_per_launch * algo_bytes_row,
+                         "algorithmic_bytes_per_row": algo_bytes_row,
                          "peak_source": peak_src,
                          "frac_of_8tbs_nominal": achieved / 8000.0},
             "cpu_baseline": cpu,
@@ -529,6 +650,7 @@ def main():
             "gpu_launches": int(launches),
             "clocks": clk,
             "check": {"loss": float(stats[0]), "n_tok": float(stats[N.STAT["n_tok"]]),
+                      "n_tok_equals_global_rows": bool(stats[N.STAT["n_tok"]] == T_all),
                       "nonfinite": float(stats[N.STAT["nonfinite"]]),
                       "clipfrac": float(stats[N.STAT["clip_count"]] /
                                         max(stats[N.STAT["n_tok_rl"]], 1)),
@@ -541,7 +663,7 @@ def main():
     return 0
 
 
-def run_e2e(args, loss, dev, world, rank, n_tok_g, n_seq_g):
+def run_e2e(args, loss, dev, world, rank, n_tok_g, n_seq_g, n_groups):
     """Public API with HOST buffers.  A step is `e2e_groups` (default: all of the
     step's groups, i.e. the same 1,048,576 rows as the device metric) RFTLoss calls, one
     GRPO group (8 x 2048 rows, 5 GB of bf16 logits) each: the group's logits
@@ -549,13 +671,15 @@ def run_e2e(args, loss, dev, world, rank, n_tok_g, n_seq_g):
     runs on the compute stream (dlogits in place), and dlogits + the stats
     vector are copied D2H on a second copy stream.  Three device slots and
     three pinned in/out buffers rotate, so the H2D of group i+1, the kernel of
-    group i and the D2H of group i-1 overlap (PCIe is full duplex)."""
+    group i and the D2H of group i-1 overlap (PCIe is full duplex).  After the
+    timing, every call's host stats and a sample of its host dlogits rows are
+    checked against the same inputs run on the device path."""
     import torch
 
     from paper_2505_17826_b200.packing import PackedBatch
 
     K, Lr = args.group_size, args.resp_len
-    ng = args.e2e_groups if args.e2e_groups > 0 else args.groups
+    ng = args.e2e_groups if args.e2e_groups > 0 else n_groups
     nbuf = min(3, ng)
     # pinned host memory: 2 * nbuf * rows * V * 2 bytes per rank (30 GB at the
     # defaults).  With many ranks per box, shrink the rotation depth, then the
@@ -596,6 +720,12 @@ def run_e2e(args, loss, dev, world, rank, n_tok_g, n_seq_g):
     h2d_bytes = ng * (rows * V * 2 + 3 * rows * 4)  # logits + target + old_lp + ref_lp
     d2h_bytes = ng * (rows * V * 2 + 32 * 8)        # dlogits + stats
 
+    def packed(b, lg):
+        return PackedBatch(logits=lg, target=dev_tgt[b], seq_offsets=so, group_offsets=go,
+                           reward=rw, old_lp=dev_meta[b][0], ref_lp=dev_meta[b][1], vocab=V,
+                           n_rows=rows, n_seqs=K, n_groups=1, n_rl_rows=rows, n_rl_seqs=K,
+                           max_rows_per_seq=Lr)
+
     def one_step():
         free = [None] * nbuf
         for i in range(ng):
@@ -610,16 +740,14 @@ def run_e2e(args, loss, dev, world, rank, n_tok_g, n_seq_g):
                 ready.record(s_in)
             with torch.cuda.stream(s_cmp):
                 s_cmp.wait_event(ready)
-                pb = PackedBatch(logits=dev_in[b], target=dev_tgt[b], seq_offsets=so,
-                                 group_offsets=go, reward=rw, old_lp=dev_meta[b][0],
-                                 ref_lp=dev_meta[b][1], vocab=V, n_rows=rows, n_seqs=K,
-                                 n_groups=1, n_rl_rows=rows, n_rl_seqs=K, max_rows_per_seq=Lr)
-                out = loss(pb, dlogits="inplace", n_tok_global=n_tok_g, n_seq_global=n_seq_g,
-                           stream=s_cmp)
+                out = loss(packed(b, dev_in[b]), dlogits="inplace", n_tok_global=n_tok_g,
+                           n_seq_global=n_seq_g, stream=s_cmp)
                 done = torch.cuda.Event()
                 done.record(s_cmp)
             with torch.cuda.stream(s_out):
                 s_out.wait_event(done)
+                # the stats tensor is read on s_out: keep it alive until that copy ran
+                out.stats.record_stream(s_out)
                 host_out[b].copy_(dev_in[b], non_blocking=True)
                 host_stats[i].copy_(out.stats, non_blocking=True)
                 free[b] = torch.cuda.Event()
@@ -633,8 +761,31 @@ def run_e2e(args, loss, dev, world, rank, n_tok_g, n_seq_g):
         one_step()
         times.append(time.perf_counter() - t0)
     dt = statistics.median(times)
+    # ---- correctness of the e2e results: the device path on the same inputs ----
+    ok_stats, ok_rows, mismatch = True, True, None
+    sample = np.random.default_rng(5).choice(rows, 8, replace=False)
+    for b in range(nbuf):
+        dev_in[b].copy_(host_in[b])
+        dev_meta[b].copy_(fmeta[b])
+        dev_tgt[b].copy_(tmeta[b])
+        ref = loss(packed(b, dev_in[b]), dlogits="new", n_tok_global=n_tok_g,
+                   n_seq_global=n_seq_g)
+        want = ref.stats.cpu()
+        for i in range(b, ng, nbuf):
+            same = bool(torch.equal(host_stats[i], want))
+            if not same and mismatch is None:
+                from paper_2505_17826_b200 import _native as N
+                d = (host_stats[i] != want).nonzero().flatten().tolist()
+                mismatch = {"call": i, **{N.STAT_NAMES[j]: [float(host_stats[i][j]),
+                                                            float(want[j])] for j in d[:4]}}
+            ok_stats &= same
+        idx = torch.as_tensor(sample, device=dev)
+        ok_rows &= bool(torch.equal(host_out[b][sample].to(dev), ref.dlogits[idx]))
+    torch.cuda.synchronize(dev)
     return {"value": ng * rows / dt, "unit": UNIT, "h2d_bytes_per_step": h2d_bytes,
             "d2h_bytes_per_step": d2h_bytes,
+            "check": {"host_stats_equal_device_path": ok_stats, "first_mismatch": mismatch,
+                      "host_dlogits_sample_equal_device_path": ok_rows},
             "note": f"{ng} RFTLoss calls x {rows} rows per step, pinned host logits in and "
                     f"dlogits + stats out, {nbuf}-deep copy/compute overlap; PCIe-bound"}
 

@@ -278,9 +278,10 @@ int tg_fused_cluster_size(const TgBatch* batch, const TgConfig* cfg);
 
 /* Timing hook (measurement only): when both are non-NULL cudaEvent_t handles,
    the next tg_loss_fwd_bwd call on this thread records ev_begin on its stream
-   immediately before its first row kernel (k_fused_tma, or k_fwd on the
-   two-pass routes) and ev_end immediately after its last row kernel
-   (k_fused_tma / k_bwd).  The hook is consumed by that call. */
+   before its first kernel and ev_end after its last one (the whole call: the
+   group prologue, the row kernels and the tail -- an event between kernels
+   chained by programmatic dependent launch would serialise them).  The hook
+   is consumed by that call. */
 int tg_set_timing_events(void* ev_begin, void* ev_end);
 
 /* Total CUDA kernel launches issued by this library in this process. */

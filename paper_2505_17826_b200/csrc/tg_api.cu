@@ -66,6 +66,7 @@ void launch_rowmeta(const KParams& P, void* meta, cudaStream_t st);
 void launch_seq_reduce(const KParams& P, cudaStream_t st);
 void launch_coupled(const KParams& P, cudaStream_t st);
 void launch_finalize(const KParams& P, bool coupled, cudaStream_t st);
+int launch_tail(const KParams& P, cudaStream_t st);
 }  // namespace tg
 
 using namespace tg;
@@ -506,6 +507,9 @@ int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspa
 
   cudaEvent_t ev_begin = g_ev_begin, ev_end = g_ev_end;
   g_ev_begin = g_ev_end = nullptr;
+  // the timing span is the whole call (prologue, row kernels, tail): events
+  // between PDL-chained kernels would serialise them
+  if (ev_begin) cudaEventRecord(ev_begin, st);
   count_launches(launch_group_prep(P, coupled, st));
   if (route == 4) {
     // coupled loss in one pass: the fused kernel writes p - e_y and the per-row
@@ -515,9 +519,7 @@ int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspa
     P.n_partials = fp.n_ctas;
     if (P.n_partials > kMaxPartials) return fail(TG_EUNSUPPORTED, "too many CTAs");
     if (b->n_rows > 0) {
-      if (ev_begin) cudaEventRecord(ev_begin, st);
       cudaError_t e = launch_fused(P, meta, fp.cl, fp.n_slots, fp.n_ctas, fp.prefetch_rows, st);
-      if (ev_end) cudaEventRecord(ev_end, st);
       if (e != cudaSuccess) return fail(TG_ECUDA, "fused kernel launch: %s", cudaGetErrorString(e));
       count_launches(1);
     }
@@ -544,24 +546,22 @@ int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspa
         launch_rowmeta(P, meta, st);
         count_launches(b->n_seqs > 0 ? 1 : 0);
       }
-      if (ev_begin) cudaEventRecord(ev_begin, st);
       cudaError_t e = l2 ? launch_fused_l2(P, meta, l2_ctas, fp.prefetch_rows, st)
                          : launch_fused(P, meta, fp.cl, fp.n_slots, fp.n_ctas, fp.prefetch_rows, st);
-      if (ev_end) cudaEventRecord(ev_end, st);
       if (e != cudaSuccess) return fail(TG_ECUDA, "fused kernel launch: %s", cudaGetErrorString(e));
       count_launches(1);
     } else {
       P.n_partials = 0;
     }
-    launch_seq_reduce(P, st);
-    count_launches(b->n_seqs > 0 ? 1 : 0);
+    count_launches(launch_tail(P, st));  // seq sums + finalize
+    if (ev_end) cudaEventRecord(ev_end, st);
+    return check_cuda("tg_loss_fwd_bwd");
   } else {
     launch_rowmeta(P, meta, st);
     count_launches(b->n_seqs > 0 ? 1 : 0);
     const bool vin = vec_ok(b->logits, b->ld, esz) &&
                      (!anchor || vec_ok(b->anchor_logits, b->ld_anchor, esz));
     const int grid = stream_grid(b->n_rows);
-    if (ev_begin) cudaEventRecord(ev_begin, st);
     if (b->n_rows > 0 && !rows_given) {
       run_forward(P, b, anchor, vin, grid, st);
       count_launches(1);
@@ -582,14 +582,15 @@ int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspa
       launch_bwd(P, anchor, vout, grid, st);
       count_launches(1);
     }
-    if (ev_end) cudaEventRecord(ev_end, st);
     if (!coupled) {
-      launch_seq_reduce(P, st);
-      count_launches(b->n_seqs > 0 ? 1 : 0);
+      count_launches(launch_tail(P, st));  // seq sums + finalize
+      if (ev_end) cudaEventRecord(ev_end, st);
+      return check_cuda("tg_loss_fwd_bwd");
     }
   }
   launch_finalize(P, coupled, st);
   count_launches(1);
+  if (ev_end) cudaEventRecord(ev_end, st);
   return check_cuda("tg_loss_fwd_bwd");
 }
 

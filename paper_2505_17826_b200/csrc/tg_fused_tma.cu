@@ -1024,6 +1024,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   }
+  // every CTA is resident: the tail kernel (PDL) may be scheduled; it waits
+  // for this grid's completion itself
+  if (tid == 0) pdl_trigger();
   if (CL > 1)
     cluster_sync_all();
   else
@@ -1095,6 +1098,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     // Off the consumers' critical path: while it reduces row k, exchanges with
     // the cluster peers and evaluates the loss terms, the consumers already run
     // phase 1 of row k+1.
+    // The group prologue (k_counts_prep) may still run (PDL): the producer and
+    // the consumers already stream the first rows; the row metadata it writes
+    // (advantages, weights) is read here only after it completed.
+    pdl_wait();
     double sd[15];
 #pragma unroll
     for (int i = 0; i < 15; ++i) sd[i] = 0.0;
@@ -1536,13 +1543,17 @@ static cudaError_t launch_fused_t(const KParams& P, const RowMeta* meta, int n_c
   cfg.blockDim = dim3(kFusedThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  // PDL: start streaming rows while k_counts_prep (already resident: it
+  // triggers on entry) finishes; only the epilogue warp waits for it
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, k_fused_tma<T, CL, kA>, P, meta, prefetch_rows);
 }
 

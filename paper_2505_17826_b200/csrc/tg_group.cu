@@ -142,6 +142,7 @@ __global__ void k_prep(const KParams P) {
 // the batch counts are reduced in shared memory, then the 32 warps take the
 // groups one warp per group.
 __global__ void __launch_bounds__(1024) k_counts_prep(const KParams P) {
+  pdl_trigger();  // the fused kernel may start streaming (its epilogue waits for us)
   __shared__ unsigned long long c[4];
   if (threadIdx.x < 4) c[threadIdx.x] = 0;
   __syncthreads();
@@ -200,24 +201,37 @@ __global__ void k_rowmeta(const KParams P, RowMeta* __restrict__ meta) {
   }
 }
 
-// one warp per sequence: LP_i and the resolved reference logprob
+// one warp, sequence i: LP_i and the resolved reference logprob.  Four
+// independent accumulators per lane (four loads in flight), combined in a
+// fixed order: the same bits from k_seq_reduce and k_tail.
+__device__ __forceinline__ void seq_sums(const KParams& P, int i, int lane) {
+  const int a = P.seq_off[i], b = P.seq_off[i + 1];
+  double s[4] = {0.0, 0.0, 0.0, 0.0}, so[4] = {0.0, 0.0, 0.0, 0.0};
+  int r = a + lane;
+  for (; r + 96 < b; r += 128) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      s[u] += double(P.lp[r + 32 * u]);
+      if (P.old_lp) so[u] += double(P.old_lp[r + 32 * u]);
+    }
+  }
+  for (int u = 0; r < b; r += 32, ++u) {
+    s[u] += double(P.lp[r]);
+    if (P.old_lp) so[u] += double(P.old_lp[r]);
+  }
+  double t = warp_sum_d((s[0] + s[1]) + (s[2] + s[3]));
+  double to = warp_sum_d((so[0] + so[1]) + (so[2] + so[3]));
+  if (lane == 0) {
+    P.sLP[i] = t;
+    P.sRef[i] = P.seq_ref_lp ? double(P.seq_ref_lp[i]) : (P.old_lp ? to : t);
+    P.seq_lp[i] = float(t);
+  }
+}
+
+// one warp per sequence
 __global__ void k_seq_reduce(const KParams P) {
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (i >= P.n_seqs) return;
-  const int a = P.seq_off[i], b = P.seq_off[i + 1];
-  double s = 0.0, so = 0.0;
-  for (int r = a + lane; r < b; r += 32) {
-    s += double(P.lp[r]);
-    if (P.old_lp) so += double(P.old_lp[r]);
-  }
-  s = warp_sum_d(s);
-  so = warp_sum_d(so);
-  if (lane == 0) {
-    P.sLP[i] = s;
-    P.sRef[i] = P.seq_ref_lp ? double(P.seq_ref_lp[i]) : (P.old_lp ? so : s);
-    P.seq_lp[i] = float(s);
-  }
+  if (i < P.n_seqs) seq_sums(P, i, threadIdx.x & 31);
 }
 
 __device__ __forceinline__ double softplus_d(double x) { return log1p(exp(-fabs(x))) + fmax(x, 0.0); }
@@ -295,12 +309,15 @@ __global__ void k_coupled(const KParams P) {
   }
 }
 
-// single CTA of 256 threads; fixed reduction order => deterministic stats
-__global__ void k_finalize(const KParams P, int coupled) {
+// fixed reduction order => deterministic stats; any block size that is a
+// multiple of 64 (warps stride over the 32 stats slots)
+__device__ void finalize_body(const KParams& P, int coupled) {
   __shared__ double part[TG_NSTAT];
   __shared__ double grp[8];
+  __shared__ double sq[3];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int j = warp; j < TG_NSTAT; j += 8) {
+  const int nw = blockDim.x >> 5;
+  for (int j = warp; j < TG_NSTAT; j += nw) {
     double s = 0.0;
     for (int c = lane; c < P.n_partials; c += 32) s += P.partials[size_t(c) * TG_NSTAT + j];
     s = warp_sum_d(s);
@@ -333,7 +350,6 @@ __global__ void k_finalize(const KParams P, int coupled) {
       grp[6] = smar;
     }
   }
-  __shared__ double sq[3];
   if (warp == 1) {  // sequence sums
     double sadv = 0, nsft = 0, rsft = 0;
     for (int i = lane; i < P.n_seqs; i += 32) {
@@ -369,6 +385,20 @@ __global__ void k_finalize(const KParams P, int coupled) {
   }
 }
 
+// single CTA of 256 threads
+__global__ void k_finalize(const KParams P, int coupled) { finalize_body(P, coupled); }
+
+// per-sequence sums (k_seq_reduce) + k_finalize in ONE single-CTA launch for
+// the per-row routes' tail: 32 warps stride over the sequences, then the
+// fixed-order reduction.  PDL-launched behind the row kernel, which it waits for.
+__global__ void __launch_bounds__(1024) k_tail(const KParams P) {
+  pdl_wait();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = warp; i < P.n_seqs; i += 32) seq_sums(P, i, lane);
+  __syncthreads();
+  finalize_body(P, 0);
+}
+
 // ---------------------------------------------------------------------------
 
 // counts + group prep: one CTA for batches of up to 2,048 groups (every
@@ -399,6 +429,29 @@ void launch_coupled(const KParams& P, cudaStream_t st) {
 
 void launch_finalize(const KParams& P, bool coupled, cudaStream_t st) {
   k_finalize<<<1, 256, 0, st>>>(P, coupled ? 1 : 0);
+}
+
+// the per-row routes' tail (seq sums + finalize) as one PDL launch; beyond
+// kTailMaxRows rows the multi-CTA k_seq_reduce is faster, so two launches.
+// Returns the number of kernels launched.
+int launch_tail(const KParams& P, cudaStream_t st) {
+  constexpr int64_t kTailMaxRows = int64_t(1) << 18;
+  if (P.n_rows > kTailMaxRows) {
+    launch_seq_reduce(P, st);
+    launch_finalize(P, false, st);
+    return (P.n_seqs > 0 ? 1 : 0) + 1;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(1024);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_tail, P);
+  return 1;
 }
 
 }  // namespace tg

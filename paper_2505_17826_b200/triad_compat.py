@@ -11,6 +11,13 @@ per-token gradient rows are scatter-added back by state into a dense table
 gradient, which is what ``SparseGrad.to_dense`` holds in the reference
 (policy.py:215-250).
 
+Gradients stay on the GPU: ``SparseGrad`` holds the touched states and
+their rows as device tensors (the reference's ``{state: row}`` dict is
+materialised only when ``.rows`` is read), ``combine_reports`` merges them on
+the device, and ``apply_update`` / ``Trainer`` step the table with
+``tg_apply_update``.  ``Trainer`` keeps the policy table resident on the GPU;
+``params`` materialises the host table when read.
+
 Objects are duck-typed: ``params`` needs ``logits`` [S, V], ``num_buckets``,
 ``vocab.size`` (and ``version`` for the Trainer); groups / experiences as in
 records.py.  Arithmetic is fp32 on the device (tables are uploaded as f32),
@@ -57,38 +64,66 @@ class AlgorithmConfig:
 
 
 class SparseGrad:
-    """policy.py:215-250: touched rows only (float64 numpy rows)."""
+    """policy.SparseGrad (policy.py:215-250): the touched rows of a table
+    gradient, held on the GPU as ascending state ids ``ids`` [n] int64 and
+    float64 rows ``vals`` [n, V].  The reference's methods are kept; ``rows``
+    gives the reference's {state: row} dict (a host copy, made on access)."""
 
-    def __init__(self) -> None:
-        self.rows: Dict[int, np.ndarray] = {}
+    def __init__(self, ids=None, vals=None) -> None:
+        self.ids = ids
+        self.vals = vals
 
-    def add_row(self, state: int, vec: np.ndarray) -> None:
-        if state in self.rows:
-            self.rows[state] = self.rows[state] + vec
-        else:
-            self.rows[state] = np.array(vec, dtype=np.float64)
+    @classmethod
+    def from_token_rows(cls, dz: torch.Tensor, states) -> "SparseGrad":
+        """Per-token gradient rows -> per-state sums (grad_logprob's add_row
+        per scored token, policy.py:253-270), on the device."""
+        dev = dz.device
+        st = torch.as_tensor(np.asarray(states, np.int64), device=dev)
+        ids, inv = torch.unique(st, sorted=True, return_inverse=True)
+        vals = torch.zeros((ids.numel(), dz.shape[1]), dtype=torch.float64, device=dev)
+        vals.index_add_(0, inv, dz.double())
+        return cls(ids, vals)
+
+    def _merge(self, ids: torch.Tensor, vals: torch.Tensor) -> None:
+        if self.ids is None:
+            self.ids, self.vals = ids, vals
+            return
+        cat = torch.cat([self.ids, ids])
+        u, inv = torch.unique(cat, sorted=True, return_inverse=True)
+        out = torch.zeros((u.numel(), vals.shape[1]), dtype=torch.float64, device=vals.device)
+        out.index_add_(0, inv, torch.cat([self.vals, vals]))
+        self.ids, self.vals = u, out
+
+    def add_row(self, state: int, vec) -> None:
+        dev = self.vals.device if self.vals is not None else _device()
+        v = torch.as_tensor(np.asarray(vec, np.float64), device=dev).reshape(1, -1)
+        self._merge(torch.tensor([int(state)], device=dev), v)
 
     def axpy(self, coef: float, other: "SparseGrad") -> None:
-        for state, vec in other.rows.items():
-            self.add_row(state, coef * vec)
+        if other.ids is not None:
+            self._merge(other.ids, coef * other.vals)
 
     def scaled(self, coef: float) -> "SparseGrad":
-        out = SparseGrad()
-        for state, vec in self.rows.items():
-            out.rows[state] = coef * vec
-        return out
+        return SparseGrad(self.ids, None if self.vals is None else coef * self.vals)
+
+    @property
+    def rows(self) -> Dict[int, np.ndarray]:
+        if self.ids is None:
+            return {}
+        return dict(zip(self.ids.cpu().tolist(), self.vals.cpu().numpy()))
 
     def to_dense(self, shape: Tuple[int, int]) -> np.ndarray:
         dense = np.zeros(shape)
-        for state, vec in self.rows.items():
-            dense[state] += vec
+        if self.ids is not None:
+            dense[self.ids.cpu().numpy()] += self.vals.cpu().numpy()
         return dense
 
     def is_finite(self) -> bool:
-        return all(np.all(np.isfinite(v)) for v in self.rows.values())
+        return self.vals is None or bool(torch.isfinite(self.vals).all())
 
     def max_abs(self) -> float:
-        return max((float(np.max(np.abs(v))) for v in self.rows.values()), default=0.0)
+        return 0.0 if self.vals is None or self.vals.numel() == 0 else \
+            float(self.vals.abs().max())
 
 
 @dataclass
@@ -133,20 +168,8 @@ def _seq_logprob(table: torch.Tensor, states: np.ndarray, target: np.ndarray,
     return seq_lp.double().cpu().numpy()
 
 
-def _scatter(dz: torch.Tensor, states: np.ndarray, S: int) -> SparseGrad:
-    dev = dz.device
-    idx = torch.as_tensor(states, device=dev)
-    dense = torch.zeros((S, dz.shape[1]), dtype=torch.float64, device=dev)
-    dense.index_add_(0, idx, dz.double())
-    host = dense.cpu().numpy()
-    g = SparseGrad()
-    for s in sorted(set(int(x) for x in states)):
-        g.rows[s] = host[s].copy()
-    return g
-
-
 def _run(groups, params, cfg: RFTLossConfig, *, anchor=None, seq_ref_override=None,
-         seq_kind=None, metrics_override=None, table=None, keep_rows=False):
+         seq_kind=None, metrics_override=None, table=None, anchor_table=None, keep_rows=False):
     dev = _device()
     h = flatten_groups(groups)
     S, V = int(params.num_buckets), int(params.vocab.size)
@@ -160,7 +183,9 @@ def _run(groups, params, cfg: RFTLossConfig, *, anchor=None, seq_ref_override=No
         if tuple(np.shape(anchor.logits)) != tuple(np.shape(params.logits)):
             raise AlgorithmError(f"parameter shapes differ: {np.shape(params.logits)} vs "
                                  f"{np.shape(anchor.logits)}")
-        anchor_rows = _table(anchor, dev)[torch.as_tensor(states, device=dev)].contiguous()
+        if anchor_table is None:
+            anchor_table = _table(anchor, dev)
+        anchor_rows = anchor_table[torch.as_tensor(states, device=dev)].contiguous()
     batch = pack_arrays(table, target, h.seq_lengths, h.group_sizes, h.reward, old_lp=h.old_lp,
                         seq_ref_lp=seq_ref, seq_kind=seq_kind, anchor_logits=anchor_rows,
                         row_index=states)
@@ -168,7 +193,7 @@ def _run(groups, params, cfg: RFTLossConfig, *, anchor=None, seq_ref_override=No
     st = out.stats_dict()
     if st["invalid"] > 0:
         raise AlgorithmError("invalid group shape for this loss")
-    grad = _scatter(out.dlogits, states, S)
+    grad = SparseGrad.from_token_rows(out.dlogits, states)
     m = stats_to_metrics(st, check=False)
     metrics = {k: m[k] for k in ("mean_reward", "baseline", "kl_estimate", "group_size")}
     if metrics_override:
@@ -290,6 +315,10 @@ class _OneGroup:
 
 def loss_sft(batch: Sequence, params) -> LossReport:
     """algorithms.py:256-274: mean over sequences of -sum_t lp."""
+    return _sft(batch, params)
+
+
+def _sft(batch, params, table=None, keep_rows=False):
     if not batch:
         raise AlgorithmError("SFT batch must be nonempty")
     cfg = RFTLossConfig.from_variant(Variant.SFT)
@@ -301,7 +330,8 @@ def loss_sft(batch: Sequence, params) -> LossReport:
                 "kl_estimate": 0.0, "group_size": float(n)}
 
     exps = [e if e.reward is not None else _with_reward(e) for e in batch]
-    return _run([_OneGroup(exps)], params, cfg, metrics_override=metrics)
+    return _run([_OneGroup(exps)], params, cfg, metrics_override=metrics, table=table,
+                keep_rows=keep_rows)
 
 
 def _with_reward(e):
@@ -316,6 +346,10 @@ def _with_reward(e):
 
 def loss_dpo(pairs: Sequence[Tuple], params, ref, dpo_beta: float) -> LossReport:
     """algorithms.py:277-315."""
+    return _dpo(pairs, params, ref, dpo_beta)
+
+
+def _dpo(pairs, params, ref, dpo_beta, table=None, ref_table=None, keep_rows=False):
     if not pairs:
         raise AlgorithmError("DPO batch must be nonempty")
     if dpo_beta <= 0:
@@ -327,7 +361,8 @@ def loss_dpo(pairs: Sequence[Tuple], params, ref, dpo_beta: float) -> LossReport
                          r if r.reward is not None else _with_reward(r)]) for c, r in pairs]
     h = flatten_groups(groups)
     st, tg = scored_states(h, int(ref.num_buckets))
-    seq_ref = _seq_logprob(_table(ref, _device()), st, tg, h.seq_lengths)
+    seq_ref = _seq_logprob(ref_table if ref_table is not None else _table(ref, _device()), st, tg,
+                           h.seq_lengths)
     cfg = RFTLossConfig.from_variant(Variant.DPO, dpo_beta=dpo_beta)
     n = len(pairs)
 
@@ -335,34 +370,33 @@ def loss_dpo(pairs: Sequence[Tuple], params, ref, dpo_beta: float) -> LossReport
         return {"mean_reward": s["sum_dpo_margin"] / n, "baseline": 0.0, "kl_estimate": 0.0,
                 "group_size": float(n)}
 
-    return _run(groups, params, cfg, seq_ref_override=seq_ref, metrics_override=metrics)
+    return _run(groups, params, cfg, seq_ref_override=seq_ref, metrics_override=metrics,
+                table=table, keep_rows=keep_rows)
 
 
 def combine_reports(reports: Sequence[LossReport]) -> LossReport:
-    """algorithms.py:368-379."""
+    """algorithms.py:368-379: losses summed, gradients merged on the device
+    (SparseGrad), metrics averaged over the reports."""
     if not reports:
         raise AlgorithmError("cannot combine an empty report list")
     grad = SparseGrad()
-    loss = 0.0
     for rep in reports:
-        loss += rep.loss
         grad.axpy(1.0, rep.gradient)
-    keys = reports[0].metrics.keys()
-    metrics = {k: float(np.mean([r.metrics[k] for r in reports])) for k in keys}
-    return LossReport(loss=loss, gradient=grad, metrics=metrics)
+    metrics = {k: float(np.mean([r.metrics[k] for r in reports])) for k in reports[0].metrics}
+    return LossReport(loss=float(sum(r.loss for r in reports)), gradient=grad, metrics=metrics)
 
 
 def apply_update(params, gradient: SparseGrad, learning_rate: float):
-    """algorithms.py:329-348: SGD step, new table, version + 1."""
-    if not gradient.is_finite():
-        raise AlgorithmError("refusing to apply a non-finite gradient")
-    logits = np.array(params.logits)
-    for state, vec in gradient.rows.items():
-        if not 0 <= state < params.num_buckets:
-            raise AlgorithmError(f"gradient row {state} outside the logits table")
-        logits[state] -= learning_rate * vec
-    return type(params)(logits=logits, version=params.version + 1, vocab=params.vocab,
-                        num_buckets=params.num_buckets)
+    """algorithms.py:329-348: SGD step returning new params with version + 1,
+    computed by tg_apply_update on an fp32 device copy of the table (refuses
+    a non-finite gradient or a row outside the table, before any write)."""
+    dev = _device()
+    table = _table(params, dev)
+    if gradient.ids is not None and gradient.ids.numel():
+        apply_update_rows(table, gradient.vals.float(), gradient.ids.cpu().numpy(),
+                          learning_rate)
+    return type(params)(logits=table.double().cpu().numpy(), version=params.version + 1,
+                        vocab=params.vocab, num_buckets=params.num_buckets)
 
 
 def apply_update_rows(table: torch.Tensor, dlogits: torch.Tensor, states: np.ndarray,
@@ -406,41 +440,21 @@ def apply_update_rows(table: torch.Tensor, dlogits: torch.Tensor, states: np.nda
 
 
 class Trainer:
-    """orchestrator.Trainer (orchestrator.py:288-322) on the CUDA loss path."""
+    """orchestrator.Trainer (orchestrator.py:288-322) on the CUDA path with the
+    policy table resident on the GPU: the loss kernels read it in place
+    (row_index) and the SGD step runs on the device from the per-token
+    gradient rows (tg_apply_update), so only the LossReport crosses PCIe.  The
+    anchor / reference snapshot (orchestrator.py:292-296) is frozen on the
+    device too.  ``params`` materialises the host table when read (version
+    counted like apply_update, algorithms.py:343-348)."""
 
     def __init__(self, params, algo: AlgorithmConfig) -> None:
-        self.params = params
-        self.algo = algo
-        self.anchor = params
-
-    def step_groups(self, groups) -> LossReport:
-        combined = group_losses(groups, self.params, self.algo, sft_params=self.anchor)
-        self.params = apply_update(self.params, combined.gradient, self.algo.learning_rate)
-        return combined
-
-    def step_sft(self, batch) -> LossReport:
-        report = loss_sft(batch, self.params)
-        self.params = apply_update(self.params, report.gradient, self.algo.learning_rate)
-        return report
-
-    def step_dpo(self, pairs) -> LossReport:
-        report = loss_dpo(pairs, self.params, self.anchor, self.algo.dpo_beta)
-        self.params = apply_update(self.params, report.gradient, self.algo.learning_rate)
-        return report
-
-
-class DeviceTrainer:
-    """``Trainer.step_groups`` with the policy table resident on the GPU: the
-    loss kernels read it in place (row_index) and the SGD step runs on the
-    device from the per-token gradient rows (``tg_apply_update``), so only the
-    LossReport crosses PCIe.  ``params`` materialises the host table on access
-    (version counted like apply_update, algorithms.py:343-348)."""
-
-    def __init__(self, params, algo: AlgorithmConfig) -> None:
+        dev = _device()
         self._host = params
         self.algo = algo
         self.anchor = params
-        self.table = _table(params, _device())
+        self.table = _table(params, dev)
+        self.anchor_table = self.table.clone()
         self.version = int(getattr(params, "version", 0))
 
     @property
@@ -449,16 +463,35 @@ class DeviceTrainer:
         return type(p)(logits=self.table.double().cpu().numpy(), version=self.version,
                        vocab=p.vocab, num_buckets=p.num_buckets)
 
+    def _apply(self, dz: torch.Tensor, states: np.ndarray) -> None:
+        apply_update_rows(self.table, dz, states, self.algo.learning_rate)
+        self.version += 1
+
     def step_groups(self, groups) -> LossReport:
         config = self.algo
         if config.variant not in (Variant.OPMD_KIMI, Variant.OPMD_PAIRWISE, Variant.OPMD_SIMPLE):
             raise AlgorithmError(f"{config.variant.value} is not a group-based loss")
         if not groups:
             raise AlgorithmError("cannot combine an empty report list")
+        if config.variant == Variant.OPMD_PAIRWISE and any(len(g.experiences) < 2 for g in groups):
+            raise AlgorithmError("pairwise loss needs a group of at least 2 rollouts")
         cfg = RFTLossConfig.from_variant(config.variant, config.tau, config.beta, config.dpo_beta)
         anchor = self.anchor if (config.variant == Variant.OPMD_SIMPLE and config.beta > 0) else None
         report, dz, states = _run(groups, self._host, cfg, anchor=anchor, table=self.table,
-                                  keep_rows=True)
-        apply_update_rows(self.table, dz, states, config.learning_rate)
-        self.version += 1
+                                  anchor_table=self.anchor_table, keep_rows=True)
+        self._apply(dz, states)
         return report
+
+    def step_sft(self, batch) -> LossReport:
+        report, dz, states = _sft(batch, self._host, table=self.table, keep_rows=True)
+        self._apply(dz, states)
+        return report
+
+    def step_dpo(self, pairs) -> LossReport:
+        report, dz, states = _dpo(pairs, self._host, self.anchor, self.algo.dpo_beta,
+                                  table=self.table, ref_table=self.anchor_table, keep_rows=True)
+        self._apply(dz, states)
+        return report
+
+
+DeviceTrainer = Trainer  # round-1 name

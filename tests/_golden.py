@@ -41,7 +41,8 @@ def load(name: str) -> dict:
         return {k: z[k] for k in z.files}
 
 
-def groups_of(fx: dict) -> List[Group]:
+def groups_of(fx: dict, prefix: str = "") -> List[Group]:
+    fx = {k[len(prefix):]: v for k, v in fx.items() if k.startswith(prefix)}
     exps = []
     for i in range(len(fx["prompt_len"])):
         a, b = int(fx["tok_off"][i]), int(fx["tok_off"][i + 1])

@@ -27,6 +27,7 @@ sys.path.insert(0, "/root/reference/pkg/src")
 from triad import algorithms as A  # noqa: E402
 from triad import policy as P  # noqa: E402
 from triad.buffer import ExperienceBuffer  # noqa: E402
+from triad.orchestrator import Trainer  # noqa: E402
 from triad.records import Experience, ExperienceState, TaskGroup  # noqa: E402
 
 OUT = Path(__file__).resolve().parent
@@ -230,6 +231,50 @@ def buffer_case(name, seed, n_exp, n_tasks, group_size, n_take, policy):
          groups=np.array(out, np.int64).reshape(-1, group_size), short=np.array(res.short))
 
 
+def trainer_case(name, seed, V, S, n_groups, K, variant, tau, beta, steps, lr, sft_n=0,
+                 dpo_pairs=0):
+    """The reference's own Trainer (orchestrator.py:288-322): `steps` x
+    step_groups (+ a step_sft / step_dpo at the end), recording every step's
+    loss and metrics and the final table and version."""
+    rng = np.random.default_rng(seed)
+    vocab = P.Vocabulary(size=V, eos_token=V - 1)
+    behavior = P.PolicyParams(table(rng, S, V, 0.4, False), 0, vocab)
+    params = P.PolicyParams(table(rng, S, V, 0.8, False), 0, vocab)
+    groups = []
+    for g in range(n_groups):
+        exps = [make_experience(rng, vocab, 1000 + g, int(rng.integers(1, 4)),
+                                int(rng.integers(1, 4)), 5, behavior, True) for _ in range(K)]
+        groups.append(TaskGroup(1000 + g, exps))
+    tr = Trainer(params, A.AlgorithmConfig(variant, tau=tau, beta=beta, learning_rate=lr))
+    losses, metrics = [], []
+    for _ in range(steps):
+        rep = tr.step_groups(groups)
+        losses.append(rep.loss)
+        metrics.append([rep.metrics[k] for k in sorted(rep.metrics)])
+    extra = {}
+    if sft_n:
+        batch = [make_experience(rng, vocab, 7, 2, 2, 5, behavior, True) for _ in range(sft_n)]
+        losses.append(tr.step_sft(batch).loss)
+        extra.update(sft=flatten_groups([TaskGroup(7, batch)]))
+    if dpo_pairs:
+        pairs = []
+        for _ in range(dpo_pairs):
+            c = make_experience(rng, vocab, 3, 2, 1, 5, behavior, False)
+            r = make_experience(rng, vocab, 3, 2, 1, 5, behavior, False)
+            r = Experience(task_key=3, tokens=c.tokens[: c.prompt_length] + r.tokens[r.prompt_length:],
+                           prompt_length=c.prompt_length, action_mask=r.action_mask,
+                           logprobs=r.logprobs, reward=0.0, model_version=0)
+            pairs.append((c, r))
+        losses.append(tr.step_dpo(pairs).loss)
+        extra.update(dpo=flatten_groups([TaskGroup(3, [c, r]) for c, r in pairs]))
+    flat = {f"{k2}_{k}": v for k2, d in extra.items() for k, v in d.items()}
+    save(name, theta=params.logits, final=tr.params.logits, version=np.array(tr.params.version),
+         losses=np.array(losses), metric_names=np.array(sorted(rep.metrics)),
+         metric_values=np.array(metrics), variant=np.array(variant), tau=np.array(tau),
+         beta=np.array(beta), lr=np.array(lr), steps=np.array(steps), **flat,
+         **flatten_groups(groups))
+
+
 def known_answers():
     """Frozen values from the reference tests (test_algorithms.py:109-188)."""
     vals = {
@@ -258,6 +303,10 @@ def main():
     buffer_case("buffer_fifo", 501, n_exp=60, n_tasks=5, group_size=4, n_take=6, policy="FIFO")
     buffer_case("buffer_priority", 502, n_exp=60, n_tasks=4, group_size=3, n_take=50, policy="PRIORITY")
     known_answers()
+    trainer_case("trainer_simple_anchor", 601, V=48, S=24, n_groups=2, K=3, variant="OPMD_SIMPLE",
+                 tau=0.5, beta=0.4, steps=3, lr=0.2, sft_n=3, dpo_pairs=2)
+    trainer_case("trainer_kimi", 602, V=64, S=32, n_groups=2, K=4, variant="OPMD_KIMI", tau=0.8,
+                 beta=0.0, steps=3, lr=0.1)
 
 
 if __name__ == "__main__":

@@ -72,35 +72,74 @@ def test_apply_update_refuses_nonfinite_and_bad_state():
     assert torch.equal(table, before)
 
 
-@pytest.mark.parametrize("name,variant,tau", [("simple_tau05", "OPMD_SIMPLE", 0.5),
-                                              ("kimi", "OPMD_KIMI", 1.0),
-                                              ("pairwise", "OPMD_PAIRWISE", 1.0)])
-def test_device_trainer_matches_host_trainer(name, variant, tau):
-    """Three steps of each reference group loss (golden inputs): the
-    device-resident table + tg_apply_update equals the host numpy path."""
+class _P:
+    def __init__(self, logits, version=0, vocab=None, num_buckets=None):
+        self.logits = np.asarray(logits, dtype=np.float64)
+        self.num_buckets = self.logits.shape[0]
+        self.version = version
+
+        class _V:
+            size = self.logits.shape[1]
+        self.vocab = vocab if vocab is not None else _V()
+
+
+@pytest.mark.parametrize("name", ["trainer_simple_anchor", "trainer_kimi"])
+def test_trainer_matches_reference_trainer(name):
+    """The reference's own orchestrator.Trainer (golden fixture: 3 step_groups,
+    then step_sft / step_dpo against the frozen anchor) against the
+    device-resident Trainer: every step's loss and metrics, the final table
+    and the version counter (orchestrator.py:288-322, algorithms.py:329-348)."""
     from _golden import groups_of, load
 
     from paper_2505_17826_b200 import triad_compat as C
 
-    class P:
-        def __init__(self, logits, version=0, vocab=None, num_buckets=None):
-            self.logits = np.asarray(logits, dtype=np.float64)
-            self.num_buckets = self.logits.shape[0]
-            self.version = version
-
-            class _V:
-                size = self.logits.shape[1]
-            self.vocab = vocab if vocab is not None else _V()
-
     fx = load(name)
+    algo = C.AlgorithmConfig(str(fx["variant"]), tau=float(fx["tau"]), beta=float(fx["beta"]),
+                             learning_rate=float(fx["lr"]))
+    tr = C.Trainer(_P(fx["theta"]), algo)
     groups = groups_of(fx)
-    algo = C.AlgorithmConfig(variant, tau=float(fx["tau"]) if "tau" in fx else tau,
-                             learning_rate=0.1)
-    host = C.Trainer(P(fx["theta"]), algo)
-    dev = C.DeviceTrainer(P(fx["theta"]), algo)
-    for _ in range(3):
-        rh = host.step_groups(groups)
-        rd = dev.step_groups(groups)
-        assert rd.loss == pytest.approx(rh.loss, rel=1e-5, abs=1e-7)
-    assert dev.version == host.params.version == 3
-    np.testing.assert_allclose(dev.params.logits, host.params.logits, rtol=1e-5, atol=1e-6)
+    names = [str(k) for k in fx["metric_names"]]
+    k = 0
+    for step in range(int(fx["steps"])):
+        rep = tr.step_groups(groups)
+        assert rep.loss == pytest.approx(float(fx["losses"][k]), rel=1e-5, abs=1e-7), step
+        for n, v in zip(names, fx["metric_values"][step]):
+            assert rep.metrics[n] == pytest.approx(float(v), rel=1e-5, abs=1e-7), (step, n)
+        k += 1
+    if "sft_tokens" in fx:
+        rep = tr.step_sft(groups_of(fx, "sft_")[0].experiences)
+        assert rep.loss == pytest.approx(float(fx["losses"][k]), rel=1e-5)
+        k += 1
+    if "dpo_tokens" in fx:
+        pairs = [(g.experiences[0], g.experiences[1]) for g in groups_of(fx, "dpo_")]
+        rep = tr.step_dpo(pairs)
+        assert rep.loss == pytest.approx(float(fx["losses"][k]), rel=1e-5)
+        k += 1
+    assert k == len(fx["losses"])
+    assert tr.version == tr.params.version == int(fx["version"])
+    np.testing.assert_allclose(tr.params.logits, fx["final"], rtol=1e-5, atol=1e-6)
+
+
+def test_apply_update_and_combine_reports_match_reference():
+    """combine_reports over per-group reports and apply_update of the merged
+    gradient (device SparseGrad, tg_apply_update) against the reference's
+    combined gradient (golden) and theta - lr * grad."""
+    from _golden import groups_of, load
+
+    from paper_2505_17826_b200 import triad_compat as C
+
+    fx = load("simple_tau05")
+    params = _P(fx["theta"])
+    algo = C.AlgorithmConfig("OPMD_SIMPLE", tau=float(fx["tau"]))
+    reps = [C.group_loss(g, params, algo) for g in groups_of(fx)]
+    comb = C.combine_reports(reps)
+    assert comb.loss == pytest.approx(float(fx["loss"]), rel=1e-5)
+    np.testing.assert_allclose(comb.gradient.to_dense(fx["theta"].shape), fx["grad"], atol=1e-6)
+    assert set(comb.gradient.rows) == set(fx["states"].tolist())   # every touched state
+    new = C.apply_update(params, comb.gradient, 0.3)
+    assert new.version == 1
+    np.testing.assert_allclose(new.logits, fx["theta"] - 0.3 * fx["grad"], rtol=1e-6, atol=1e-6)
+    bad = C.SparseGrad()
+    bad.add_row(0, np.full(fx["theta"].shape[1], np.nan))
+    with pytest.raises(AlgorithmError, match="non-finite"):
+        C.apply_update(params, bad, 0.1)

@@ -346,3 +346,21 @@ def test_blocked_single_pass_matches_general(cfg):
     assert out["loss"] == pytest.approx(ref["stats"][O.STAT["loss"]], rel=1e-12, abs=1e-14)
     assert np.max(np.abs(dz - ref["dz"])) <= 1e-14
     assert np.max(np.abs(out["lp"] - ref["lp"])) <= 1e-14
+
+
+@pytest.mark.parametrize("name", ["trainer_simple_anchor", "trainer_kimi"])
+def test_oracle_group_steps_reproduce_reference_trainer(name):
+    """Pins the trainer fixtures (the reference's own orchestrator.Trainer):
+    the oracle's reference-order group loss, scattered by state and applied as
+    theta -= lr * grad (algorithms.py:329-348), reproduces every step_groups
+    loss of the reference to the last bit (the later SFT / DPO steps are
+    covered by their own fixtures)."""
+    fx = load(name)
+    theta = fx["theta"].copy()
+    anchor = fx["theta"]
+    lr = float(fx["lr"])
+    for step in range(int(fx["steps"])):
+        batch, states = TP.pack_groups(groups_of(fx), theta, anchor)
+        rep = O.ref_group_batch(batch, str(fx["variant"]), float(fx["tau"]), float(fx["beta"]))
+        assert rep.loss == float(fx["losses"][step]), step
+        theta = theta - lr * TP.scatter_rows(rep.dz, states, theta.shape[0])
