@@ -24,8 +24,8 @@ OBJDIR = ROOT / "build" / "obj"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
               "-I", str(ROOT / "include"), "-I", str(CSRC)]
-CU_SOURCES = ["tg_fused_tma.cu", "tg_fused_l2.cu", "tg_stream.cu", "tg_group.cu", "tg_pack.cu",
-              "tg_lmhead.cu", "tg_update.cu", "tg_api.cu"]
+CU_SOURCES = ["tg_fused_tma.cu", "tg_stream.cu", "tg_group.cu", "tg_pack.cu", "tg_lmhead.cu",
+              "tg_update.cu", "tg_api.cu"]
 CPP_SOURCES = ["tg_host.cpp"]
 
 
@@ -55,9 +55,14 @@ def _stale(target: Path, deps) -> bool:
     return any(Path(d).stat().st_mtime > t for d in deps)
 
 
-# instrumented builds for kernel studies (never the product library):
+# builds for kernel studies (never the product library):
 #   prof -> libtg_loss_prof.so with per-CTA cycle accounting in k_fused_tma
-VARIANTS = {"prof": ["-DTG_FUSED_PROF"]}
+#   ab   -> libtg_loss_ab.so: the run-time A/B switches (TG_FUSED_CL, TG_FUSED_IMPL=2
+#           with the L2-reread kernel tg_fused_l2.cu, TG_FWD_TMA, TG_PREFETCH_ROWS,
+#           TG_FUSED_ANCHOR, TG_LMHEAD_PAIR / _ORDER); tests/test_gpu_alt_paths.py
+VARIANTS = {"prof": ["-DTG_FUSED_PROF"], "ab": ["-DTG_AB_SWITCHES"]}
+EXTRA_SOURCES = {"ab": ["tg_fused_l2.cu"]}
+AB_LIB = LIBDIR / "libtg_loss_ab.so"
 
 
 def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = False,
@@ -73,7 +78,7 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
     LIBDIR.mkdir(parents=True, exist_ok=True)
     headers = list(CSRC.glob("*.cuh")) + [ROOT / "include" / "tg_loss.h"]
     objs = []
-    for src in CU_SOURCES:
+    for src in CU_SOURCES + EXTRA_SOURCES.get(variant or "", []):
         obj = OBJDIR_ / (src + ".o")
         objs.append(obj)
         if force or _stale(obj, [CSRC / src, *headers]):

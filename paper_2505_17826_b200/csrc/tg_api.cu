@@ -48,9 +48,11 @@ cudaError_t launch_update(float* table, int64_t ld_table, int64_t n_states, int6
                           int64_t n_touched, int64_t n_rows, double lr, int32_t* status,
                           cudaStream_t stream);
 int lm_split(int64_t n_rows, int64_t vocab, int n_sms);
+#ifdef TG_AB_SWITCHES
 cudaError_t launch_fused_l2(const KParams& P, const void* meta, int n_ctas, int prefetch,
                             cudaStream_t st);
 int l2_threads();
+#endif
 int fused_max_clusters(int dtype, int cl);
 int fused_max_slots();
 int fused_resident_chunks();
@@ -311,13 +313,10 @@ struct FusedPlan {
   int cl = 0, n_slots = 0, n_ctas = 0, prefetch_rows = 1;
 };
 
-// Tuning overrides for measurement (A/B on the GPU without rebuilding):
+// Tuning overrides for measurement, A/B build only (tg_common.cuh ab_env):
 // TG_FUSED_CL=1|2|3|4 forces the cluster size, TG_PREFETCH_ROWS=n the L2
 // look-ahead depth (rows per cluster; 0 disables).
-int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return (v && *v) ? atoi(v) : dflt;
-}
+int env_int(const char* name, int dflt) { return ab_env(name, dflt); }
 
 FusedPlan fused_plan(const TgBatch* b, const TgOut* o, bool anchor = false) {
   FusedPlan fp;
@@ -535,10 +534,15 @@ int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspa
     count_launches(1);
   } else if (route == 1) {
     const FusedPlan fp = fused_plan(b, o, anchor);
-    // TG_FUSED_IMPL=l2: the L2-reread variant (tg_fused_l2.cu), for A/B
+#ifdef TG_AB_SWITCHES
+    // TG_FUSED_IMPL=2: the L2-reread variant (tg_fused_l2.cu), A/B build only
     const bool l2 = env_int("TG_FUSED_IMPL", 0) == 2;
     const int64_t l2_slots = int64_t(dev_info().sms) * (1024 / l2_threads());
     const int l2_ctas = int(b->n_rows < l2_slots ? b->n_rows : l2_slots);
+#else
+    constexpr bool l2 = false;
+    constexpr int l2_ctas = 0;
+#endif
     P.n_partials = l2 ? l2_ctas : fp.n_ctas;
     if (P.n_partials > kMaxPartials) return fail(TG_EUNSUPPORTED, "too many CTAs");
     if (b->n_rows > 0) {
@@ -546,8 +550,12 @@ int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspa
         launch_rowmeta(P, meta, st);
         count_launches(b->n_seqs > 0 ? 1 : 0);
       }
+#ifdef TG_AB_SWITCHES
       cudaError_t e = l2 ? launch_fused_l2(P, meta, l2_ctas, fp.prefetch_rows, st)
                          : launch_fused(P, meta, fp.cl, fp.n_slots, fp.n_ctas, fp.prefetch_rows, st);
+#else
+      cudaError_t e = launch_fused(P, meta, fp.cl, fp.n_slots, fp.n_ctas, fp.prefetch_rows, st);
+#endif
       if (e != cudaSuccess) return fail(TG_ECUDA, "fused kernel launch: %s", cudaGetErrorString(e));
       count_launches(1);
     } else {

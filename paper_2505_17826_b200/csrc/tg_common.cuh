@@ -5,6 +5,8 @@
 // block (a flattened TgBatch + TgConfig + TgOut + workspace carve-up).
 #pragma once
 
+#include <stdlib.h>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -235,6 +237,18 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
                : "memory");
 }
+
+// Run-time A/B switches (TG_FUSED_CL, TG_FUSED_IMPL, TG_FWD_TMA, ...) exist only
+// in the A/B build variant (`_build --variant=ab`, libtg_loss_ab.so); the
+// product library always takes the measured defaults.
+#ifdef TG_AB_SWITCHES
+inline int ab_env(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
+#else
+inline int ab_env(const char*, int dflt) { return dflt; }
+#endif
 
 // Programmatic dependent launch (PDL): a kernel launched with
 // cudaLaunchAttributeProgrammaticStreamSerialization may start while its

@@ -648,8 +648,8 @@ __global__ void k_lmhead_merge(const LmParams P) {
 static bool lm_pair_mode(bool dz = false) {
   static int mode = -2;
   if (mode == -2) {
-    const char* v = getenv("TG_LMHEAD_PAIR");
-    mode = (v && *v) ? (atoi(v) != 0) : -1;
+    const int v = ab_env("TG_LMHEAD_PAIR", -1);  // A/B build only
+    mode = v < 0 ? -1 : (v != 0);
   }
   return mode < 0 ? dz : mode != 0;
 }
@@ -664,8 +664,8 @@ static bool lm_pair_mode(bool dz = false) {
 static int lm_sp_major(int64_t cols, int64_t dim, int n_split, int n_sms) {
   static int mode = -2;
   if (mode == -2) {
-    const char* v = getenv("TG_LMHEAD_ORDER");
-    mode = (v && *v) ? (atoi(v) != 0) : -1;
+    const int v = ab_env("TG_LMHEAD_ORDER", -1);  // A/B build only
+    mode = v < 0 ? -1 : (v != 0);
   }
   if (mode >= 0) return mode;
   const double ws = 2.0 * double(dim) * (double(n_sms) * LM_BM + double(cols) / n_split);

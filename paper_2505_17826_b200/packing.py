@@ -154,7 +154,10 @@ class HostGroups:
 
 
 def flatten_groups(groups) -> HostGroups:
-    toks, masks, tok_off, plen, old, lens, gsz, rew, refs, exps = [], [], [0], [], [], [], [], [], [], []
+    """TaskGroups -> flat host arrays: each experience's token / mask / logprob
+    lists become numpy arrays in one C-level conversion each (no per-token
+    Python), then one concatenation per field.  Validation as records.py:21-131."""
+    toks, masks, olds, plen, lens, gsz, rew, refs, exps = [], [], [], [], [], [], [], [], []
     for g in groups:
         gexps = list(g.experiences)
         if not gexps:
@@ -164,28 +167,35 @@ def flatten_groups(groups) -> HostGroups:
             raise AlgorithmError("ref_logprobs length must match the group size")
         gsz.append(len(gexps))
         for j, e in enumerate(gexps):
-            n_true = sum(1 for m in e.action_mask if m)
-            if len(e.logprobs) != n_true:
-                raise AlgorithmError("logprobs length must match mask-true count")
-            if len(e.tokens) != len(e.action_mask):
+            t = np.asarray(e.tokens, dtype=np.int64).reshape(-1)
+            m = np.asarray(e.action_mask, dtype=bool).reshape(-1)
+            lp = np.asarray(e.logprobs, dtype=np.float64).reshape(-1)
+            if t.size != m.size:
                 raise AlgorithmError("action_mask length must match tokens")
+            n_true = int(np.count_nonzero(m))
+            if lp.size != n_true:
+                raise AlgorithmError("logprobs length must match mask-true count")
             if e.reward is None:
                 raise AlgorithmError("READY experience requires a reward")
-            toks.extend(int(t) for t in e.tokens)
-            masks.extend(1 if m else 0 for m in e.action_mask)
-            tok_off.append(len(toks))
+            toks.append(t)
+            masks.append(m)
+            olds.append(lp)
             plen.append(int(e.prompt_length))
-            old.extend(float(x) for x in e.logprobs)
             lens.append(n_true)
             rew.append(float(e.reward))
+            # records.py:64-66, 119-121: Experience.total_logprob = float(sum(logprobs)),
+            # a sequential left-to-right sum (kept bit-exact)
             refs.append(float(gref[j]) if gref is not None else float(sum(e.logprobs)))
             exps.append(e)
+    cat = (lambda xs, dt: np.concatenate(xs).astype(dt, copy=False) if xs
+           else np.zeros(0, dt))
+    tok_off = np.concatenate([[0], np.cumsum([t.size for t in toks], dtype=np.int64)])
     return HostGroups(
-        tokens=np.asarray(toks, np.int64), mask=np.asarray(masks, np.uint8),
-        tok_off=np.asarray(tok_off, np.int64), prompt_len=np.asarray(plen, np.int64),
-        old_lp=np.asarray(old, np.float64), seq_lengths=np.asarray(lens, np.int64),
-        group_sizes=np.asarray(gsz, np.int64), reward=np.asarray(rew, np.float64),
-        seq_ref_lp=np.asarray(refs, np.float64), experiences=exps)
+        tokens=cat(toks, np.int64), mask=cat(masks, np.uint8), tok_off=tok_off.astype(np.int64),
+        prompt_len=np.asarray(plen, np.int64), old_lp=cat(olds, np.float64),
+        seq_lengths=np.asarray(lens, np.int64), group_sizes=np.asarray(gsz, np.int64),
+        reward=np.asarray(rew, np.float64), seq_ref_lp=np.asarray(refs, np.float64),
+        experiences=exps)
 
 
 def scored_states(h: HostGroups, num_buckets: int):

@@ -223,7 +223,10 @@ def test_lmhead_backward_in_both_cta_modes(pair):
     import os
     import subprocess
     import sys
-    env = dict(os.environ, TG_LMHEAD_PAIR=pair)
+    from pathlib import Path
+    ab = Path(__file__).resolve().parents[1] / "paper_2505_17826_b200" / "_lib" / "libtg_loss_ab.so"
+    assert ab.exists(), "build the A/B variant (__graft_entry__.build())"
+    env = dict(os.environ, TG_LMHEAD_PAIR=pair, TG_LOSS_LIB=str(ab))  # switches: A/B build
     r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-q", "-x", "-p",
                         "no:cacheprovider", "-k", "matches_torch_fp32 or backward_from_hidden or matches_formula"],
                        env=env, capture_output=True, text=True, timeout=600)
