@@ -54,7 +54,7 @@
 extern "C" {
 #endif
 
-#define TG_ABI_VERSION 3
+#define TG_ABI_VERSION 4
 
 /* return codes */
 enum { TG_OK = 0, TG_EINVAL = 1, TG_ECUDA = 2, TG_EUNSUPPORTED = 3, TG_EWORKSPACE = 4 };
@@ -248,6 +248,35 @@ int tg_lmhead_dlogits(const void* hidden, int64_t ld_hidden, const void* weight,
                       int64_t ld_weight, int64_t n_rows, int64_t vocab, int64_t dim,
                       int64_t col0, int64_t n_cols, const int32_t* target, const float* lse,
                       const float* row_coef, void* dz, int64_t ld_dz, void* stream);
+
+/* The two gradient GEMMs of one vocabulary chunk, on the tensor cores (no
+   cuBLAS): dz [n_rows, ld_dz] bf16 is the chunk written by tg_lmhead_dlogits.
+     tg_lmhead_grad_hidden:  d_hidden [n_rows, ld_dh] fp32 (+)= dz . weight[col0 : col0 + n_cols]
+                             (accumulate != 0 adds to d_hidden -- the chunks of one
+                             step -- else overwrites it)
+     tg_lmhead_grad_weight:  d_weight [n_cols, ld_dw] bf16 = dz^T . hidden
+                             (the chunk's rows of d W; pass d_weight + col0 * ld_dw)
+   fp32 accumulation over the whole chunk / all rows.  Together with
+   tg_lmhead_logprob_fwd and tg_lmhead_dlogits they are the RFT loss's
+   backward through an LM head: the SparseGrad.add_row / apply_update
+   analogue (policy.py:215-250, algorithms.py:329-348) for a dense head.  Size
+   rules as tg_lmhead_logprob_fwd; ld_dh a multiple of 4, ld_dw of 8, all
+   pointers 16-byte aligned. */
+int tg_lmhead_grad_hidden(const void* dz, int64_t ld_dz, const void* weight, int64_t ld_weight,
+                          int64_t n_rows, int64_t vocab, int64_t dim, int64_t col0,
+                          int64_t n_cols, float* d_hidden, int64_t ld_dh, int accumulate,
+                          void* stream);
+int tg_lmhead_grad_weight(const void* dz, int64_t ld_dz, const void* hidden, int64_t ld_hidden,
+                          int64_t n_rows, int64_t dim, int64_t n_cols, void* d_weight,
+                          int64_t ld_dw, void* stream);
+/* Both GEMMs of one chunk in one launch (one tile queue over the two
+   outputs, so neither GEMM's partial last wave leaves SMs idle); the same
+   arguments and results as the two calls above. */
+int tg_lmhead_grad_chunk(const void* dz, int64_t ld_dz, const void* hidden, int64_t ld_hidden,
+                         const void* weight, int64_t ld_weight, int64_t n_rows, int64_t vocab,
+                         int64_t dim, int64_t col0, int64_t n_cols, float* d_hidden,
+                         int64_t ld_dh, int accumulate, void* d_weight, int64_t ld_dw,
+                         void* stream);
 
 /* Optimizer step: algorithms.apply_update (algorithms.py:329-348) on the
    device.  table [n_states, ld_table] fp32 (updated in place) gets

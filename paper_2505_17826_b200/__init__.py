@@ -8,8 +8,10 @@ logits -> logprob -> group advantage -> policy loss (+ KL, entropy, anchor KL)
 """
 
 from .config import AlgorithmError, RFTLossConfig, Variant
-from .loss import (LossOutput, RFTLoss, lmhead_dlogits, lmhead_logprob_fwd, lmhead_loss_fwd,
-                   lmhead_loss_fwd_bwd, logprob_fwd, stats_to_metrics)
+from .loss import (LossOutput, RFTLoss, lmhead_dlogits, lmhead_grad_chunk, lmhead_grad_hidden,
+                   lmhead_grad_weight,
+                   lmhead_logprob_fwd, lmhead_loss_fwd, lmhead_loss_fwd_bwd, logprob_fwd,
+                   stats_to_metrics)
 from .packing import PackedBatch, PolicyError, group_by_task, pack_arrays
 from .registry import (ADVANTAGE_FNS, ENTROPY_LOSS_FNS, KL_FNS, LOSS_AGG_MODES,
                        POLICY_LOSS_FNS)
@@ -17,6 +19,6 @@ from .registry import (ADVANTAGE_FNS, ENTROPY_LOSS_FNS, KL_FNS, LOSS_AGG_MODES,
 __all__ = [
     "AlgorithmError", "PolicyError", "RFTLossConfig", "Variant", "RFTLoss", "LossOutput",
     "logprob_fwd", "lmhead_logprob_fwd", "lmhead_loss_fwd", "lmhead_loss_fwd_bwd",
-    "lmhead_dlogits", "stats_to_metrics", "PackedBatch", "pack_arrays", "group_by_task",
+    "lmhead_dlogits", "lmhead_grad_chunk", "lmhead_grad_hidden", "lmhead_grad_weight", "stats_to_metrics", "PackedBatch", "pack_arrays", "group_by_task",
     "ADVANTAGE_FNS", "POLICY_LOSS_FNS", "KL_FNS", "ENTROPY_LOSS_FNS", "LOSS_AGG_MODES",
 ]

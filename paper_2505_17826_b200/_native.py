@@ -77,9 +77,10 @@ EXPORTED = [
     "tg_last_error", "tg_abi_version", "tg_scored_states", "tg_group_by_task",
     "tg_set_timing_events", "tg_launch_count", "tg_pack_rows", "tg_lmhead_logprob_fwd",
     "tg_lmhead_workspace_size", "tg_apply_update", "tg_lmhead_dlogits", "tg_fused_cluster_size",
+    "tg_lmhead_grad_hidden", "tg_lmhead_grad_weight", "tg_lmhead_grad_chunk",
 ]
 
-ABI_VERSION = 3  # include/tg_loss.h TG_ABI_VERSION
+ABI_VERSION = 4  # include/tg_loss.h TG_ABI_VERSION
 
 _lib = None
 
@@ -151,6 +152,17 @@ def lib() -> ctypes.CDLL:
     L.tg_lmhead_dlogits.argtypes = [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64,
                                     c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
                                     c_void_p, c_int64, c_void_p]
+    L.tg_lmhead_grad_hidden.restype = c_int
+    L.tg_lmhead_grad_hidden.argtypes = [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64,
+                                        c_int64, c_int64, c_int64, c_void_p, c_int64, c_int,
+                                        c_void_p]
+    L.tg_lmhead_grad_weight.restype = c_int
+    L.tg_lmhead_grad_weight.argtypes = [c_void_p, c_int64, c_void_p, c_int64, c_int64, c_int64,
+                                        c_int64, c_void_p, c_int64, c_void_p]
+    L.tg_lmhead_grad_chunk.restype = c_int
+    L.tg_lmhead_grad_chunk.argtypes = [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64,
+                                       c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p,
+                                       c_int64, c_int, c_void_p, c_int64, c_void_p]
     if L.tg_abi_version() != ABI_VERSION:
         raise RuntimeError("libtg_loss ABI mismatch")
     _lib = L

@@ -27,9 +27,8 @@
 
 namespace tg {
 size_t fused_smem_bytes(int n_slots);
-cudaError_t launch_fused(const KParams& P, const void* meta, int cl, int n_slots, int n_ctas,
-                         int prefetch_rows,
-                         cudaStream_t stream);
+cudaError_t launch_fused(const KParams& P, const void* meta, int cl, int amode, int n_slots,
+                         int n_ctas, int prefetch_rows, cudaStream_t stream);
 int fused_chunk_bytes();
 cudaError_t launch_lmhead_logprob(const void* hidden, int64_t ld_hidden, const void* weight,
                                   int64_t ld_weight, int64_t n_rows, int64_t vocab, int64_t dim,
@@ -48,6 +47,18 @@ cudaError_t launch_update(float* table, int64_t ld_table, int64_t n_states, int6
                           int64_t n_touched, int64_t n_rows, double lr, int32_t* status,
                           cudaStream_t stream);
 int lm_split(int64_t n_rows, int64_t vocab, int n_sms);
+cudaError_t launch_grad_hidden(const void* dz, int64_t ld_dz, const void* weight,
+                               int64_t ld_weight, int64_t n_rows, int64_t n_cols, int64_t dim,
+                               int64_t col0, float* d_hidden, int64_t ld_dh, int accumulate,
+                               int n_sms, cudaStream_t stream);
+cudaError_t launch_grad_weight(const void* dz, int64_t ld_dz, const void* hidden,
+                               int64_t ld_hidden, int64_t n_rows, int64_t n_cols, int64_t dim,
+                               void* d_weight, int64_t ld_dw, int n_sms, cudaStream_t stream);
+cudaError_t launch_grad_chunk(const void* dz, int64_t ld_dz, const void* hidden,
+                              int64_t ld_hidden, const void* weight, int64_t ld_weight,
+                              int64_t n_rows, int64_t n_cols, int64_t dim, int64_t col0,
+                              float* d_hidden, int64_t ld_dh, int accumulate, void* d_weight,
+                              int64_t ld_dw, int n_sms, cudaStream_t stream);
 #ifdef TG_AB_SWITCHES
 cudaError_t launch_fused_l2(const KParams& P, const void* meta, int n_ctas, int prefetch,
                             cudaStream_t st);
@@ -56,6 +67,7 @@ int l2_threads();
 int fused_max_clusters(int dtype, int cl);
 int fused_max_slots();
 int fused_resident_chunks();
+int fused_resident_chunks_z();
 size_t rowmeta_bytes();
 void launch_fwd(const KParams& P, bool anchor, bool vec, int grid, cudaStream_t st);
 cudaError_t launch_fwd_tma(const KParams& P, int n_sms, cudaStream_t stream);
@@ -311,6 +323,7 @@ void fill_params(KParams& P, const TgBatch* b, const TgConfig* c, const TgOut* o
 // Fused-kernel plan: cluster size and ring slots, or cl = 0 if not eligible.
 struct FusedPlan {
   int cl = 0, n_slots = 0, n_ctas = 0, prefetch_rows = 1;
+  int amode = 0;  // anchor KL: 1 = z + za stashed, 2 = z stashed, za re-read from L2
 };
 
 // Tuning overrides for measurement, A/B build only (tg_common.cuh ab_env):
@@ -344,6 +357,15 @@ FusedPlan fused_plan(const TgBatch* b, const TgOut* o, bool anchor = false) {
   if (n_slots > fused_max_slots()) n_slots = fused_max_slots();
   if (n_slots < fused_max_slots()) return fp;  // the kernel's ring size is compile-time
   static const int kOrder[4] = {1, 2, 4, 3};
+  // anchor KL: mode 1 (z and za stashed) at the smallest cluster size that
+  // holds both slices, else mode 2 (z stashed, za re-read from L2 in phase 2:
+  // twice the columns per CTA).  Mode 2 where mode 1 also fits measured slower
+  // (profiles/r02_anchor_modes.txt: 4.63 vs 4.99 TB/s at V = 151,936 bf16,
+  // CL = 2 vs 4 -- the L2 re-read stalls phase 2 and 7 % of it misses), so it
+  // only serves rows mode 1 cannot hold (fp32 at Qwen vocabulary: 6V bytes
+  // instead of the two-pass 10V).  TG_FUSED_ANCHOR_MODE forces one (A/B build).
+  const int force_mode = anchor ? env_int("TG_FUSED_ANCHOR_MODE", 0) : 0;
+  for (int pass = 0; pass < (anchor ? 2 : 1); ++pass)
   for (int oi = 0; oi < 4; ++oi) {
     const int cl = kOrder[oi];
     if (force_cl ? cl != force_cl : cl == 3) continue;  // CL = 3 only on request
@@ -351,16 +373,29 @@ FusedPlan fused_plan(const TgBatch* b, const TgOut* o, bool anchor = false) {
     const int64_t slice_vec = (nvec + cl - 1) / cl;
     const int64_t nchunk = (slice_vec * 16 + fused_chunk_bytes() - 1) / fused_chunk_bytes();
     // resident TMEM chunks: the slice + >= 2 prefix chunks (anchor: a stash
-    // slot holds a z + za half-chunk pair)
+    // slot holds a z + za half-chunk pair in mode 1, the z half chunk in mode 2)
     const int64_t half = fused_chunk_bytes() / 2;
     const int64_t nslot = anchor ? (slice_vec * 16 + half - 1) / half : nchunk;
     // (a forced cluster size may run with a single slot of look-ahead)
-    if (nslot + ((force_cl && anchor) ? 1 : 2) <= fused_resident_chunks()) {
+    const int64_t need = nslot + ((force_cl && anchor) ? 1 : 2);
+    int amode = 0;
+    if (anchor) {
+      const int want = force_mode ? force_mode : pass + 1;
+      if (want == pass + 1) {
+        if (want == 1 && need <= fused_resident_chunks()) amode = 1;
+        if (want == 2 && need <= fused_resident_chunks_z() &&
+            (cl == 2 || (cl == 1 && b->dtype == TG_DTYPE_BF16) ||
+             (cl == 4 && b->dtype != TG_DTYPE_BF16)))  // instantiated
+          amode = 2;
+      }
+    }
+    if (anchor ? amode != 0 : need <= fused_resident_chunks()) {
       // persistent grid: as many clusters as can be co-resident, at most one per row
       int64_t clusters_max = fused_max_clusters(b->dtype, cl);
       if (clusters_max <= 0) clusters_max = d.sms / cl;
       const int64_t clusters = b->n_rows < clusters_max ? b->n_rows : clusters_max;
       fp.cl = cl;
+      fp.amode = amode;
       fp.n_slots = n_slots;
       fp.n_ctas = int(clusters * cl);
       return fp;
@@ -518,7 +553,7 @@ int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspa
     P.n_partials = fp.n_ctas;
     if (P.n_partials > kMaxPartials) return fail(TG_EUNSUPPORTED, "too many CTAs");
     if (b->n_rows > 0) {
-      cudaError_t e = launch_fused(P, meta, fp.cl, fp.n_slots, fp.n_ctas, fp.prefetch_rows, st);
+      cudaError_t e = launch_fused(P, meta, fp.cl, fp.amode, fp.n_slots, fp.n_ctas, fp.prefetch_rows, st);
       if (e != cudaSuccess) return fail(TG_ECUDA, "fused kernel launch: %s", cudaGetErrorString(e));
       count_launches(1);
     }
@@ -552,9 +587,9 @@ int tg_loss_fwd_bwd(const TgBatch* b, const TgConfig* c, TgOut* o, void* workspa
       }
 #ifdef TG_AB_SWITCHES
       cudaError_t e = l2 ? launch_fused_l2(P, meta, l2_ctas, fp.prefetch_rows, st)
-                         : launch_fused(P, meta, fp.cl, fp.n_slots, fp.n_ctas, fp.prefetch_rows, st);
+                         : launch_fused(P, meta, fp.cl, fp.amode, fp.n_slots, fp.n_ctas, fp.prefetch_rows, st);
 #else
-      cudaError_t e = launch_fused(P, meta, fp.cl, fp.n_slots, fp.n_ctas, fp.prefetch_rows, st);
+      cudaError_t e = launch_fused(P, meta, fp.cl, fp.amode, fp.n_slots, fp.n_ctas, fp.prefetch_rows, st);
 #endif
       if (e != cudaSuccess) return fail(TG_ECUDA, "fused kernel launch: %s", cudaGetErrorString(e));
       count_launches(1);
@@ -702,6 +737,102 @@ int tg_lmhead_dlogits(const void* hidden, int64_t ld_hidden, const void* weight,
     return fail(TG_EUNSUPPORTED, "cuTensorMapEncodeTiled is unavailable (driver too old)");
   count_launches(1);
   if (e != cudaSuccess) return fail(TG_ECUDA, "tg_lmhead_dlogits: %s", cudaGetErrorString(e));
+  return TG_OK;
+}
+
+int tg_lmhead_grad_hidden(const void* dz, int64_t ld_dz, const void* weight, int64_t ld_weight,
+                          int64_t n_rows, int64_t vocab, int64_t dim, int64_t col0,
+                          int64_t n_cols, float* d_hidden, int64_t ld_dh, int accumulate,
+                          void* stream) {
+  // (hidden is not read: check the weight's layout with itself in its place)
+  const int rc = lmhead_check(weight, ld_weight, weight, ld_weight, n_rows, vocab, dim);
+  if (rc) return rc;
+  if (col0 < 0 || n_cols < 1 || col0 + n_cols > vocab)
+    return fail(TG_EINVAL, "vocabulary chunk [%lld, %lld) outside [0, %lld)", (long long)col0,
+                (long long)(col0 + n_cols), (long long)vocab);
+  if (ld_dz < n_cols || ld_dz % 8 != 0)
+    return fail(TG_EINVAL, "ld_dz must be >= n_cols and a multiple of 8, got %lld",
+                (long long)ld_dz);
+  if (ld_dh < dim || ld_dh % 4 != 0)
+    return fail(TG_EINVAL, "ld_dh must be >= dim and a multiple of 4, got %lld", (long long)ld_dh);
+  if (n_rows == 0) return TG_OK;
+  if (!dz || !d_hidden) return fail(TG_EINVAL, "dz and d_hidden are required");
+  if (!aligned16(dz) || !aligned16(d_hidden))
+    return fail(TG_EINVAL, "dz and d_hidden must be 16-byte aligned");
+  const DevInfo d = dev_info();
+  cudaGetLastError();
+  cudaError_t e = launch_grad_hidden(dz, ld_dz, weight, ld_weight, n_rows, n_cols, dim, col0,
+                                     d_hidden, ld_dh, accumulate, d.sms > 0 ? d.sms : 148,
+                                     reinterpret_cast<cudaStream_t>(stream));
+  if (e == cudaErrorNotSupported)
+    return fail(TG_EUNSUPPORTED, "cuTensorMapEncodeTiled is unavailable (driver too old)");
+  count_launches(1);
+  if (e != cudaSuccess) return fail(TG_ECUDA, "tg_lmhead_grad_hidden: %s", cudaGetErrorString(e));
+  return TG_OK;
+}
+
+int tg_lmhead_grad_weight(const void* dz, int64_t ld_dz, const void* hidden, int64_t ld_hidden,
+                          int64_t n_rows, int64_t dim, int64_t n_cols, void* d_weight,
+                          int64_t ld_dw, void* stream) {
+  const int rc = lmhead_check(hidden, ld_hidden, hidden, ld_hidden, n_rows, n_cols, dim);
+  if (rc) return rc;
+  if (ld_dz < n_cols || ld_dz % 8 != 0)
+    return fail(TG_EINVAL, "ld_dz must be >= n_cols and a multiple of 8, got %lld",
+                (long long)ld_dz);
+  if (ld_dw < dim || ld_dw % 8 != 0)
+    return fail(TG_EINVAL, "ld_dw must be >= dim and a multiple of 8, got %lld", (long long)ld_dw);
+  if (!d_weight || !aligned16(d_weight)) return fail(TG_EINVAL, "d_weight must be 16-byte aligned");
+  if (n_rows > 0 && (!dz || !aligned16(dz))) return fail(TG_EINVAL, "dz must be 16-byte aligned");
+  const DevInfo d = dev_info();
+  cudaGetLastError();
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (n_rows == 0) {  // an empty batch has a zero gradient
+    e = cudaMemset2DAsync(d_weight, size_t(ld_dw) * 2, 0, size_t(dim) * 2, size_t(n_cols), st);
+  } else {
+    e = launch_grad_weight(dz, ld_dz, hidden, ld_hidden, n_rows, n_cols, dim, d_weight, ld_dw,
+                           d.sms > 0 ? d.sms : 148, st);
+    if (e == cudaErrorNotSupported)
+      return fail(TG_EUNSUPPORTED, "cuTensorMapEncodeTiled is unavailable (driver too old)");
+    count_launches(1);
+  }
+  if (e != cudaSuccess) return fail(TG_ECUDA, "tg_lmhead_grad_weight: %s", cudaGetErrorString(e));
+  return TG_OK;
+}
+
+int tg_lmhead_grad_chunk(const void* dz, int64_t ld_dz, const void* hidden, int64_t ld_hidden,
+                         const void* weight, int64_t ld_weight, int64_t n_rows, int64_t vocab,
+                         int64_t dim, int64_t col0, int64_t n_cols, float* d_hidden,
+                         int64_t ld_dh, int accumulate, void* d_weight, int64_t ld_dw,
+                         void* stream) {
+  const int rc = lmhead_check(hidden, ld_hidden, weight, ld_weight, n_rows, vocab, dim);
+  if (rc) return rc;
+  if (col0 < 0 || n_cols < 1 || col0 + n_cols > vocab)
+    return fail(TG_EINVAL, "vocabulary chunk [%lld, %lld) outside [0, %lld)", (long long)col0,
+                (long long)(col0 + n_cols), (long long)vocab);
+  if (ld_dz < n_cols || ld_dz % 8 != 0)
+    return fail(TG_EINVAL, "ld_dz must be >= n_cols and a multiple of 8, got %lld",
+                (long long)ld_dz);
+  if (ld_dh < dim || ld_dh % 4 != 0)
+    return fail(TG_EINVAL, "ld_dh must be >= dim and a multiple of 4, got %lld", (long long)ld_dh);
+  if (ld_dw < dim || ld_dw % 8 != 0)
+    return fail(TG_EINVAL, "ld_dw must be >= dim and a multiple of 8, got %lld", (long long)ld_dw);
+  if (n_rows == 0)  // d hidden has no rows; d W of an empty batch is zero
+    return tg_lmhead_grad_weight(dz, ld_dz, hidden, ld_hidden, 0, dim, n_cols, d_weight, ld_dw,
+                                 stream);
+  if (!dz || !d_hidden || !d_weight) return fail(TG_EINVAL, "dz, d_hidden and d_weight are required");
+  if (!aligned16(dz) || !aligned16(d_hidden) || !aligned16(d_weight))
+    return fail(TG_EINVAL, "dz, d_hidden and d_weight must be 16-byte aligned");
+  const DevInfo d = dev_info();
+  cudaGetLastError();
+  cudaError_t e = launch_grad_chunk(dz, ld_dz, hidden, ld_hidden, weight, ld_weight, n_rows,
+                                    n_cols, dim, col0, d_hidden, ld_dh, accumulate, d_weight,
+                                    ld_dw, d.sms > 0 ? d.sms : 148,
+                                    reinterpret_cast<cudaStream_t>(stream));
+  if (e == cudaErrorNotSupported)
+    return fail(TG_EUNSUPPORTED, "cuTensorMapEncodeTiled is unavailable (driver too old)");
+  count_launches(1);
+  if (e != cudaSuccess) return fail(TG_ECUDA, "tg_lmhead_grad_chunk: %s", cudaGetErrorString(e));
   return TG_OK;
 }
 

@@ -85,6 +85,7 @@ struct FusedSmemTail {
   float4 bcast[2];  // (a, h, lse, s) of a row, from the epilogue warp
   float wpart_q[2][4 * kConsumerWarps];  // kA: every CTA's anchor log-sum-exp partials
   float bcast_ca[2];                     // kA: the row's anchor coefficient ca
+  float zy[2];  // CL > 1: the row's target logit, from the CTA whose slice holds it
   uint32_t tmem_base;  // TG_TMEM_STASH: 512 TMEM columns of this CTA
 #ifdef TG_FUSED_PROF
   unsigned long long prof[16];
@@ -183,6 +184,49 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint4 (&u)[4]) {
       "r"(u[1].w), "r"(u[2].x), "r"(u[2].y), "r"(u[2].z), "r"(u[2].w), "r"(u[3].x), "r"(u[3].y),
       "r"(u[3].z), "r"(u[3].w)
       : "memory");
+}
+
+// anchor mode 2: a z-only stash slot (2 vectors = 8 columns per thread), 16 per warp
+constexpr int kTSlotsZ = 16;
+__device__ __forceinline__ uint32_t stash_addr_z(const RingBase& rb, uint32_t chunk) {
+  return rb.tmem + (chunk % uint32_t(kTSlotsZ)) * 8u;
+}
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint4& a, const uint4& b) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+      "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint4& a, uint4& b) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+#ifndef TG_ZA_EVICT_LAST
+#define TG_ZA_EVICT_LAST 1
+#endif
+__device__ __forceinline__ uint64_t policy_za() {
+  uint64_t p;
+  if (TG_ZA_EVICT_LAST)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// L2-resident re-read of the anchor row (mode 2): read-only path, no L1
+// allocation, evict-first once consumed
+__device__ __forceinline__ uint4 ld_l2_hint(const void* p, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
 }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint4 (&u)[4]) {
@@ -657,7 +701,7 @@ __device__ __forceinline__ void accumulate_a(const uint4& uz, const uint4& uq, u
   }
 }
 
-template <typename T, bool kPartial, bool kMaskTail>
+template <typename T, int kMode, bool kPartial, bool kMaskTail>
 __device__ __forceinline__ void phase1_chunk_a(AccA& acc, RingIt& it, const RingBase& rb,
                                                int vbase, const Slice& sl, int tid) {
   uint4 u[2 * kVA];  // [0, kVA): z vectors, [kVA, 2 kVA): za vectors of the same columns
@@ -676,7 +720,10 @@ __device__ __forceinline__ void phase1_chunk_a(AccA& acc, RingIt& it, const Ring
     u[kVA + g] = valid[g] ? lds128(a + kHalf + g * kConsumers * 16) : Pk<T>::neutral();
   }
   static_assert(2 * kVA == 4, "one 16-column stash slot per z + za pair");
-  tmem_st16(stash_addr(rb, it.c), u);
+  if constexpr (kMode == 2)  // z only: za is re-read from L2 in phase 2
+    tmem_st8(stash_addr_z(rb, it.c), u[0], u[1]);
+  else
+    tmem_st16(stash_addr(rb, it.c), u);
   __syncwarp();
   if ((tid & 31) == 0) arrive_u32(it.empty(rb));
   it.next();
@@ -756,7 +803,7 @@ __device__ __forceinline__ void phase1_chunk_a(AccA& acc, RingIt& it, const Ring
 }
 
 // logical chunks [c0, c1) of a row whose first ring position is `row_it`
-template <typename T>
+template <typename T, int kMode>
 __device__ __forceinline__ void phase1_range_a(AccA& acc, RingIt row_it, const RingBase& rb,
                                                const Slice& sl, int c0, int c1, int tid) {
   RingIt it = row_it;
@@ -766,11 +813,11 @@ __device__ __forceinline__ void phase1_range_a(AccA& acc, RingIt row_it, const R
     const int vend = vbase + kVecPerChunkA;
     const bool has_tail = sl.tail_vec >= vbase && sl.tail_vec < vend;
     if (vend <= sl.v1 && !has_tail)
-      phase1_chunk_a<T, false, false>(acc, it, rb, vbase, sl, tid);
+      phase1_chunk_a<T, kMode, false, false>(acc, it, rb, vbase, sl, tid);
     else if (!has_tail)
-      phase1_chunk_a<T, true, false>(acc, it, rb, vbase, sl, tid);
+      phase1_chunk_a<T, kMode, true, false>(acc, it, rb, vbase, sl, tid);
     else
-      phase1_chunk_a<T, true, true>(acc, it, rb, vbase, sl, tid);
+      phase1_chunk_a<T, kMode, true, true>(acc, it, rb, vbase, sl, tid);
     vbase = vend;
   }
 }
@@ -795,15 +842,23 @@ __device__ __forceinline__ float4 warp_partial_a(const AccA& acc, float& lq) {
 }
 
 // phase 2 of one logical chunk: z and za from the two stash slots
-template <typename T, bool kCheck>
+// (mode 2: z from the stash, za = q[] re-read from L2 by the caller)
+template <typename T, int kMode, bool kCheck>
 __device__ __forceinline__ void phase2_chunk_a(const RingIt& it, const RingBase& rb, int vbase,
                                                const Slice& sl, char* dzrow, int vy, int ye,
                                                float s_t, uint64_t nl2, uint64_t av2,
-                                               uint64_t hz2, uint64_t nca2, int tid) {
+                                               uint64_t hz2, uint64_t nca2, int tid,
+                                               const uint4 (&q)[kVA]) {
   constexpr int EPV = Vec<T>::N;
   char* dst = dzrow + int64_t(vbase + tid) * 16;
   uint4 su[2 * kVA];
-  tmem_ld16(stash_addr(rb, it.c), su);
+  if constexpr (kMode == 2) {
+    tmem_ld8(stash_addr_z(rb, it.c), su[0], su[1]);
+#pragma unroll
+    for (int g = 0; g < kVA; ++g) su[kVA + g] = q[g];
+  } else {
+    tmem_ld16(stash_addr(rb, it.c), su);
+  }
   const uint64_t l2e2 = pk2(kLog2e, kLog2e);
 #pragma unroll
   for (int g = 0; g < kVA; ++g) {
@@ -839,20 +894,44 @@ __device__ __forceinline__ void phase2_chunk_a(const RingIt& it, const RingBase&
   }
 }
 
+// mode 2: the za vectors of one chunk from L2 (neutral past the slice end)
 template <typename T>
+__device__ __forceinline__ void load_za(uint4 (&q)[kVA], const char* qrow, int vbase,
+                                        const Slice& sl, int tid, uint64_t pol) {
+#pragma unroll
+  for (int g = 0; g < kVA; ++g) {
+    const int vec = vbase + g * kConsumers + tid;
+    q[g] = vec < sl.v1 ? ld_l2_hint(qrow + int64_t(vec) * 16, pol) : Pk<T>::neutral();
+  }
+}
+
+template <typename T, int kMode>
 __device__ __forceinline__ void phase2_row_a(const Slice& sl, RingIt it, const RingBase& rb,
-                                             char* dzrow, int vy, int ye, float s_t,
-                                             uint64_t nl2, uint64_t av2, uint64_t hz2,
-                                             uint64_t nca2, int tid) {
+                                             const char* qrow, char* dzrow, int vy, int ye,
+                                             float s_t, uint64_t nl2, uint64_t av2, uint64_t hz2,
+                                             uint64_t nca2, int tid, uint64_t pol) {
   int vbase = sl.v0;
+  uint4 q[kVA];
+  // mode 2: the za loads run one chunk ahead of their use (L2 latency)
+  if constexpr (kMode == 2) load_za<T>(q, qrow, vbase, sl, tid, pol);
   for (int j = 0; j < sl.nchunk; ++j) {
     const int vend = vbase + kVecPerChunkA;
+    uint4 qn[kVA];
+    if constexpr (kMode == 2) {
+      if (j + 1 < sl.nchunk) load_za<T>(qn, qrow, vend, sl, tid, pol);
+    }
     const bool check = (vend > sl.v1) || (sl.tail_vec >= vbase && sl.tail_vec < vend) ||
                        (vy >= vbase && vy < vend);
     if (check)
-      phase2_chunk_a<T, true>(it, rb, vbase, sl, dzrow, vy, ye, s_t, nl2, av2, hz2, nca2, tid);
+      phase2_chunk_a<T, kMode, true>(it, rb, vbase, sl, dzrow, vy, ye, s_t, nl2, av2, hz2, nca2,
+                                     tid, q);
     else
-      phase2_chunk_a<T, false>(it, rb, vbase, sl, dzrow, vy, ye, s_t, nl2, av2, hz2, nca2, tid);
+      phase2_chunk_a<T, kMode, false>(it, rb, vbase, sl, dzrow, vy, ye, s_t, nl2, av2, hz2,
+                                      nca2, tid, q);
+    if constexpr (kMode == 2) {
+#pragma unroll
+      for (int g = 0; g < kVA; ++g) q[g] = qn[g];
+    }
     it.next();
     vbase = vend;
   }
@@ -888,7 +967,7 @@ __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
 // Consumer warps of the fused anchor path: the same row loop as the default
 // consumers (first row's prefix, phase 1, partial post to every CTA of the
 // cluster, next row's prefix, phase 2), over z + za half-chunk pairs.
-template <typename T, int CL>
+template <typename T, int CL, int kMode>
 __device__ __forceinline__ void consumer_rows_a(const KParams& P, FusedSmemTail* tail,
                                                 const RingBase& rb, const Slice& sl, int pre,
                                                 int64_t cid, int64_t ncl, uint32_t rank,
@@ -902,13 +981,14 @@ __device__ __forceinline__ void consumer_rows_a(const KParams& P, FusedSmemTail*
 #endif
   RingIt pos0 = {0u};
   AccA acc = acc_init_a();
+  const uint64_t pol_q = policy_evict_first();  // mode 2: the anchor row's last use
   int vtid = tid;
   if constexpr (kConsumerWarps == 16) {  // sub-partitions 2 / 3 first (see the default path)
     const int q = warp & 3, grp = warp >> 2;
     const int vw = (q >= 2) ? (grp * 2 + (q - 2)) : (8 + grp * 2 + q);
     vtid = vw * 32 + lane;
   }
-  if (cid < NR) phase1_range_a<T>(acc, pos0, rb, sl, 0, pre, vtid);
+  if (cid < NR) phase1_range_a<T, kMode>(acc, pos0, rb, sl, 0, pre, vtid);
   int64_t k = 0;
   for (int64_t row = cid; row < NR; row += ncl, ++k) {
     const int64_t nrow = row + ncl;
@@ -916,7 +996,7 @@ __device__ __forceinline__ void consumer_rows_a(const KParams& P, FusedSmemTail*
     const int vy = (y >= 0 && y < V) ? (y / EPV) : -1;
     const int ye = (vy >= 0) ? y - vy * EPV : 0;
     const int par = int(k & 1);
-    phase1_range_a<T>(acc, pos0, rb, sl, pre, sl.nchunk, vtid);
+    phase1_range_a<T, kMode>(acc, pos0, rb, sl, pre, sl.nchunk, vtid);
     float lq;
     const float4 o = warp_partial_a(acc, lq);
     if (lane == 0) {
@@ -939,7 +1019,7 @@ __device__ __forceinline__ void consumer_rows_a(const KParams& P, FusedSmemTail*
     RingIt npos = pos0;
     npos.advance(sl.nchunk);
     acc_new_row_a(acc);
-    if (nrow < NR) phase1_range_a<T>(acc, npos, rb, sl, 0, pre, vtid);
+    if (nrow < NR) phase1_range_a<T, kMode>(acc, npos, rb, sl, 0, pre, vtid);
     {
       TG_PROF_T0();
       mbar_wait_u32<(CL == 1 ? 0 : TG_SLEEP_BCAST)>(smem_u32(&tail->bbar[par]),
@@ -953,7 +1033,9 @@ __device__ __forceinline__ void consumer_rows_a(const KParams& P, FusedSmemTail*
     const uint64_t nl2 = pk2(-lseL, -lseL), av2 = pk2(bc.x, bc.x), hz2 = pk2(bc.y, bc.y);
     const uint64_t nca2 = pk2(-ca, -ca);
     char* dzrow = reinterpret_cast<char*>(P.dz) + row * P.ld_out * ESZ;
-    phase2_row_a<T>(sl, pos0, rb, dzrow, vy, ye, bc.w, nl2, av2, hz2, nca2, vtid);
+    const char* qrow = reinterpret_cast<const char*>(P.anchor) + row * P.ld_anchor * ESZ;
+    phase2_row_a<T, kMode>(sl, pos0, rb, qrow, dzrow, vy, ye, bc.w, nl2, av2, hz2, nca2, vtid,
+                           pol_q);
     pos0 = npos;
 #ifdef TG_FUSED_PROF
     if (tid == 0) tail->prof[6] += 1;
@@ -964,10 +1046,13 @@ __device__ __forceinline__ void consumer_rows_a(const KParams& P, FusedSmemTail*
 #endif
 }
 
-template <typename T, int CL, bool kA = false>
+template <typename T, int CL, int kA = 0>
 __global__ void __launch_bounds__(kFusedThreads, 1)
     k_fused_tma(const KParams P, const RowMeta* __restrict__ meta, int prefetch_rows) {
-  static_assert(!kA || kStash, "the fused anchor path keeps z and za in the TMEM stash");
+  // kA: 0 no anchor; 1 anchor KL with z and za in the TMEM stash; 2 anchor KL
+  // with z in the stash and za re-read from L2 in phase 2 (twice the stash
+  // columns per slot: Qwen-vocabulary rows fit 2-CTA clusters, all 148 SMs)
+  static_assert(!kA || kStash, "the fused anchor path keeps the row slices in the TMEM stash");
   // kA: a ring / stash slot holds a z + za half-chunk pair
   constexpr int EPV = Vec<T>::N;  // elements per 16-byte vector
   constexpr int ESZ = elem_bytes<T>();
@@ -994,8 +1079,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   sl.tail_vec = (V % EPV) ? nvec - 1 : -1;  // global vector holding columns >= V
   sl.tail_valid = V - (nvec - 1) * EPV;
   // next-row phase-1 chunks that fit in the ring beside this row's slice
-  const int pre =
-      min(min(kMaxPrefixChunks, (kStash ? kTSlots : kSlots) - sl.nchunk), sl.nchunk);
+  const int pre = min(
+      min(kMaxPrefixChunks, (kStash ? (kA == 2 ? kTSlotsZ : kTSlots) : kSlots) - sl.nchunk),
+      sl.nchunk);
 
   if (tid == 0) {
     for (int i = 0; i < kSlots; ++i) {
@@ -1044,6 +1130,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     // ===================== producer warp: bulk TMA into the ring =====================
     if (lane == 0 && sl.nchunk > 0) {
       const uint64_t pol = policy_evict_first();
+      // mode 2: the anchor row stays in L2 until phase 2 re-reads it
+      const uint64_t pol_q = policy_za();
       const char* base = reinterpret_cast<const char*>(P.logits);
       auto slice_ptr = [&](int64_t row) {
         const int64_t src_row = P.row_index ? P.row_index[row] : row;
@@ -1085,7 +1173,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
             asm volatile(
                 "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
                 " [%0], [%1], %2, [%3], %4;" ::"r"(it.addr(rb) + kHalf),
-                "l"(qsrc + off), "r"(bytes), "r"(it.full(rb)), "l"(pol)
+                "l"(qsrc + off), "r"(bytes), "r"(it.full(rb)), "l"(kA == 2 ? pol_q : pol)
                 : "memory");
           }
           it.next();
@@ -1108,27 +1196,52 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     double sd_a[2] = {0.0, 0.0};  // kA: anchor loss, Sigma KL(p || q)
     // the row's metadata and target logit are fetched one row ahead (after the
     // previous row's broadcast), so their dependent loads stay off the path
+    //
+    // The target logit is read from global memory only by the CTA whose slice
+    // holds it (and sent to the peers with the partials): with dlogits written
+    // in place, a peer's phase 2 may overwrite that column as soon as its own
+    // broadcast of the row went out, while the owner's phase 2 comes after its
+    // own broadcast, which needs this load.
     int seq_cur = (lane == 0 && cid < NR) ? seq_of_row(P, cid) : 0;
     RowMeta nxt;
     float nzy = kNegInf;
-    auto fetch = [&](int64_t r) {
+    // CTA rank whose column slice holds the target vector (-1: no valid target)
+    auto owner_of = [&](int y) {
+      if (y < 0 || y >= V) return -1;
+      const int vyv = y / EPV;
+      int own = 0;
+#pragma unroll
+      for (int q = 1; q < CL; ++q)
+        if (int((int64_t(q) * nvec) / CL) <= vyv) own = q;
+      return own;
+    };
+    auto fetch = [&](int64_t r, int parr) {
       nxt = row_meta(P, r, seq_cur);
       nzy = kNegInf;  // raw, unclamped target logit
-      if (nxt.y >= 0 && nxt.y < V) {
+      if (owner_of(nxt.y) == int(rank)) {
         const int64_t src_row = P.row_index ? P.row_index[r] : r;
         nzy = Vec<T>::load1(reinterpret_cast<const char*>(P.logits) + src_row * P.ld * ESZ, nxt.y);
+        if constexpr (CL > 1) {
+          const uint32_t za = smem_u32(&tail->zy[parr]), zb = smem_u32(&tail->pbar[parr]);
+#pragma unroll
+          for (int q = 0; q < CL; ++q)
+            if (q != int(rank)) st_async_f32(map_to_rank(za, q), nzy, map_to_rank(zb, q));
+        }
       }
     };
-    if (lane == 0 && cid < NR) fetch(cid);
+    if (lane == 0 && cid < NR) fetch(cid, 0);
     int64_t k = 0;
     for (int64_t row = cid; row < NR; row += ncl, ++k) {
       const int par = int(k & 1);
       const uint32_t parity = uint32_t((k >> 1) & 1);
       const RowMeta cur = nxt;
-      const float tzy = nzy;
+      float tzy = nzy;
+      int own = 0;
       if (lane == 0) {
+        own = owner_of(cur.y);
         if constexpr (CL > 1)
-          mbar_arrive_expect_tx(&tail->pbar[par], (CL - 1) * kConsumerWarps * (kA ? 20 : 16));
+          mbar_arrive_expect_tx(&tail->pbar[par], (CL - 1) * kConsumerWarps * (kA ? 20 : 16) +
+                                                      (own >= 0 && own != int(rank) ? 4 : 0));
       }
       {
         TG_PROF_T0();
@@ -1156,8 +1269,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       // (m, Sigma e, Sigma e z[, Sigma e (z - za)]) of the row; kA: the anchor's
       // log-sum-exp from the per-warp ones
       constexpr bool kRedux = TG_MERGE_REDUX && kA && NP > 32;
-      const float4 tot4 = kRedux ? merge_partials<NP, kA>(tail->wpart[par], lane)
-                                 : merge_partials_online<NP, kA>(tail->wpart[par], lane);
+      const float4 tot4 = kRedux ? merge_partials<NP, (kA != 0)>(tail->wpart[par], lane)
+                                 : merge_partials_online<NP, (kA != 0)>(tail->wpart[par], lane);
       const Online tot = {tot4.x, tot4.y, tot4.z};
       float lseq = 0.f;
       if constexpr (kA)
@@ -1167,10 +1280,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         // fast log / divide on the critical path; full precision when the row's
         // lp feeds sequence sums that couple the gradient (route 4) or the
         // anchor KL takes a difference of log-sum-exps, as in k_fwd / k_fwd_tma
-        const bool precise = kA || (P.flags & TG_FLAG_UNSCALED_GRAD) != 0;
+        const bool precise = kA != 0 || (P.flags & TG_FLAG_UNSCALED_GRAD) != 0;
         const float lse = tot.m + (precise ? logf(tot.s) : __logf(tot.s));
         const float H = lse - (precise ? tot.t / tot.s : __fdividef(tot.t, tot.s));
         const bool bad_target = (cur.flags & 2u) != 0;
+        if (CL > 1 && own >= 0 && own != int(rank)) tzy = tail->zy[par];
         const float lp = tzy - lse;
         RowTerms o;
         if (P.flags & TG_FLAG_UNSCALED_GRAD) {  // coupled, one pass: dz = p - e, scale later
@@ -1191,7 +1305,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         }
         tail->bcast[par] = make_float4(o.s + o.h * (H - lse) - a_anchor, o.h + ca, lse, o.s);
         arrive_u32(smem_u32(&tail->bbar[par]));
-        if (row + ncl < NR) fetch(row + ncl);
+        if (row + ncl < NR) fetch(row + ncl, par ^ 1);
 #ifdef TG_FUSED_PROF
         tail->prof[7] += (unsigned long long)(clock64() - t_crit);
         tail->prof[8] += (unsigned long long)(clock64() - t_xdone);
@@ -1248,8 +1362,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       dst[TG_S_ANCHOR_LOSS] = sd_a[0];
       dst[TG_S_SUM_ANCHOR_KL] = sd_a[1];
     }
-  } else if (kA && warp < kConsumerWarps) {
-    consumer_rows_a<T, CL>(P, tail, rb, sl, pre, cid, ncl, rank, warp, lane, tid);
+  } else if (kA != 0 && warp < kConsumerWarps) {
+    consumer_rows_a<T, CL, kA>(P, tail, rb, sl, pre, cid, ncl, rank, warp, lane, tid);
   } else if (warp < kConsumerWarps) {
     // ===================== consumer warps =====================
     RingIt pos0 = {0u};  // the current row's first chunk
@@ -1531,7 +1645,7 @@ cudaError_t launch_fwd_tma(const KParams& P, int n_sms, cudaStream_t stream) {
 
 size_t fused_smem_bytes(int n_slots) { return size_t(n_slots) * kChunk + sizeof(FusedSmemTail); }
 
-template <typename T, int CL, bool kA = false>
+template <typename T, int CL, int kA = 0>
 static cudaError_t launch_fused_t(const KParams& P, const RowMeta* meta, int n_ctas,
                                   int prefetch_rows, cudaStream_t stream) {
   const size_t smem = fused_smem_bytes(kSlots);
@@ -1557,20 +1671,30 @@ static cudaError_t launch_fused_t(const KParams& P, const RowMeta* meta, int n_c
   return cudaLaunchKernelEx(&cfg, k_fused_tma<T, CL, kA>, P, meta, prefetch_rows);
 }
 
-cudaError_t launch_fused(const KParams& P, const void* meta, int cl, int n_slots, int n_ctas,
-                         int prefetch_rows, cudaStream_t stream) {
+cudaError_t launch_fused(const KParams& P, const void* meta, int cl, int amode, int n_slots,
+                         int n_ctas, int prefetch_rows, cudaStream_t stream) {
   if (n_slots != kSlots) return cudaErrorInvalidValue;
   const RowMeta* m = reinterpret_cast<const RowMeta*>(meta);
   if (P.anchor && P.anchor_beta > 0.f) {  // fused anchor KL (fused_plan's anchor rules)
+    if (amode == 2) {  // z stashed, za re-read from L2
+      if (P.dtype == TG_DTYPE_BF16) {
+        if (cl == 1) return launch_fused_t<bf16_t, 1, 2>(P, m, n_ctas, prefetch_rows, stream);
+        if (cl == 2) return launch_fused_t<bf16_t, 2, 2>(P, m, n_ctas, prefetch_rows, stream);
+      } else {
+        if (cl == 2) return launch_fused_t<float, 2, 2>(P, m, n_ctas, prefetch_rows, stream);
+        if (cl == 4) return launch_fused_t<float, 4, 2>(P, m, n_ctas, prefetch_rows, stream);
+      }
+      return cudaErrorInvalidValue;
+    }
     if (P.dtype == TG_DTYPE_BF16) {
-      if (cl == 1) return launch_fused_t<bf16_t, 1, true>(P, m, n_ctas, prefetch_rows, stream);
-      if (cl == 2) return launch_fused_t<bf16_t, 2, true>(P, m, n_ctas, prefetch_rows, stream);
-      if (cl == 3) return launch_fused_t<bf16_t, 3, true>(P, m, n_ctas, prefetch_rows, stream);
-      if (cl == 4) return launch_fused_t<bf16_t, 4, true>(P, m, n_ctas, prefetch_rows, stream);
+      if (cl == 1) return launch_fused_t<bf16_t, 1, 1>(P, m, n_ctas, prefetch_rows, stream);
+      if (cl == 2) return launch_fused_t<bf16_t, 2, 1>(P, m, n_ctas, prefetch_rows, stream);
+      if (cl == 3) return launch_fused_t<bf16_t, 3, 1>(P, m, n_ctas, prefetch_rows, stream);
+      if (cl == 4) return launch_fused_t<bf16_t, 4, 1>(P, m, n_ctas, prefetch_rows, stream);
     } else {  // fp32 rows: the slices fit the stash up to V ~ 65 k (CL <= 4)
-      if (cl == 1) return launch_fused_t<float, 1, true>(P, m, n_ctas, prefetch_rows, stream);
-      if (cl == 2) return launch_fused_t<float, 2, true>(P, m, n_ctas, prefetch_rows, stream);
-      if (cl == 4) return launch_fused_t<float, 4, true>(P, m, n_ctas, prefetch_rows, stream);
+      if (cl == 1) return launch_fused_t<float, 1, 1>(P, m, n_ctas, prefetch_rows, stream);
+      if (cl == 2) return launch_fused_t<float, 2, 1>(P, m, n_ctas, prefetch_rows, stream);
+      if (cl == 4) return launch_fused_t<float, 4, 1>(P, m, n_ctas, prefetch_rows, stream);
     }
     return cudaErrorInvalidValue;
   }
@@ -1657,6 +1781,8 @@ int fused_max_slots() { return kSlots; }
 // chunks of a row slice (+ look-ahead) that can stay resident: the shared-memory
 // ring, or with the TMEM stash the per-warp TMEM ring
 int fused_resident_chunks() { return kStash ? kTSlots : kSlots; }
+// anchor mode 2 (z-only stash slots)
+int fused_resident_chunks_z() { return kStash ? kTSlotsZ : 0; }
 size_t rowmeta_bytes() { return sizeof(RowMeta); }
 
 }  // namespace tg

@@ -485,6 +485,80 @@ def lmhead_dlogits(hidden: torch.Tensor, weight: torch.Tensor, target: torch.Ten
     return out
 
 
+def _check_bf16_2d(name: str, t: torch.Tensor, dev: torch.device) -> None:
+    if t.dtype != torch.bfloat16 or t.dim() != 2 or t.stride(1) != 1 or t.device != dev:
+        raise ValueError(f"{name} must be a 2-D bf16 tensor with unit column stride on {dev}")
+
+
+def lmhead_grad_hidden(dz: torch.Tensor, weight: torch.Tensor, col0: int,
+                       out: torch.Tensor, accumulate: bool = True,
+                       stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """``out [T, d] fp32 (+)= dz [T, n] . weight[col0 : col0 + n]`` on the tensor
+    cores (``tg_lmhead_grad_hidden``): d hidden from one vocabulary chunk of
+    d loss / d logits."""
+    dev = dz.device
+    _check_bf16_2d("dz", dz, dev)
+    _check_bf16_2d("weight", weight, dev)
+    T, n = dz.shape
+    V, d = weight.shape
+    if out.dtype != torch.float32 or out.shape != (T, d) or out.stride(1) != 1:
+        raise ValueError(f"out must be a float32 [{T}, {d}] tensor with unit column stride")
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    with torch.cuda.device(dev):
+        N.check(N.lib().tg_lmhead_grad_hidden(
+            dz.data_ptr(), dz.stride(0), weight.data_ptr(), weight.stride(0), T, V, d, int(col0),
+            n, out.data_ptr(), out.stride(0), int(bool(accumulate)), s.cuda_stream))
+    return out
+
+
+def lmhead_grad_weight(dz: torch.Tensor, hidden: torch.Tensor, out: torch.Tensor,
+                       stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """``out [n, d] bf16 = dz [T, n]^T . hidden [T, d]`` on the tensor cores
+    (``tg_lmhead_grad_weight``): the rows of d W for one vocabulary chunk."""
+    dev = dz.device
+    _check_bf16_2d("dz", dz, dev)
+    _check_bf16_2d("hidden", hidden, dev)
+    T, n = dz.shape
+    d = hidden.shape[1]
+    if hidden.shape[0] != T:
+        raise ValueError("dz and hidden must have the same rows")
+    _check_bf16_2d("out", out, dev)
+    if out.shape != (n, d):
+        raise ValueError(f"out must be [{n}, {d}]")
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    with torch.cuda.device(dev):
+        N.check(N.lib().tg_lmhead_grad_weight(
+            dz.data_ptr(), dz.stride(0), hidden.data_ptr(), hidden.stride(0), T, d, n,
+            out.data_ptr(), out.stride(0), s.cuda_stream))
+    return out
+
+
+def lmhead_grad_chunk(dz: torch.Tensor, hidden: torch.Tensor, weight: torch.Tensor, col0: int,
+                      d_hidden: torch.Tensor, d_weight_rows: torch.Tensor,
+                      accumulate: bool = True,
+                      stream: Optional[torch.cuda.Stream] = None) -> None:
+    """Both gradient GEMMs of one vocabulary chunk in one tcgen05 launch
+    (``tg_lmhead_grad_chunk``): ``d_hidden (+)= dz . weight[col0 : col0 + n]``
+    (fp32) and ``d_weight_rows = dz^T . hidden`` (bf16 [n, d])."""
+    dev = dz.device
+    for name, t in (("dz", dz), ("hidden", hidden), ("weight", weight),
+                    ("d_weight_rows", d_weight_rows)):
+        _check_bf16_2d(name, t, dev)
+    T, n = dz.shape
+    V, d = weight.shape
+    if hidden.shape != (T, d) or d_weight_rows.shape != (n, d):
+        raise ValueError(f"hidden must be [{T}, {d}] and d_weight_rows [{n}, {d}]")
+    if d_hidden.dtype != torch.float32 or d_hidden.shape != (T, d) or d_hidden.stride(1) != 1:
+        raise ValueError(f"d_hidden must be a float32 [{T}, {d}] tensor with unit column stride")
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    with torch.cuda.device(dev):
+        N.check(N.lib().tg_lmhead_grad_chunk(
+            dz.data_ptr(), dz.stride(0), hidden.data_ptr(), hidden.stride(0), weight.data_ptr(),
+            weight.stride(0), T, V, d, int(col0), n, d_hidden.data_ptr(), d_hidden.stride(0),
+            int(bool(accumulate)), d_weight_rows.data_ptr(), d_weight_rows.stride(0),
+            s.cuda_stream))
+
+
 def lmhead_loss_fwd_bwd(hidden: torch.Tensor, weight: torch.Tensor, loss: "RFTLoss", target,
                         seq_lengths, group_sizes, reward, *, chunk_cols: int = 16384,
                         grad_weight: bool = True, **pack_kw):
@@ -495,9 +569,9 @@ def lmhead_loss_fwd_bwd(hidden: torch.Tensor, weight: torch.Tensor, loss: "RFTLo
     2. the loss epilogue on those rows (``TG_FLAG_ROWS_GIVEN``), which also
        returns the per-row gradient coefficients;
     3. per vocabulary chunk of ``chunk_cols`` columns: ``tg_lmhead_dlogits``
-       recomputes the chunk's logits and writes its bf16 d loss / d z, then two
-       plain GEMMs (cuBLAS through torch) accumulate d hidden += dz . W_chunk
-       (fp32) and write d W_chunk = dz^T . hidden.
+       recomputes the chunk's logits and writes its bf16 d loss / d z, then the
+       two tcgen05 GEMMs d hidden += dz . W_chunk (fp32) and d W_chunk = dz^T .
+       hidden in one launch (``tg_lmhead_grad_chunk``).
 
     Peak extra memory is T x chunk_cols bf16.  Returns ``(LossOutput,
     d_hidden [T, d] fp32, d_weight [V, d] bf16 or None)``."""
@@ -507,7 +581,7 @@ def lmhead_loss_fwd_bwd(hidden: torch.Tensor, weight: torch.Tensor, loss: "RFTLo
     T, d = hidden.shape
     V = int(weight.shape[0])
     dev = hidden.device
-    d_hidden = torch.zeros(T, d, dtype=torch.float32, device=dev)
+    d_hidden = torch.empty(T, d, dtype=torch.float32, device=dev)
     d_weight = torch.empty(V, d, dtype=torch.bfloat16, device=dev) if grad_weight else None
     if T == 0:
         if d_weight is not None:
@@ -520,10 +594,11 @@ def lmhead_loss_fwd_bwd(hidden: torch.Tensor, weight: torch.Tensor, loss: "RFTLo
     for c0 in range(0, V, chunk):
         nc = min(chunk, V - c0)
         dz = lmhead_dlogits(hidden, weight, tgt, out.lse, out.row_coef, c0, nc, out=buf[:, :nc])
-        w_c = weight[c0:c0 + nc]
-        d_hidden = torch.addmm(d_hidden, dz, w_c, out_dtype=torch.float32)
-        if d_weight is not None:
-            torch.mm(dz.t(), hidden, out=d_weight[c0:c0 + nc])
+        if d_weight is not None:  # both GEMMs in one launch
+            lmhead_grad_chunk(dz, hidden, weight, c0, d_hidden, d_weight[c0:c0 + nc],
+                              accumulate=c0 > 0)
+        else:
+            lmhead_grad_hidden(dz, weight, c0, d_hidden, accumulate=c0 > 0)
     return out, d_hidden, d_weight
 
 

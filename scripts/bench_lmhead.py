@@ -89,7 +89,19 @@ def main():
     nc = min(a.chunk, V)
     dzb = torch.empty(T, nc, dtype=torch.bfloat16, device="cuda")
     ms_dz = timed(lambda: lmhead_dlogits(h, w, fo.target, fo.lse, fo.row_coef, 0, nc, out=dzb))
-    del dzb
+    # the two backward GEMMs of one chunk: tcgen05 (tg_lmhead_grad_*) vs cuBLAS
+    from paper_2505_17826_b200 import lmhead_grad_hidden, lmhead_grad_weight
+    dzc = (torch.randn(T, nc, device="cuda") * 1e-3).to(torch.bfloat16)
+    dh_buf = torch.zeros(T, d, dtype=torch.float32, device="cuda")
+    dw_buf = torch.empty(nc, d, dtype=torch.bfloat16, device="cuda")
+    ms_gh = timed(lambda: lmhead_grad_hidden(dzc, w, 0, dh_buf, accumulate=True))
+    ms_gw = timed(lambda: lmhead_grad_weight(dzc, h, dw_buf))
+    from paper_2505_17826_b200 import lmhead_grad_chunk
+    ms_gc = timed(lambda: lmhead_grad_chunk(dzc, h, w, 0, dh_buf, dw_buf, accumulate=True))
+    ms_gh_cublas = timed(lambda: torch.addmm(dh_buf, dzc, w[:nc], out_dtype=torch.float32))
+    ms_gw_cublas = timed(lambda: torch.mm(dzc.t(), h, out=dw_buf))
+    gflop_c = 2.0 * T * nc * d / 1e9
+    del dzb, dzc
     lp_f, _, lse_f = lmhead_logprob_fwd(h, w, y)
     # train_unfused left dlogits in the logits buffer: recompute the logits first
     torch.matmul(h, w.T, out=logits)
@@ -115,7 +127,14 @@ def main():
            "train_step_chunked_ms": ms_train_chunked, "train_chunk_cols": a.chunk,
            "train_step_unfused_ms": ms_train_unfused,
            "dlogits_kernel_ms_per_chunk": ms_dz,
-           "dlogits_kernel_tflops": 2.0 * T * nc * d / ms_dz / 1e9}
+           "dlogits_kernel_tflops": 2.0 * T * nc * d / ms_dz / 1e9,
+           "grad_hidden_ms_per_chunk": ms_gh, "grad_hidden_tflops": gflop_c / ms_gh,
+           "grad_hidden_cublas_tflops": gflop_c / ms_gh_cublas,
+           "grad_weight_ms_per_chunk": ms_gw, "grad_weight_tflops": gflop_c / ms_gw,
+           "grad_weight_cublas_tflops": gflop_c / ms_gw_cublas,
+           "grad_chunk_one_launch_ms": ms_gc, "grad_chunk_tflops": 2 * gflop_c / ms_gc,
+           "grad_pair_cublas_ms": ms_gh_cublas + ms_gw_cublas,
+           "peak_note": "frac = vs the burst bf16 peak (an isolated kernel)"}
     print(json.dumps(out))
 
 

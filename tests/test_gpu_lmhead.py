@@ -260,3 +260,84 @@ def test_lmhead_random_shapes(seed):
                                 torch.arange(col0, col0 + n, device="cuda")).float()
     tol = 2.0 ** -8 * float(want.abs().max()) + 1e-2 * want.abs()
     assert bool(((got - want).abs() <= tol).all())
+
+
+# ---------------------------------------------------------------------------
+# the backward GEMMs on tcgen05 (tg_lmhead_grad_hidden / tg_lmhead_grad_weight)
+# against float64 torch products of the same bf16 operands.  The tensor cores
+# multiply bf16 exactly and accumulate in fp32: the bar is fp32 summation
+# noise, |a - b| <= 1e-5 (|A| |B|) + 1e-6 elementwise (plus bf16 rounding of
+# the d W output, 2^-8 |b|).
+
+
+def _gemm_operands(T, n, d, V, col0, seed):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    pitch = (n + 7) // 8 * 8 + 8  # dz as a column slice of a wider buffer
+    dz = torch.randn(T, pitch, device="cuda", generator=g).to(torch.bfloat16)[:, :n]
+    w = torch.randn(V, d, device="cuda", generator=g).to(torch.bfloat16)
+    h = torch.randn(T, d, device="cuda", generator=g).to(torch.bfloat16)
+    return dz, w, h
+
+
+@pytest.mark.parametrize("T,n,d,col0", [(128, 256, 256, 0), (300, 1000, 192, 100), (37, 72, 64, 5),
+                                        (1024, 4096, 1536, 2048), (129, 65, 3584, 7)])
+def test_grad_hidden_gemm_matches_float64(T, n, d, col0):
+    from paper_2505_17826_b200 import lmhead_grad_hidden
+    V = col0 + n + 3
+    dz, w, h = _gemm_operands(T, n, d, V, col0, seed=T + n + d)
+    wc = w[col0:col0 + n].double()
+    want = dz.double() @ wc
+    bound = dz.double().abs() @ wc.abs()
+    base = torch.full((T, d), 0.25, device="cuda")
+    got = lmhead_grad_hidden(dz, w, col0, base.clone(), accumulate=True).double()
+    assert bool(((got - 0.25 - want).abs() <= 1e-5 * bound + 1e-6).all())
+    got = lmhead_grad_hidden(dz, w, col0, base.clone(), accumulate=False).double()
+    assert bool(((got - want).abs() <= 1e-5 * bound + 1e-6).all())
+
+
+@pytest.mark.parametrize("T,n,d", [(128, 256, 256), (300, 1000, 192), (37, 72, 64), (2048, 4096, 1536),
+                                   (777, 130, 3584)])
+def test_grad_weight_gemm_matches_float64(T, n, d):
+    from paper_2505_17826_b200 import lmhead_grad_weight
+    dz, _, h = _gemm_operands(T, n, d, 1, 0, seed=7 * T + n)
+    want = dz.double().T @ h.double()
+    bound = dz.double().abs().T @ h.double().abs()
+    out = torch.full((n + 2, d), 7.0, device="cuda").to(torch.bfloat16)
+    got = lmhead_grad_weight(dz, h, out[1:n + 1]).double()
+    assert bool(((got - want).abs() <= 2.0 ** -8 * want.abs() + 1e-5 * bound + 1e-6).all())
+    assert bool((out[0] == 7.0).all() and (out[n + 1] == 7.0).all())  # rows outside untouched
+
+
+def test_grad_gemm_argument_errors():
+    from paper_2505_17826_b200 import lmhead_grad_hidden, lmhead_grad_weight
+    from paper_2505_17826_b200._native import NativeError
+    dz, w, h = _gemm_operands(64, 128, 64, 256, 0, seed=1)
+    with pytest.raises(NativeError):  # chunk past the vocabulary
+        lmhead_grad_hidden(dz, w, 200, torch.zeros(64, 64, device="cuda"))
+    with pytest.raises(ValueError):   # wrong output shape
+        lmhead_grad_hidden(dz, w, 0, torch.zeros(64, 32, device="cuda"))
+    with pytest.raises(ValueError):
+        lmhead_grad_weight(dz, h[:10], torch.empty(128, 64, dtype=torch.bfloat16, device="cuda"))
+    with pytest.raises(NativeError):  # d W row pitch must be a multiple of 8 elements
+        lmhead_grad_weight(dz, h, torch.empty(128, 68, dtype=torch.bfloat16, device="cuda")[:, :64])
+
+
+@pytest.mark.parametrize("T,n,d,col0", [(300, 1000, 192, 100), (1024, 4096, 1536, 2048),
+                                        (4096, 640, 256, 0), (37, 72, 64, 5)])
+def test_grad_chunk_one_launch_matches_float64(T, n, d, col0):
+    """tg_lmhead_grad_chunk: both GEMMs of a chunk on one tile queue (the job
+    with the longer K first) give the two single-GEMM results."""
+    from paper_2505_17826_b200 import lmhead_grad_chunk
+    V = col0 + n + 9
+    dz, w, h = _gemm_operands(T, n, d, V, col0, seed=3 * T + n)
+    wc = w[col0:col0 + n].double()
+    want_h = dz.double() @ wc
+    bound_h = dz.double().abs() @ wc.abs()
+    want_w = dz.double().T @ h.double()
+    bound_w = dz.double().abs().T @ h.double().abs()
+    dh = torch.full((T, d), -1.0, device="cuda")
+    dw = torch.empty(n, d, dtype=torch.bfloat16, device="cuda")
+    lmhead_grad_chunk(dz, h, w, col0, dh, dw, accumulate=True)
+    assert bool(((dh.double() + 1.0 - want_h).abs() <= 1e-5 * bound_h + 1e-6).all())
+    err_w = (dw.double() - want_w).abs()
+    assert bool((err_w <= 2.0 ** -8 * want_w.abs() + 1e-5 * bound_w + 1e-6).all())
