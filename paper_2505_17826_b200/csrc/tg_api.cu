@@ -68,6 +68,7 @@ int fused_max_clusters(int dtype, int cl);
 int fused_max_slots();
 int fused_resident_chunks();
 int fused_resident_chunks_z();
+int fused_anchor_half_bytes(int amode);
 size_t rowmeta_bytes();
 void launch_fwd(const KParams& P, bool anchor, bool vec, int grid, cudaStream_t st);
 cudaError_t launch_fwd_tma(const KParams& P, int n_sms, cudaStream_t stream);
@@ -365,7 +366,9 @@ FusedPlan fused_plan(const TgBatch* b, const TgOut* o, bool anchor = false) {
   // only serves rows mode 1 cannot hold (fp32 at Qwen vocabulary: 6V bytes
   // instead of the two-pass 10V).  TG_FUSED_ANCHOR_MODE forces one (A/B build).
   const int force_mode = anchor ? env_int("TG_FUSED_ANCHOR_MODE", 0) : 0;
-  for (int pass = 0; pass < (anchor ? 2 : 1); ++pass)
+  static const int kModeOrder[2] = {1, 2};
+  const int n_pass = anchor ? (force_mode ? 1 : 2) : 1;
+  for (int pass = 0; pass < n_pass; ++pass)
   for (int oi = 0; oi < 4; ++oi) {
     const int cl = kOrder[oi];
     if (force_cl ? cl != force_cl : cl == 3) continue;  // CL = 3 only on request
@@ -374,20 +377,19 @@ FusedPlan fused_plan(const TgBatch* b, const TgOut* o, bool anchor = false) {
     const int64_t nchunk = (slice_vec * 16 + fused_chunk_bytes() - 1) / fused_chunk_bytes();
     // resident TMEM chunks: the slice + >= 2 prefix chunks (anchor: a stash
     // slot holds a z + za half-chunk pair in mode 1, the z half chunk in mode 2)
-    const int64_t half = fused_chunk_bytes() / 2;
-    const int64_t nslot = anchor ? (slice_vec * 16 + half - 1) / half : nchunk;
-    // (a forced cluster size may run with a single slot of look-ahead)
-    const int64_t need = nslot + ((force_cl && anchor) ? 1 : 2);
     int amode = 0;
+    int64_t need = nchunk + 2;
     if (anchor) {
-      const int want = force_mode ? force_mode : pass + 1;
-      if (want == pass + 1) {
-        if (want == 1 && need <= fused_resident_chunks()) amode = 1;
-        if (want == 2 && need <= fused_resident_chunks_z() &&
-            (cl == 2 || (cl == 1 && b->dtype == TG_DTYPE_BF16) ||
-             (cl == 4 && b->dtype != TG_DTYPE_BF16)))  // instantiated
-          amode = 2;
-      }
+      const int want = force_mode ? force_mode : kModeOrder[pass];
+      const int64_t half = fused_anchor_half_bytes(want);
+      const int64_t nslot = (slice_vec * 16 + half - 1) / half;
+      // (a forced cluster size may run with a single slot of look-ahead)
+      need = nslot + (force_cl ? 1 : 2);
+      if (want == 1 && need <= fused_resident_chunks()) amode = 1;
+      if (want == 2 && need <= fused_resident_chunks_z() &&
+          (cl == 2 || (cl == 1 && b->dtype == TG_DTYPE_BF16) ||
+           (cl == 4 && b->dtype != TG_DTYPE_BF16)))  // instantiated
+        amode = 2;
     }
     if (anchor ? amode != 0 : need <= fused_resident_chunks()) {
       // persistent grid: as many clusters as can be co-resident, at most one per row

@@ -76,9 +76,11 @@ static_assert(kConsumerWarps <= 32, "one partial per epilogue lane");
 constexpr int kMaxPrefixChunks = 8;  // next-row phase-1 chunks run before this row's phase 2
 constexpr uint32_t kPrefetchPiece = 65536;  // bytes per L2 prefetch instruction
 
+constexpr int kMaxRingSlots = kSlots;
+
 struct FusedSmemTail {
-  uint64_t full[kSlots];
-  uint64_t empty[kSlots];
+  uint64_t full[kMaxRingSlots];
+  uint64_t empty[kMaxRingSlots];
   uint64_t pbar[2];   // consumers -> epilogue warp: per-warp partials written
   uint64_t bbar[2];   // epilogue warp -> consumers: (a, h, lse, s) written
   float4 wpart[2][4 * kConsumerWarps];  // [rank * warps + warp]: every CTA's partials
@@ -242,16 +244,18 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint4 (&u)[4]) {
 
 // Ring position as a running chunk counter: slot = c mod kSlots, mbarrier phase
 // parity = (c / kSlots) & 1 (compile-time divisor: a multiply-shift at most).
-struct RingIt {
+template <int NS, uint32_t CB>
+struct RingItT {
   uint32_t c;
-  __device__ __forceinline__ uint32_t slot() const { return c % uint32_t(kSlots); }
-  __device__ __forceinline__ uint32_t phase() const { return (c / kSlots) & 1u; }
-  __device__ __forceinline__ uint32_t addr(const RingBase& rb) const { return rb.ring + slot() * kChunk; }
+  __device__ __forceinline__ uint32_t slot() const { return c % uint32_t(NS); }
+  __device__ __forceinline__ uint32_t phase() const { return (c / uint32_t(NS)) & 1u; }
+  __device__ __forceinline__ uint32_t addr(const RingBase& rb) const { return rb.ring + slot() * CB; }
   __device__ __forceinline__ uint32_t full(const RingBase& rb) const { return rb.full + slot() * 8u; }
   __device__ __forceinline__ uint32_t empty(const RingBase& rb) const { return rb.empty + slot() * 8u; }
   __device__ __forceinline__ void next() { ++c; }
   __device__ __forceinline__ void advance(int n) { c += uint32_t(n); }
 };
+using RingIt = RingItT<kSlots, uint32_t(kChunk)>;
 
 __device__ __forceinline__ void prefetch_l2(const char* p, uint32_t bytes) {
   for (uint32_t off = 0; off < bytes; off += kPrefetchPiece) {
@@ -654,9 +658,28 @@ __device__ __forceinline__ float merge_lse(const float* lq, int lane) {
 // Phase 1 adds Sigma p (z - za) (aligned with z's reference max) and the
 // anchor's own online sum; the epilogue forms lse_q and KL(p || q); phase 2
 // writes dz = p (a + hz z - ca za) - s [v = y] (k_bwd's formula).
-constexpr int kVA = kVecPerThread / 2;           // z (and za) vectors per thread per slot
-constexpr int kVecPerChunkA = kConsumers * kVA;   // z vectors per slot
-constexpr uint32_t kHalf = uint32_t(kVecPerChunkA) * 16u;  // bytes of z (or za) per slot
+//
+// Slot geometry per anchor mode (kA):
+//   1: 32 KB ring slots (2 z + 2 za vectors per thread), one 16-column TMEM slot
+//      per ring slot (8 per warp);
+//   2: the same ring, z only in 8-column TMEM slots (16 per warp), za re-read
+//      from L2 in phase 2.
+// (Measured and dropped, profiles/r02_anchor_modes.txt: 16 KB ring slots with
+// z + za in 8-column TMEM slots -- 13 slots per 3-CTA slice leave 3 of look-
+// ahead -- ran 10-18 % slower than mode 1: the per-slot costs double.)
+constexpr int kVA = kVecPerThread / 2;  // modes 1 / 2: z (and za) vectors per thread per slot
+
+template <int M>
+struct AGeo {
+  static constexpr int VA = kVA;                           // z vectors per thread per slot
+  static constexpr int VPC = kConsumers * VA;              // z vectors per slot
+  static constexpr uint32_t HALF = uint32_t(VPC) * 16u;    // bytes of z (= of za) per slot
+  static constexpr int SLOTS = kSlots;
+  static constexpr uint32_t CHUNK = 2u * HALF;             // ring slot bytes
+  static constexpr int TSLOTS = (M == 1) ? kTSlots : kTSlotsZ;  // TMEM slots per warp
+  using It = RingItT<SLOTS, CHUNK>;
+};
+static_assert(AGeo<1>::CHUNK == uint32_t(kChunk), "a z + za slot is one ring slot");
 
 struct AccA {
   Acc1 z;         // (m, nm2, s2, t2, fresh) of the logits
@@ -702,8 +725,11 @@ __device__ __forceinline__ void accumulate_a(const uint4& uz, const uint4& uq, u
 }
 
 template <typename T, int kMode, bool kPartial, bool kMaskTail>
-__device__ __forceinline__ void phase1_chunk_a(AccA& acc, RingIt& it, const RingBase& rb,
-                                               int vbase, const Slice& sl, int tid) {
+__device__ __forceinline__ void phase1_chunk_a(AccA& acc, typename AGeo<kMode>::It& it,
+                                               const RingBase& rb, int vbase, const Slice& sl,
+                                               int tid) {
+  constexpr int kVA = AGeo<kMode>::VA;
+  constexpr uint32_t kHalf = AGeo<kMode>::HALF;
   uint4 u[2 * kVA];  // [0, kVA): z vectors, [kVA, 2 kVA): za vectors of the same columns
   bool valid[kVA];
   {
@@ -719,11 +745,10 @@ __device__ __forceinline__ void phase1_chunk_a(AccA& acc, RingIt& it, const Ring
     u[g] = valid[g] ? lds128(a + g * kConsumers * 16) : Pk<T>::neutral();
     u[kVA + g] = valid[g] ? lds128(a + kHalf + g * kConsumers * 16) : Pk<T>::neutral();
   }
-  static_assert(2 * kVA == 4, "one 16-column stash slot per z + za pair");
-  if constexpr (kMode == 2)  // z only: za is re-read from L2 in phase 2
+  if constexpr (kMode == 1)
+    tmem_st16(stash_addr(rb, it.c), u);  // z, z, za, za
+  else  // mode 2: z, z (za is re-read from L2 in phase 2)
     tmem_st8(stash_addr_z(rb, it.c), u[0], u[1]);
-  else
-    tmem_st16(stash_addr(rb, it.c), u);
   __syncwarp();
   if ((tid & 31) == 0) arrive_u32(it.empty(rb));
   it.next();
@@ -804,9 +829,11 @@ __device__ __forceinline__ void phase1_chunk_a(AccA& acc, RingIt& it, const Ring
 
 // logical chunks [c0, c1) of a row whose first ring position is `row_it`
 template <typename T, int kMode>
-__device__ __forceinline__ void phase1_range_a(AccA& acc, RingIt row_it, const RingBase& rb,
-                                               const Slice& sl, int c0, int c1, int tid) {
-  RingIt it = row_it;
+__device__ __forceinline__ void phase1_range_a(AccA& acc, typename AGeo<kMode>::It row_it,
+                                               const RingBase& rb, const Slice& sl, int c0,
+                                               int c1, int tid) {
+  constexpr int kVecPerChunkA = AGeo<kMode>::VPC;
+  typename AGeo<kMode>::It it = row_it;
   it.advance(c0);
   int vbase = sl.v0 + c0 * kVecPerChunkA;
   for (int c = c0; c < c1; ++c) {
@@ -844,11 +871,13 @@ __device__ __forceinline__ float4 warp_partial_a(const AccA& acc, float& lq) {
 // phase 2 of one logical chunk: z and za from the two stash slots
 // (mode 2: z from the stash, za = q[] re-read from L2 by the caller)
 template <typename T, int kMode, bool kCheck>
-__device__ __forceinline__ void phase2_chunk_a(const RingIt& it, const RingBase& rb, int vbase,
-                                               const Slice& sl, char* dzrow, int vy, int ye,
-                                               float s_t, uint64_t nl2, uint64_t av2,
-                                               uint64_t hz2, uint64_t nca2, int tid,
-                                               const uint4 (&q)[kVA]) {
+__device__ __forceinline__ void phase2_chunk_a(const typename AGeo<kMode>::It& it,
+                                               const RingBase& rb, int vbase, const Slice& sl,
+                                               char* dzrow, int vy, int ye, float s_t,
+                                               uint64_t nl2, uint64_t av2, uint64_t hz2,
+                                               uint64_t nca2, int tid,
+                                               const uint4 (&q)[AGeo<kMode>::VA]) {
+  constexpr int kVA = AGeo<kMode>::VA;
   constexpr int EPV = Vec<T>::N;
   char* dst = dzrow + int64_t(vbase + tid) * 16;
   uint4 su[2 * kVA];
@@ -895,7 +924,7 @@ __device__ __forceinline__ void phase2_chunk_a(const RingIt& it, const RingBase&
 }
 
 // mode 2: the za vectors of one chunk from L2 (neutral past the slice end)
-template <typename T>
+template <typename T, int kVA>
 __device__ __forceinline__ void load_za(uint4 (&q)[kVA], const char* qrow, int vbase,
                                         const Slice& sl, int tid, uint64_t pol) {
 #pragma unroll
@@ -906,19 +935,22 @@ __device__ __forceinline__ void load_za(uint4 (&q)[kVA], const char* qrow, int v
 }
 
 template <typename T, int kMode>
-__device__ __forceinline__ void phase2_row_a(const Slice& sl, RingIt it, const RingBase& rb,
-                                             const char* qrow, char* dzrow, int vy, int ye,
-                                             float s_t, uint64_t nl2, uint64_t av2, uint64_t hz2,
-                                             uint64_t nca2, int tid, uint64_t pol) {
+__device__ __forceinline__ void phase2_row_a(const Slice& sl, typename AGeo<kMode>::It it,
+                                             const RingBase& rb, const char* qrow, char* dzrow,
+                                             int vy, int ye, float s_t, uint64_t nl2,
+                                             uint64_t av2, uint64_t hz2, uint64_t nca2, int tid,
+                                             uint64_t pol) {
+  constexpr int kVA = AGeo<kMode>::VA;
+  constexpr int kVecPerChunkA = AGeo<kMode>::VPC;
   int vbase = sl.v0;
   uint4 q[kVA];
   // mode 2: the za loads run one chunk ahead of their use (L2 latency)
-  if constexpr (kMode == 2) load_za<T>(q, qrow, vbase, sl, tid, pol);
+  if constexpr (kMode == 2) load_za<T, kVA>(q, qrow, vbase, sl, tid, pol);
   for (int j = 0; j < sl.nchunk; ++j) {
     const int vend = vbase + kVecPerChunkA;
     uint4 qn[kVA];
     if constexpr (kMode == 2) {
-      if (j + 1 < sl.nchunk) load_za<T>(qn, qrow, vend, sl, tid, pol);
+      if (j + 1 < sl.nchunk) load_za<T, kVA>(qn, qrow, vend, sl, tid, pol);
     }
     const bool check = (vend > sl.v1) || (sl.tail_vec >= vbase && sl.tail_vec < vend) ||
                        (vy >= vbase && vy < vend);
@@ -979,7 +1011,7 @@ __device__ __forceinline__ void consumer_rows_a(const KParams& P, FusedSmemTail*
 #ifdef TG_FUSED_PROF
   const long long t_start = clock64();
 #endif
-  RingIt pos0 = {0u};
+  typename AGeo<kMode>::It pos0 = {0u};
   AccA acc = acc_init_a();
   const uint64_t pol_q = policy_evict_first();  // mode 2: the anchor row's last use
   int vtid = tid;
@@ -1016,7 +1048,7 @@ __device__ __forceinline__ void consumer_rows_a(const KParams& P, FusedSmemTail*
       }
       arrive_u32(smem_u32(&tail->pbar[par]));
     }
-    RingIt npos = pos0;
+    typename AGeo<kMode>::It npos = pos0;
     npos.advance(sl.nchunk);
     acc_new_row_a(acc);
     if (nrow < NR) phase1_range_a<T, kMode>(acc, npos, rb, sl, 0, pre, vtid);
@@ -1075,16 +1107,20 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   sl.v0 = int((int64_t(rank) * nvec) / CL);
   sl.v1 = int((int64_t(rank + 1) * nvec) / CL);
   const uint32_t slice_bytes = uint32_t(sl.v1 - sl.v0) * 16u;
-  sl.nchunk = int((slice_bytes + (kA ? kHalf : kChunk) - 1) / (kA ? kHalf : kChunk));
+  constexpr uint32_t kStep = kA ? AGeo<kA ? kA : 1>::HALF : uint32_t(kChunk);  // row bytes per slot
+  constexpr int kRing = kA ? AGeo<kA ? kA : 1>::SLOTS : kSlots;
+  using PIt = RingItT<kRing, kA ? AGeo<kA ? kA : 1>::CHUNK : uint32_t(kChunk)>;
+  sl.nchunk = int((slice_bytes + kStep - 1) / kStep);
   sl.tail_vec = (V % EPV) ? nvec - 1 : -1;  // global vector holding columns >= V
   sl.tail_valid = V - (nvec - 1) * EPV;
   // next-row phase-1 chunks that fit in the ring beside this row's slice
-  const int pre = min(
-      min(kMaxPrefixChunks, (kStash ? (kA == 2 ? kTSlotsZ : kTSlots) : kSlots) - sl.nchunk),
-      sl.nchunk);
+  const int pre = min(min(kMaxPrefixChunks,
+                          (kStash ? (kA ? AGeo<kA ? kA : 1>::TSLOTS : kTSlots) : kSlots) -
+                              sl.nchunk),
+                      sl.nchunk);
 
   if (tid == 0) {
-    for (int i = 0; i < kSlots; ++i) {
+    for (int i = 0; i < kRing; ++i) {
       mbar_init(&tail->full[i], 1);
       mbar_init(&tail->empty[i], kConsumerWarps);
     }
@@ -1141,7 +1177,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         const int64_t r = cid + int64_t(i) * ncl;
         if (r < NR) prefetch_l2(slice_ptr(r), slice_bytes);
       }
-      RingIt it = {0u};
+      PIt it = {0u};
       for (int64_t row = cid; row < NR; row += ncl) {
         if (prefetch_rows > 0) {
           const int64_t r = row + int64_t(prefetch_rows) * ncl;
@@ -1155,7 +1191,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
             TG_PROF_ADD(tail, 3);
           }
           // kA: a half chunk of z and the same columns of the anchor row in one slot
-          const uint32_t step = kA ? kHalf : uint32_t(kChunk);
+          const uint32_t step = kStep;
           const uint32_t off = uint32_t(j) * step;
           const uint32_t bytes = min(step, slice_bytes - off);
           asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
@@ -1172,7 +1208,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
                                row * P.ld_anchor * ESZ + int64_t(sl.v0) * 16;
             asm volatile(
                 "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-                " [%0], [%1], %2, [%3], %4;" ::"r"(it.addr(rb) + kHalf),
+                " [%0], [%1], %2, [%3], %4;" ::"r"(it.addr(rb) + kStep),
                 "l"(qsrc + off), "r"(bytes), "r"(it.full(rb)), "l"(kA == 2 ? pol_q : pol)
                 : "memory");
           }
@@ -1783,6 +1819,8 @@ int fused_max_slots() { return kSlots; }
 int fused_resident_chunks() { return kStash ? kTSlots : kSlots; }
 // anchor mode 2 (z-only stash slots)
 int fused_resident_chunks_z() { return kStash ? kTSlotsZ : 0; }
+// bytes of the row per ring slot in each anchor mode (z half of a z + za slot)
+int fused_anchor_half_bytes(int) { return int(AGeo<1>::HALF); }
 size_t rowmeta_bytes() { return sizeof(RowMeta); }
 
 }  // namespace tg
