@@ -78,7 +78,8 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
     LIBDIR.mkdir(parents=True, exist_ok=True)
     headers = list(CSRC.glob("*.cuh")) + [ROOT / "include" / "tg_loss.h"]
     objs = []
-    for src in CU_SOURCES + EXTRA_SOURCES.get(variant or "", []):
+    extra_src = EXTRA_SOURCES["ab"] if "-DTG_AB_SWITCHES" in defines else []
+    for src in CU_SOURCES + extra_src:
         obj = OBJDIR_ / (src + ".o")
         objs.append(obj)
         if force or _stale(obj, [CSRC / src, *headers]):

@@ -68,6 +68,7 @@ int fused_max_clusters(int dtype, int cl);
 int fused_max_slots();
 int fused_resident_chunks();
 int fused_resident_chunks_z();
+int fused_resident_chunks_split();
 int fused_anchor_half_bytes(int amode);
 size_t rowmeta_bytes();
 void launch_fwd(const KParams& P, bool anchor, bool vec, int grid, cudaStream_t st);
@@ -324,7 +325,9 @@ void fill_params(KParams& P, const TgBatch* b, const TgConfig* c, const TgOut* o
 // Fused-kernel plan: cluster size and ring slots, or cl = 0 if not eligible.
 struct FusedPlan {
   int cl = 0, n_slots = 0, n_ctas = 0, prefetch_rows = 1;
-  int amode = 0;  // anchor KL: 1 = z + za stashed, 2 = z stashed, za re-read from L2
+  // anchor KL: 1 = z + za stashed in TMEM, 2 = z stashed, za re-read from L2,
+  // 3 = z + za stashed in TMEM and shared-memory positions
+  int amode = 0;
 };
 
 // Tuning overrides for measurement, A/B build only (tg_common.cuh ab_env):
@@ -365,8 +368,13 @@ FusedPlan fused_plan(const TgBatch* b, const TgOut* o, bool anchor = false) {
   // CL = 2 vs 4 -- the L2 re-read stalls phase 2 and 7 % of it misses), so it
   // only serves rows mode 1 cannot hold (fp32 at Qwen vocabulary: 6V bytes
   // instead of the two-pass 10V).  TG_FUSED_ANCHOR_MODE forces one (A/B build).
+  //
+  // Mode 3 (split stash: 8 TMEM + 5 shared-memory z + za pair positions) holds
+  // a 2-CTA slice at V = 151,936 bf16, so those rows run on 2-CTA clusters over
+  // all 148 SMs instead of mode 1's 4-CTA clusters on 132.  Per cluster size
+  // the order is mode 1, mode 3 (pass 0), then mode 2 (pass 1).
   const int force_mode = anchor ? env_int("TG_FUSED_ANCHOR_MODE", 0) : 0;
-  static const int kModeOrder[2] = {1, 2};
+  static const int kModeOrder[2][2] = {{1, 3}, {2, 0}};
   const int n_pass = anchor ? (force_mode ? 1 : 2) : 1;
   for (int pass = 0; pass < n_pass; ++pass)
   for (int oi = 0; oi < 4; ++oi) {
@@ -376,20 +384,26 @@ FusedPlan fused_plan(const TgBatch* b, const TgOut* o, bool anchor = false) {
     const int64_t slice_vec = (nvec + cl - 1) / cl;
     const int64_t nchunk = (slice_vec * 16 + fused_chunk_bytes() - 1) / fused_chunk_bytes();
     // resident TMEM chunks: the slice + >= 2 prefix chunks (anchor: a stash
-    // slot holds a z + za half-chunk pair in mode 1, the z half chunk in mode 2)
+    // slot holds a z + za half-chunk pair in modes 1 / 3, the z half chunk in mode 2)
     int amode = 0;
     int64_t need = nchunk + 2;
     if (anchor) {
-      const int want = force_mode ? force_mode : kModeOrder[pass];
-      const int64_t half = fused_anchor_half_bytes(want);
+      const int64_t half = fused_anchor_half_bytes(1);
       const int64_t nslot = (slice_vec * 16 + half - 1) / half;
       // (a forced cluster size may run with a single slot of look-ahead)
       need = nslot + (force_cl ? 1 : 2);
-      if (want == 1 && need <= fused_resident_chunks()) amode = 1;
-      if (want == 2 && need <= fused_resident_chunks_z() &&
-          (cl == 2 || (cl == 1 && b->dtype == TG_DTYPE_BF16) ||
-           (cl == 4 && b->dtype != TG_DTYPE_BF16)))  // instantiated
-        amode = 2;
+      for (int mi = 0; mi < 2 && amode == 0; ++mi) {
+        const int want = force_mode ? (mi == 0 ? force_mode : 0) : kModeOrder[pass][mi];
+        if (want == 1 && need <= fused_resident_chunks()) amode = 1;
+        if (want == 2 && need <= fused_resident_chunks_z() &&
+            (cl == 2 || (cl == 1 && b->dtype == TG_DTYPE_BF16) ||
+             (cl == 4 && b->dtype != TG_DTYPE_BF16)))  // instantiated
+          amode = 2;
+        if (want == 3 && need <= fused_resident_chunks_split() &&
+            ((cl == 2 && b->dtype == TG_DTYPE_BF16) ||
+             (cl == 4 && b->dtype != TG_DTYPE_BF16)))  // instantiated
+          amode = 3;
+      }
     }
     if (anchor ? amode != 0 : need <= fused_resident_chunks()) {
       // persistent grid: as many clusters as can be co-resident, at most one per row
@@ -398,6 +412,9 @@ FusedPlan fused_plan(const TgBatch* b, const TgOut* o, bool anchor = false) {
       const int64_t clusters = b->n_rows < clusters_max ? b->n_rows : clusters_max;
       fp.cl = cl;
       fp.amode = amode;
+      // mode 3: L2 look-ahead of the stash positions behind the landing slots
+      // (kernel argument bits 16..31)
+      if (amode == 3) fp.prefetch_rows |= env_int("TG_PREFETCH_CHUNKS", 6) << 16;
       fp.n_slots = n_slots;
       fp.n_ctas = int(clusters * cl);
       return fp;

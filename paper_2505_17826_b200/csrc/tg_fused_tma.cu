@@ -44,6 +44,7 @@
 #include "tg_vecmath.cuh"
 
 #include <mutex>
+#include <type_traits>
 
 namespace tg {
 
@@ -92,8 +93,9 @@ struct FusedSmemTail {
 #ifdef TG_FUSED_PROF
   unsigned long long prof[16];
   unsigned long long post_first[2], post_last[2];
-  uint32_t post_t[2][kConsumerWarps];  // low 32 bits of clock64 (differences within a row)
 #endif
+  uint64_t tfull[8];   // anchor mode 3: TMEM position filled (tcgen05.cp complete)
+  uint64_t tempty[8];  // anchor mode 3: TMEM position read by phase 2 (every consumer warp)
 };
 
 // the ring + tail must fit the 227 KB per-CTA opt-in shared memory of sm_100
@@ -112,8 +114,8 @@ static_assert(size_t(kSlots) * kChunk + sizeof(FusedSmemTail) <= 232448,
 // prof[8] epilogue: cluster exchange complete -> broadcast
 // prof[9] first local warp partial posted -> epilogue wakes (all partials in)
 // prof[10] first -> last local warp partial posted (intra-CTA skew)
-// prof[11..14] post lag behind the first local post, summed over the consumer
-//              warps of SM sub-partition 0..3 (warp % 4)
+// prof[11] / [12] anchor mode 3: consumer data waits on TMEM / shared positions
+// prof[13] / [14] anchor mode 3 copier: waits for a free TMEM position / landed data
 // prof[15] phase-1 chunks that took the checked path (counted per warp)
 #ifdef TG_FUSED_PROF
 __device__ unsigned long long g_fused_prof[1024][16];
@@ -155,6 +157,7 @@ __device__ __forceinline__ void arrive_u32(uint32_t bar) {
 struct RingBase {
   uint32_t ring, full, empty;  // shared addresses of slot 0's data / full / empty barrier
   uint32_t tmem;               // TMEM stash of this thread (lane, warp's column block), or 0
+  uint32_t tfull;              // anchor mode 3: tfull[0] (tempty[0] follows 64 bytes later)
 };
 
 // ---- TMEM stash of the row slice (TG_TMEM_STASH) ------------------------------
@@ -186,6 +189,24 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint4 (&u)[4]) {
       "r"(u[1].w), "r"(u[2].x), "r"(u[2].y), "r"(u[2].z), "r"(u[2].w), "r"(u[3].x), "r"(u[3].y),
       "r"(u[3].z), "r"(u[3].w)
       : "memory");
+}
+
+// tcgen05.cp of a [128 rows x 16 B] shared-memory matrix (rows 16 B apart: the
+// no-swizzle canonical layout, 8-row core matrices 128 B apart = SBO) into 4
+// TMEM columns of lanes 0..127 (row i -> lane i)
+__device__ __forceinline__ void tmem_cp_128x128b(uint32_t taddr, uint32_t saddr) {
+  uint64_t d = uint64_t((saddr >> 4) & 0x3FFFu);
+  d |= uint64_t(128u >> 4) << 16;  // leading byte offset (one core matrix wide: unused)
+  d |= uint64_t(128u >> 4) << 32;  // stride byte offset: next 8 rows
+  d |= uint64_t(1u) << 46;         // descriptor version (sm_100); layout 0 = no swizzle
+  asm volatile("tcgen05.cp.cta_group::1.128x128b [%0], %1;" ::"r"(taddr), "l"(d) : "memory");
+}
+
+// arrive on a CTA mbarrier once this thread's prior tcgen05 operations completed
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
 }
 
 // anchor mode 2: a z-only stash slot (2 vectors = 8 columns per thread), 16 per warp
@@ -667,7 +688,74 @@ __device__ __forceinline__ float merge_lse(const float* lq, int lane) {
 // (Measured and dropped, profiles/r02_anchor_modes.txt: 16 KB ring slots with
 // z + za in 8-column TMEM slots -- 13 slots per 3-CTA slice leave 3 of look-
 // ahead -- ran 10-18 % slower than mode 1: the per-slot costs double.)
-constexpr int kVA = kVecPerThread / 2;  // modes 1 / 2: z (and za) vectors per thread per slot
+//   3: split stash -- the row slices are larger than TMEM (a 2-CTA slice at
+//      V = 151,936 bf16 is 10 z + za pairs = 304 KB), so the stash is a ring of
+//      kTSlots + kSSlots positions: positions 0..7 of every period are TMEM
+//      slots (the pair lands in one of kLSlots shared-memory landing slots and
+//      phase 1 copies it to TMEM, as in mode 1), positions 8.. are shared-memory
+//      stash slots (the pair lands there and stays until phase 2 has read it
+//      again).  TMEM 256 KB + 5 x 32 KB shared = 13 pairs resident: a 10-pair
+//      slice + 3 of look-ahead, on all 148 SMs (2-CTA clusters) instead of the
+//      132 that 4-CTA clusters of mode 1 occupy.
+constexpr int kVA = kVecPerThread / 2;  // z (and za) vectors per thread per slot
+
+#ifndef TG_ANCHOR_SSLOTS
+#define TG_ANCHOR_SSLOTS 5
+#endif
+constexpr int kSSlots = TG_ANCHOR_SSLOTS;   // mode 3: shared-memory stash slots
+// Mode 3, TMEM positions: by default the consumers copy each landed pair into
+// TMEM in phase 1 (lds + tcgen05.st, as mode 1) and free the landing slot; the
+// producer keeps the pairs behind the landing slots in L2 (bulk prefetch a few
+// positions ahead, TG_PREFETCH_CHUNKS).  TG_SPLIT_UTCCP=1 (A/B build variant):
+// a copier lane moves each landed pair into TMEM with tcgen05.cp (4 column
+// blocks x 4 vectors of 128 lanes x 16 B) once the TMEM position is free and
+// frees the landing slot on the copy's commit -- parity-green, but 4.90 vs
+// 5.21 TB/s (profiles/r02_anchor_split.txt): the copier shares the producer
+// warp's issue with the two TMA lanes, and the consumers then wait on the
+// copies (18 % of the span on TMEM positions).
+#ifndef TG_SPLIT_UTCCP
+#define TG_SPLIT_UTCCP 0
+#endif
+constexpr bool kSplitCp = TG_SPLIT_UTCCP != 0;
+constexpr int kLSlots = kSlots - kSSlots;   // mode 3: landing slots of the TMEM positions
+static_assert(kSSlots >= 1 && kLSlots >= 1, "mode 3 needs stash and landing slots");
+static_assert(kTSlots == 8, "FusedSmemTail::tfull / tempty hold one barrier per TMEM position");
+
+// Mode-3 stash position as a running counter c (same protocol as RingItT):
+// period kP = kTSlots + kSSlots; pos = c mod kP.  TMEM position (pos < kTSlots):
+// landing slot = (t mod kLSlots), t = the running count of TMEM positions, its
+// mbarrier phase (t / kLSlots) & 1; shared stash position: slot kLSlots + pos -
+// kTSlots, phase (c / kP) & 1.  Buffer / barrier index = the slot.
+template <uint32_t CB>
+struct SplitItT {
+  static constexpr uint32_t kP = uint32_t(kTSlots + kSSlots);
+  uint32_t c;
+  __device__ __forceinline__ uint32_t pos() const { return c % kP; }
+  __device__ __forceinline__ bool in_tmem() const { return pos() < uint32_t(kTSlots); }
+  __device__ __forceinline__ uint32_t tcount() const {
+    return (c / kP) * uint32_t(kTSlots) + pos();
+  }
+  __device__ __forceinline__ uint32_t slot() const {
+    return in_tmem() ? tcount() % uint32_t(kLSlots) : uint32_t(kLSlots) + pos() - uint32_t(kTSlots);
+  }
+  __device__ __forceinline__ uint32_t phase() const {
+    return (in_tmem() ? tcount() / uint32_t(kLSlots) : c / kP) & 1u;
+  }
+  __device__ __forceinline__ uint32_t addr(const RingBase& rb) const { return rb.ring + slot() * CB; }
+  __device__ __forceinline__ uint32_t full(const RingBase& rb) const { return rb.full + slot() * 8u; }
+  __device__ __forceinline__ uint32_t empty(const RingBase& rb) const { return rb.empty + slot() * 8u; }
+  __device__ __forceinline__ uint32_t tmem(const RingBase& rb) const {
+    return rb.tmem + pos() * uint32_t(kTCols);
+  }
+  // TMEM position barriers (tcgen05.cp landing) and their phase
+  __device__ __forceinline__ uint32_t tfull(const RingBase& rb) const { return rb.tfull + pos() * 8u; }
+  __device__ __forceinline__ uint32_t tempty(const RingBase& rb) const {
+    return rb.tfull + 64u + pos() * 8u;
+  }
+  __device__ __forceinline__ uint32_t tphase() const { return (c / kP) & 1u; }
+  __device__ __forceinline__ void next() { ++c; }
+  __device__ __forceinline__ void advance(int n) { c += uint32_t(n); }
+};
 
 template <int M>
 struct AGeo {
@@ -676,8 +764,9 @@ struct AGeo {
   static constexpr uint32_t HALF = uint32_t(VPC) * 16u;    // bytes of z (= of za) per slot
   static constexpr int SLOTS = kSlots;
   static constexpr uint32_t CHUNK = 2u * HALF;             // ring slot bytes
-  static constexpr int TSLOTS = (M == 1) ? kTSlots : kTSlotsZ;  // TMEM slots per warp
-  using It = RingItT<SLOTS, CHUNK>;
+  // resident positions per warp (the stash ring's period)
+  static constexpr int TSLOTS = (M == 1) ? kTSlots : (M == 2) ? kTSlotsZ : kTSlots + kSSlots;
+  using It = typename std::conditional<M == 3, SplitItT<CHUNK>, RingItT<SLOTS, CHUNK>>::type;
 };
 static_assert(AGeo<1>::CHUNK == uint32_t(kChunk), "a z + za slot is one ring slot");
 
@@ -732,25 +821,61 @@ __device__ __forceinline__ void phase1_chunk_a(AccA& acc, typename AGeo<kMode>::
   constexpr uint32_t kHalf = AGeo<kMode>::HALF;
   uint4 u[2 * kVA];  // [0, kVA): z vectors, [kVA, 2 kVA): za vectors of the same columns
   bool valid[kVA];
-  {
+  // mode 3 with the copier: a TMEM position's pair is read from TMEM once the
+  // tcgen05.cp into it completed
+  bool from_tmem = false;
+  if constexpr (kMode == 3 && kSplitCp) {
+    from_tmem = it.in_tmem();
+    TG_PROF_T0();
+    if (from_tmem)
+      wait_full(it.tfull(rb), it.tphase());
+    else
+      wait_full(it.full(rb), it.phase());
+    TG_PROF_ADD(prof_tail(), 0);
+#ifdef TG_FUSED_PROF
+    if ((threadIdx.x & 31) == 0)
+      atomicAdd(&prof_tail()->prof[from_tmem ? 11 : 12], (unsigned long long)(clock64() - _tp0));
+#endif
+  } else {
     TG_PROF_T0();
     wait_full(it.full(rb), it.phase());
     TG_PROF_ADD(prof_tail(), 0);
   }
-  const uint32_t a = it.addr(rb) + tid * 16;
+  if (from_tmem) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if constexpr (kMode == 3) tmem_ld16(it.tmem(rb), u);
 #pragma unroll
-  for (int g = 0; g < kVA; ++g) {
-    const int vec = vbase + g * kConsumers + tid;
-    valid[g] = !kPartial || vec < sl.v1;
-    u[g] = valid[g] ? lds128(a + g * kConsumers * 16) : Pk<T>::neutral();
-    u[kVA + g] = valid[g] ? lds128(a + kHalf + g * kConsumers * 16) : Pk<T>::neutral();
+    for (int g = 0; g < kVA; ++g) {
+      valid[g] = !kPartial || vbase + g * kConsumers + tid < sl.v1;
+      if (!valid[g]) {
+        u[g] = Pk<T>::neutral();
+        u[kVA + g] = Pk<T>::neutral();
+      }
+    }
+  } else {
+    const uint32_t a = it.addr(rb) + tid * 16;
+#pragma unroll
+    for (int g = 0; g < kVA; ++g) {
+      const int vec = vbase + g * kConsumers + tid;
+      valid[g] = !kPartial || vec < sl.v1;
+      u[g] = valid[g] ? lds128(a + g * kConsumers * 16) : Pk<T>::neutral();
+      u[kVA + g] = valid[g] ? lds128(a + kHalf + g * kConsumers * 16) : Pk<T>::neutral();
+    }
   }
-  if constexpr (kMode == 1)
-    tmem_st16(stash_addr(rb, it.c), u);  // z, z, za, za
-  else  // mode 2: z, z (za is re-read from L2 in phase 2)
-    tmem_st8(stash_addr_z(rb, it.c), u[0], u[1]);
-  __syncwarp();
-  if ((tid & 31) == 0) arrive_u32(it.empty(rb));
+  if constexpr (kMode == 3) {  // TMEM position: copy out, free the landing slot;
+    if (!kSplitCp && it.in_tmem()) {  // shared stash position: kept until phase 2
+      tmem_st16(it.tmem(rb), u);
+      __syncwarp();
+      if ((tid & 31) == 0) arrive_u32(it.empty(rb));
+    }
+  } else {
+    if constexpr (kMode == 1)
+      tmem_st16(stash_addr(rb, it.c), u);  // z, z, za, za
+    else  // mode 2: z, z (za is re-read from L2 in phase 2)
+      tmem_st8(stash_addr_z(rb, it.c), u[0], u[1]);
+    __syncwarp();
+    if ((tid & 31) == 0) arrive_u32(it.empty(rb));
+  }
   it.next();
   if constexpr (kMaskTail) {
 #pragma unroll
@@ -885,6 +1010,17 @@ __device__ __forceinline__ void phase2_chunk_a(const typename AGeo<kMode>::It& i
     tmem_ld8(stash_addr_z(rb, it.c), su[0], su[1]);
 #pragma unroll
     for (int g = 0; g < kVA; ++g) su[kVA + g] = q[g];
+  } else if constexpr (kMode == 3) {
+    if (it.in_tmem()) {
+      tmem_ld16(it.tmem(rb), su);
+    } else {  // the pair is still in its shared-memory stash slot
+      const uint32_t a = it.addr(rb) + tid * 16;
+#pragma unroll
+      for (int g = 0; g < kVA; ++g) {
+        su[g] = lds128(a + g * kConsumers * 16);
+        su[kVA + g] = lds128(a + AGeo<kMode>::HALF + g * kConsumers * 16);
+      }
+    }
   } else {
     tmem_ld16(stash_addr(rb, it.c), su);
   }
@@ -919,6 +1055,16 @@ __device__ __forceinline__ void phase2_chunk_a(const typename AGeo<kMode>::It& i
         }
       }
       if (!done) st_stream(dst + g * kConsumers * 16, Vec<T>::pack(d));
+    }
+  }
+  if constexpr (kMode == 3) {  // a shared stash slot is free once every warp read it
+    if (!it.in_tmem()) {
+      __syncwarp();
+      if ((tid & 31) == 0) arrive_u32(it.empty(rb));
+    } else if constexpr (kSplitCp) {  // the TMEM position, for the copier
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if ((tid & 31) == 0) arrive_u32(it.tempty(rb));
     }
   }
 }
@@ -1015,7 +1161,9 @@ __device__ __forceinline__ void consumer_rows_a(const KParams& P, FusedSmemTail*
   AccA acc = acc_init_a();
   const uint64_t pol_q = policy_evict_first();  // mode 2: the anchor row's last use
   int vtid = tid;
-  if constexpr (kConsumerWarps == 16) {  // sub-partitions 2 / 3 first (see the default path)
+  // (mode 3 with the copier: identity -- a TMEM column block's 128 lanes are
+  // the 128 consecutive threads whose vectors one tcgen05.cp.128x128b moves)
+  if constexpr (kConsumerWarps == 16 && !(kMode == 3 && kSplitCp)) {  // sub-partitions 2 / 3 first
     const int q = warp & 3, grp = warp >> 2;
     const int vw = (q >= 2) ? (grp * 2 + (q - 2)) : (8 + grp * 2 + q);
     vtid = vw * 32 + lane;
@@ -1080,7 +1228,11 @@ __device__ __forceinline__ void consumer_rows_a(const KParams& P, FusedSmemTail*
 
 template <typename T, int CL, int kA = 0>
 __global__ void __launch_bounds__(kFusedThreads, 1)
-    k_fused_tma(const KParams P, const RowMeta* __restrict__ meta, int prefetch_rows) {
+    k_fused_tma(const KParams P, const RowMeta* __restrict__ meta, int prefetch) {
+  // prefetch: bits 0..15 L2 look-ahead in rows (bulk prefetch of whole row
+  // slices), bits 16..31 (anchor mode 3) L2 look-ahead in stash positions
+  const int prefetch_rows = prefetch & 0xFFFF;
+  const uint32_t pf_chunks = uint32_t(prefetch) >> 16;
   // kA: 0 no anchor; 1 anchor KL with z and za in the TMEM stash; 2 anchor KL
   // with z in the stash and za re-read from L2 in phase 2 (twice the stash
   // columns per slot: Qwen-vocabulary rows fit 2-CTA clusters, all 148 SMs)
@@ -1091,7 +1243,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* ring = smem;
   FusedSmemTail* tail = reinterpret_cast<FusedSmemTail*>(smem + size_t(kSlots) * kChunk);
-  const RingBase rb0 = {smem_u32(ring), smem_u32(&tail->full[0]), smem_u32(&tail->empty[0]), 0u};
+  const RingBase rb0 = {smem_u32(ring), smem_u32(&tail->full[0]), smem_u32(&tail->empty[0]), 0u,
+                       smem_u32(&tail->tfull[0])};
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -1109,7 +1262,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   const uint32_t slice_bytes = uint32_t(sl.v1 - sl.v0) * 16u;
   constexpr uint32_t kStep = kA ? AGeo<kA ? kA : 1>::HALF : uint32_t(kChunk);  // row bytes per slot
   constexpr int kRing = kA ? AGeo<kA ? kA : 1>::SLOTS : kSlots;
-  using PIt = RingItT<kRing, kA ? AGeo<kA ? kA : 1>::CHUNK : uint32_t(kChunk)>;
+  using PIt = typename std::conditional<(kA == 3), typename AGeo<3>::It,
+                                        RingItT<kRing, kA ? AGeo<kA ? kA : 1>::CHUNK
+                                                          : uint32_t(kChunk)>>::type;
   sl.nchunk = int((slice_bytes + kStep - 1) / kStep);
   sl.tail_vec = (V % EPV) ? nvec - 1 : -1;  // global vector holding columns >= V
   sl.tail_valid = V - (nvec - 1) * EPV;
@@ -1120,9 +1275,17 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
                       sl.nchunk);
 
   if (tid == 0) {
+    // mode 3 with the copier: a landing slot is freed by the copy's commit
+    constexpr bool kCp = kA == 3 && kSplitCp;
     for (int i = 0; i < kRing; ++i) {
       mbar_init(&tail->full[i], 1);
-      mbar_init(&tail->empty[i], kConsumerWarps);
+      mbar_init(&tail->empty[i], (kCp && i < kLSlots) ? 1 : kConsumerWarps);
+    }
+    if constexpr (kCp) {
+      for (int i = 0; i < kTSlots; ++i) {
+        mbar_init(&tail->tfull[i], 1);
+        mbar_init(&tail->tempty[i], kConsumerWarps);
+      }
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tail->pbar[i], kConsumerWarps + (CL > 1 ? 1 : 0));  // + epilogue expect_tx
@@ -1164,7 +1327,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
 
   if (warp == kProducerWarp) {
     // ===================== producer warp: bulk TMA into the ring =====================
-    if (lane == 0 && sl.nchunk > 0) {
+    // mode 3: lane 0 issues the TMEM positions (landing slots), lane 1 the
+    // shared stash positions -- two in-order issuers, so a stash slot still
+    // held by phase 2 does not hold up the landing slots' read-ahead
+    if (lane < (kA == 3 ? 2 : 1) && sl.nchunk > 0) {
       const uint64_t pol = policy_evict_first();
       // mode 2: the anchor row stays in L2 until phase 2 re-reads it
       const uint64_t pol_q = policy_za();
@@ -1173,18 +1339,40 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         const int64_t src_row = P.row_index ? P.row_index[row] : row;
         return base + src_row * P.ld * ESZ + int64_t(sl.v0) * 16;
       };
-      for (int i = 0; i < prefetch_rows; ++i) {
+      for (int i = 0; i < prefetch_rows && lane == 0; ++i) {
         const int64_t r = cid + int64_t(i) * ncl;
         if (r < NR) prefetch_l2(slice_ptr(r), slice_bytes);
       }
       PIt it = {0u};
+      uint32_t pc = 0;  // mode 3: next position to prefetch into L2
       for (int64_t row = cid; row < NR; row += ncl) {
-        if (prefetch_rows > 0) {
+        if (prefetch_rows > 0 && lane == 0) {
           const int64_t r = row + int64_t(prefetch_rows) * ncl;
           if (r < NR) prefetch_l2(slice_ptr(r), slice_bytes);
         }
         const char* src = slice_ptr(row);
         for (int j = 0; j < sl.nchunk; ++j) {
+          if constexpr (kA == 3) {
+            // L2 look-ahead by positions: the landing slots hold only a few
+            // pairs, so the pairs behind them are pulled into L2 early and
+            // their TMA loads then see L2 latency
+            if (lane == 0 && pf_chunks > 0) {
+              for (; pc < it.c + pf_chunks; ++pc) {
+                const int64_t prow = cid + int64_t(pc / uint32_t(sl.nchunk)) * ncl;
+                if (prow >= NR) break;
+                const uint32_t poff = (pc % uint32_t(sl.nchunk)) * kStep;
+                const uint32_t pb = min(kStep, slice_bytes - poff);
+                prefetch_l2(slice_ptr(prow) + poff, pb);
+                prefetch_l2(reinterpret_cast<const char*>(P.anchor) + prow * P.ld_anchor * ESZ +
+                                int64_t(sl.v0) * 16 + poff,
+                            pb);
+              }
+            }
+            if (it.in_tmem() != (lane == 0)) {  // the other issuer's position
+              it.next();
+              continue;
+            }
+          }
           {
             TG_PROF_T0();
             mbar_wait_u32<TG_SLEEP_PROD>(it.empty(rb), it.phase() ^ 1u);
@@ -1213,6 +1401,46 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
                 : "memory");
           }
           it.next();
+        }
+      }
+    }
+    if constexpr (kA == 3 && kSplitCp) {
+      // ---- copier lane (mode 3): landed TMEM-position pairs -> TMEM (tcgen05.cp) ----
+      if (lane == 2 && sl.nchunk > 0) {
+        PIt it = {0u};
+        const uint32_t tb = tail->tmem_base;  // lane 0, column 0 of the CTA's 512 columns
+        for (int64_t row = cid; row < NR; row += ncl) {
+          for (int j = 0; j < sl.nchunk; ++j) {
+            if (it.in_tmem()) {
+#ifdef TG_FUSED_PROF
+              const long long c0 = clock64();
+#endif
+              mbar_wait_u32<TG_SLEEP_PROD>(it.tempty(rb), it.tphase() ^ 1u);
+#ifdef TG_FUSED_PROF
+              const long long c1 = clock64();
+#endif
+              mbar_wait_u32<0>(it.full(rb), it.phase());
+#ifdef TG_FUSED_PROF
+              tail->prof[13] += (unsigned long long)(c1 - c0);
+              tail->prof[14] += (unsigned long long)(clock64() - c1);
+#endif
+              asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+              const uint32_t src = it.addr(rb);
+              const uint32_t dst = tb + it.pos() * uint32_t(kTCols);
+              // column block cb = warps 4 cb .. 4 cb + 3 = threads 128 cb .. + 127;
+              // vector v of every thread: z g = 0 / 1, za g = 0 / 1
+#pragma unroll
+              for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+                for (int v = 0; v < 4; ++v)
+                  tmem_cp_128x128b(dst + uint32_t(cb) * 128u + uint32_t(v) * 4u,
+                                   src + (v >= 2 ? kStep : 0u) + uint32_t(v & 1) * kConsumers * 16u +
+                                       uint32_t(cb) * 128u * 16u);
+              tc_commit(it.tfull(rb));  // the consumers may read the position
+              tc_commit(it.empty(rb));  // the landing slot may be refilled
+            }
+            it.next();
+          }
         }
       }
     }
@@ -1293,8 +1521,6 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       if (lane == 0) {
         tail->prof[9] += (unsigned long long)t_crit - tail->post_first[par];
         tail->prof[10] += tail->post_last[par] - tail->post_first[par];
-        for (int w = 0; w < kConsumerWarps; ++w)
-          tail->prof[11 + (w & 3)] += uint32_t(tail->post_t[par][w] - uint32_t(tail->post_first[par]));
         tail->post_first[par] = ~0ull;
         tail->post_last[par] = 0ull;
       }
@@ -1445,7 +1671,6 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         const unsigned long long tpost = clock64();
         atomicMin(&tail->post_first[par], tpost);
         atomicMax(&tail->post_last[par], tpost);
-        tail->post_t[par][warp] = uint32_t(tpost);
 #endif
         tail->wpart[par][slot] = make_float4(o.m, o.s, o.t, 0.f);
         if constexpr (CL > 1) {
@@ -1712,6 +1937,13 @@ cudaError_t launch_fused(const KParams& P, const void* meta, int cl, int amode, 
   if (n_slots != kSlots) return cudaErrorInvalidValue;
   const RowMeta* m = reinterpret_cast<const RowMeta*>(meta);
   if (P.anchor && P.anchor_beta > 0.f) {  // fused anchor KL (fused_plan's anchor rules)
+    if (amode == 3) {  // split stash: TMEM + shared-memory positions
+      if (P.dtype == TG_DTYPE_BF16 && cl == 2)
+        return launch_fused_t<bf16_t, 2, 3>(P, m, n_ctas, prefetch_rows, stream);
+      if (P.dtype != TG_DTYPE_BF16 && cl == 4)
+        return launch_fused_t<float, 4, 3>(P, m, n_ctas, prefetch_rows, stream);
+      return cudaErrorInvalidValue;
+    }
     if (amode == 2) {  // z stashed, za re-read from L2
       if (P.dtype == TG_DTYPE_BF16) {
         if (cl == 1) return launch_fused_t<bf16_t, 1, 2>(P, m, n_ctas, prefetch_rows, stream);
@@ -1819,6 +2051,8 @@ int fused_max_slots() { return kSlots; }
 int fused_resident_chunks() { return kStash ? kTSlots : kSlots; }
 // anchor mode 2 (z-only stash slots)
 int fused_resident_chunks_z() { return kStash ? kTSlotsZ : 0; }
+// anchor mode 3 (TMEM + shared-memory stash positions)
+int fused_resident_chunks_split() { return kStash ? kTSlots + kSSlots : 0; }
 // bytes of the row per ring slot in each anchor mode (z half of a z + za slot)
 int fused_anchor_half_bytes(int) { return int(AGeo<1>::HALF); }
 size_t rowmeta_bytes() { return sizeof(RowMeta); }

@@ -25,5 +25,7 @@ for f in sys.argv[1:]:
           f"{(a[:, 7] / rows).mean():.0f} cyc; first local partial -> epilogue wake "
           f"{(a[:, 9] / rows).mean():.0f} cyc, intra-CTA post skew {(a[:, 10] / rows).mean():.0f} cyc")
     print(f"  checked-path phase-1 chunks per row per warp: {(a[:, 15] / rows / NCW).mean():.3f}")
-    lag = [(a[:, 11 + q] / rows / (NCW / 4)).mean() for q in range(4)]
-    print("  mean post lag by SM sub-partition (warp % 4): " + ", ".join(f"{x:.0f}" for x in lag))
+    if a[:, 11:15].sum() > 0:  # anchor mode 3 (split stash)
+        w = [100 * (a[:, 11 + q] / (NCW if q < 2 else 1) / span).mean() for q in range(4)]
+        print(f"  mode 3: consumer data wait on TMEM positions {w[0]:.2f} %, on shared positions "
+              f"{w[1]:.2f} %; copier waits: free TMEM position {w[2]:.2f} %, landed data {w[3]:.2f} %")

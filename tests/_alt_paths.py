@@ -30,6 +30,32 @@ def fused():
             compare(out, O.general_loss(batch, oracle_cfg(cfg)), torch.bfloat16)
 
 
+def anchor():
+    """The fused anchor KL's other stash modes at Qwen vocabulary (the default
+    there is mode 3, the split stash): TG_FUSED_ANCHOR_MODE=1 (z + za in TMEM,
+    4-CTA clusters) or 2 (z in TMEM, za re-read from L2, 2-CTA clusters)."""
+    import os
+
+    from _cases import make_case, oracle_cfg
+    from test_gpu_parity import compare
+
+    from oracle import rft_oracle as O
+    from paper_2505_17826_b200 import RFTLoss, RFTLossConfig
+
+    cfg = RFTLossConfig.from_variant("OPMD_SIMPLE", tau=0.4, beta=0.9)
+    mode = os.environ["TG_FUSED_ANCHOR_MODE"]
+    # mode 1 holds a bf16 row in 4-CTA slices only (fp32 rows do not fit it);
+    # mode 2: bf16 on 2-CTA, fp32 on 4-CTA clusters
+    cases = {"1": [(torch.bfloat16, 4)], "2": [(torch.bfloat16, 2), (torch.float32, 4)]}[mode]
+    for dtype, want_cl in cases:
+        lens = [24] * 8 if dtype == torch.bfloat16 else [12] * 4
+        batch, packed = make_case(6, 151936, lens, [len(lens) // 2] * 2, dtype=dtype,
+                                  anchor=True)
+        loss = RFTLoss(cfg)
+        assert loss.route(packed) == 1 and loss.cluster_size(packed) == want_cl
+        compare(loss(packed, dlogits="new"), O.general_loss(batch, oracle_cfg(cfg)), dtype)
+
+
 def lmhead():
     from paper_2505_17826_b200 import lmhead_logprob_fwd
 
@@ -50,5 +76,5 @@ def lmhead():
 
 
 if __name__ == "__main__":
-    {"fused": fused, "lmhead": lmhead}[sys.argv[1]]()
+    {"fused": fused, "lmhead": lmhead, "anchor": anchor}[sys.argv[1]]()
     print("ok")

@@ -180,8 +180,8 @@ def test_fused_anchor_kl_route_matches_oracle(shape, case_kw):
 @pytest.mark.parametrize("shape,route", [("v1000", 1), ("v32000", 1), ("v151936", 1)])
 def test_fp32_anchor_kl_routes_match_oracle(shape, route):
     """fp32 rows take the fused anchor path: both slices in the TMEM stash
-    (V up to ~65 k), or z stashed and the anchor row re-read from L2 (Qwen
-    vocabulary, 4-CTA clusters); against the oracle."""
+    (V up to ~65 k), or the split TMEM + shared-memory stash (Qwen vocabulary,
+    4-CTA clusters); against the oracle."""
     V, lens, gs = SHAPES[shape]
     cfg = RFTLossConfig.from_variant("OPMD_SIMPLE", tau=0.4, beta=0.9)
     batch, packed = make_case(7, V, lens, gs, dtype=torch.float32, anchor=True)
@@ -193,8 +193,8 @@ def test_fp32_anchor_kl_routes_match_oracle(shape, route):
 @pytest.mark.parametrize("shape", ["v32000", "v151936"])
 def test_fused_anchor_kl_with_masked_vocabulary_matches_two_pass(shape):
     """-inf logits (masked vocabulary, in both the policy and the anchor rows)
-    take the fused anchor path's checked branch (V = 151,936: the L2 re-read
-    of the anchor row clamps them in phase 2); the oracle cannot evaluate
+    take the fused anchor path's checked branch (V = 151,936: the split
+    stash, phase 2 clamps them from TMEM and shared-memory positions); the oracle cannot evaluate
     KL(p || q) there (inf - inf), so the two-pass route -- which clamps -inf
     the same way -- is the reference."""
     V, lens, gs = SHAPES[shape]

@@ -120,14 +120,16 @@ def test_fp32_cluster_instantiations_every_element(V, cl):
 ANCHOR = RFTLossConfig.from_variant("OPMD_SIMPLE", tau=0.4, beta=0.9)
 
 
-@pytest.mark.parametrize("dtype,cl", [(torch.bfloat16, 4), (torch.float32, 4)])
+@pytest.mark.parametrize("dtype,cl", [(torch.bfloat16, 2), (torch.float32, 4)])
 def test_anchor_instantiations_every_element(dtype, cl):
     """regularizer_g fused at Qwen vocabulary, every element against the
-    oracle, plus the anchor statistics: bf16 runs k_fused_tma<bf16, 4, kA = 1>
-    (z and za in the TMEM stash), fp32 k_fused_tma<float, 4, kA = 2> (z in the
-    stash, the anchor row re-read from L2 in phase 2)."""
-    lens = LENS if dtype == torch.bfloat16 else [23, 17, 29, 11]
-    groups = GROUPS if dtype == torch.bfloat16 else [2, 2]
+    oracle, plus the anchor statistics: bf16 runs k_fused_tma<bf16, 2, kA = 3>
+    and fp32 k_fused_tma<float, 4, kA = 3> (split stash: 8 TMEM + 5 shared-
+    memory z + za positions per 13-position period, 10-position row slices, so
+    with several rows per cluster every alignment of a row on the period and
+    both slot kinds' mbarrier phases are exercised)."""
+    lens = LENS if dtype == torch.bfloat16 else [23, 17, 29, 11, 31, 19, 27, 13]
+    groups = GROUPS
     batch, packed = make_case(105, V_QWEN, lens, groups, dtype=dtype, anchor=True)
     loss = RFTLoss(ANCHOR)
     assert loss.route(packed) == 1 and loss.cluster_size(packed) == cl
@@ -180,7 +182,7 @@ FD_CASES = {
                                               loss_agg_mode="seq-sum")),
     "bf16_cl2_opmd_simple": (V_QWEN, torch.bfloat16, 2,
                              RFTLossConfig.from_variant("OPMD_SIMPLE", tau=0.5)),
-    "bf16_cl4_anchor": (V_QWEN, torch.bfloat16, 4, ANCHOR),
+    "bf16_cl2_anchor_split_stash": (V_QWEN, torch.bfloat16, 2, ANCHOR),
     "f32_cl2_ppo_k3_entropy": (65536, torch.float32, 2,
                                RFTLossConfig(advantage_fn="rloo", policy_loss_fn="ppo_clip",
                                              kl_fn="low_var_kl", kl_coef=0.05,
