@@ -717,6 +717,14 @@ constexpr int kSSlots = TG_ANCHOR_SSLOTS;   // mode 3: shared-memory stash slots
 #define TG_SPLIT_UTCCP 0
 #endif
 constexpr bool kSplitCp = TG_SPLIT_UTCCP != 0;
+// Sanitizer study (-DTG_ARRIVE_ALL): every consumer thread arrives on the mode-3
+// slot barriers, and every epilogue lane on the broadcast barrier, instead of
+// one lane per warp after __syncwarp / the warp's shuffles -- racecheck does not
+// follow that release chain (profiles/r02_sanitizer.txt)
+#ifndef TG_ARRIVE_ALL
+#define TG_ARRIVE_ALL 0
+#endif
+constexpr bool kArriveAll = TG_ARRIVE_ALL != 0;
 constexpr int kLSlots = kSlots - kSSlots;   // mode 3: landing slots of the TMEM positions
 static_assert(kSSlots >= 1 && kLSlots >= 1, "mode 3 needs stash and landing slots");
 static_assert(kTSlots == 8, "FusedSmemTail::tfull / tempty hold one barrier per TMEM position");
@@ -866,7 +874,7 @@ __device__ __forceinline__ void phase1_chunk_a(AccA& acc, typename AGeo<kMode>::
     if (!kSplitCp && it.in_tmem()) {  // shared stash position: kept until phase 2
       tmem_st16(it.tmem(rb), u);
       __syncwarp();
-      if ((tid & 31) == 0) arrive_u32(it.empty(rb));
+      if (kArriveAll || (tid & 31) == 0) arrive_u32(it.empty(rb));
     }
   } else {
     if constexpr (kMode == 1)
@@ -1060,7 +1068,7 @@ __device__ __forceinline__ void phase2_chunk_a(const typename AGeo<kMode>::It& i
   if constexpr (kMode == 3) {  // a shared stash slot is free once every warp read it
     if (!it.in_tmem()) {
       __syncwarp();
-      if ((tid & 31) == 0) arrive_u32(it.empty(rb));
+      if (kArriveAll || (tid & 31) == 0) arrive_u32(it.empty(rb));
     } else if constexpr (kSplitCp) {  // the TMEM position, for the copier
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -1279,7 +1287,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     constexpr bool kCp = kA == 3 && kSplitCp;
     for (int i = 0; i < kRing; ++i) {
       mbar_init(&tail->full[i], 1);
-      mbar_init(&tail->empty[i], (kCp && i < kLSlots) ? 1 : kConsumerWarps);
+      mbar_init(&tail->empty[i], (kCp && i < kLSlots) ? 1
+                                 : (kA == 3 && kArriveAll) ? kConsumers : kConsumerWarps);
     }
     if constexpr (kCp) {
       for (int i = 0; i < kTSlots; ++i) {
@@ -1289,7 +1298,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tail->pbar[i], kConsumerWarps + (CL > 1 ? 1 : 0));  // + epilogue expect_tx
-      mbar_init(&tail->bbar[i], 1);
+      mbar_init(&tail->bbar[i], kArriveAll ? 32 : 1);
     }
     fence_mbar_init();
 #ifdef TG_FUSED_PROF
@@ -1538,6 +1547,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       if constexpr (kA)
         lseq = kRedux ? merge_lse<NP>(tail->wpart_q[par], lane)
                       : merge_lse_online<NP>(tail->wpart_q[par], lane);
+      // sanitizer build: every lane that read the partials releases them
+      if (kArriveAll && lane != 0) arrive_u32(smem_u32(&tail->bbar[par]));
       if (lane == 0) {
         // fast log / divide on the critical path; full precision when the row's
         // lp feeds sequence sums that couple the gradient (route 4) or the

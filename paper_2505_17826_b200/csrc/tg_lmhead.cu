@@ -547,20 +547,21 @@ __global__ void k_lmhead_merge(const LmParams P) {
   }
 }
 
-// Forward: single CTAs by default -- A/B on B200 (profiles/r01_lmhead_ab.txt):
-// pairs +1 % at d = 1536, -6 % at d = 3584 over the full vocabulary.  Backward
-// (dz) chunks: 2-CTA pairs by default -- +9 % at d = 1536 and 3584
-// (profiles/r01_lmhead_bwd.txt): the dz staging writes and TMA-store reads
-// compete with the UMMA operand reads for shared-memory bandwidth, and pairs
-// halve the W-tile bytes each SM stages and reads.  TG_LMHEAD_PAIR=0/1 forces
-// one mode for both.
+// 2-CTA pairs by default, forward and backward (dz) chunks: each SM stages and
+// reads half of the W tile, and ncu shows the single-CTA forward with its
+// tensor-memory operand path 92-94 % busy (profiles/r02_lmhead_fwd_ab.txt).
+// Round-2 A/B, 16,384 rows (same box): forward 1,620 vs 1,558 TFLOP/s at
+// d = 1536 (split-major), 1,412 vs 1,376 at d = 3584 (row-block-major); round 1
+// measured the dz chunks +9 % (profiles/r01_lmhead_bwd.txt).  TG_LMHEAD_PAIR=0/1
+// forces one mode for both (A/B build).
 static bool lm_pair_mode(bool dz = false) {
+  (void)dz;
   static int mode = -2;
   if (mode == -2) {
     const int v = ab_env("TG_LMHEAD_PAIR", -1);  // A/B build only
     mode = v < 0 ? -1 : (v != 0);
   }
-  return mode < 0 ? dz : mode != 0;
+  return mode != 0;
 }
 
 // Work-unit order.  Split-major when the CTAs resident at once (one 128-row X

@@ -47,13 +47,21 @@ def loss_paths():
                 loss(pack_arrays(z.clone(), y, lens, groups, rew, old_lp=old, ref_lp=old),
                      dlogits="new", unscaled=True).metrics()
         logprob_fwd(pack_arrays(z, y, lens, groups, rew))
-    # anchor KL (regularizer_g)
-    V = 4096
-    z = torch.randn(6, V, device="cuda").to(torch.bfloat16)
-    q = torch.randn(6, V, device="cuda").to(torch.bfloat16)
-    loss = RFTLoss(RFTLossConfig(policy_loss_fn="opmd_simple", anchor_beta=0.1))
-    loss(pack_arrays(z, rng.integers(0, V, 6), [3, 3], [2], np.array([0., 1.], np.float32),
-                     anchor_logits=q), dlogits="new").metrics()
+
+
+def anchor_paths():
+    rng = np.random.default_rng(1)
+    # anchor KL (regularizer_g): mode 1 (V = 4096) and the split stash (mode 3:
+    # bf16 2-CTA and fp32 4-CTA clusters at V = 151,936; enough rows per cluster
+    # for the 13-position period to wrap)
+    for V, dtype, T in ((4096, torch.bfloat16, 6), (151936, torch.bfloat16, 300),
+                        (151936, torch.float32, 140)):
+        z = torch.randn(T, V, device="cuda").to(dtype)
+        q = torch.randn(T, V, device="cuda").to(dtype)
+        loss = RFTLoss(RFTLossConfig(policy_loss_fn="opmd_simple", anchor_beta=0.1))
+        lens = [T // 2, T - T // 2]
+        loss(pack_arrays(z, rng.integers(0, V, T), lens, [2], np.array([0., 1.], np.float32),
+                         anchor_logits=q), dlogits="new").metrics()
 
 
 def lmhead_paths():
@@ -77,6 +85,8 @@ if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "all"
     if which in ("all", "loss"):
         loss_paths()
+    if which in ("all", "loss", "anchor"):
+        anchor_paths()
     if which in ("all", "lmhead"):
         lmhead_paths()
     torch.cuda.synchronize()

@@ -1,6 +1,6 @@
 """Run in a subprocess by test_gpu_alt_paths.py: the environment selects an
 alternative kernel (TG_FUSED_IMPL=2: the L2-reread fused kernel;
-TG_LMHEAD_PAIR=1: the 2-CTA LM-head kernel), read once per process.  Exits
+TG_LMHEAD_PAIR=0: the single-CTA LM-head kernel), read once per process.  Exits
 non-zero on a parity failure."""
 
 import sys

@@ -1,7 +1,7 @@
 """The environment-selected alternative kernels (kept for A/B in the A/B build
 libtg_loss_ab.so, never in the product library) stay parity-green: the
-L2-reread fused loss kernel (TG_FUSED_IMPL=2) against the oracle, the 2-CTA
-LM-head kernel (TG_LMHEAD_PAIR=1) against torch fp32, the anchor KL's
+L2-reread fused loss kernel (TG_FUSED_IMPL=2) against the oracle, the single-CTA
+LM-head kernel (TG_LMHEAD_PAIR=0) against torch fp32, the anchor KL's
 stash modes 1 / 2 (TG_FUSED_ANCHOR_MODE) against the oracle.  Each runs in a
 subprocess because the selection is read once per process."""
 
@@ -23,7 +23,7 @@ AB_LIB = HERE.parent / "paper_2505_17826_b200" / "_lib" / "libtg_loss_ab.so"
 
 
 @pytest.mark.parametrize("what,env", [("fused", {"TG_FUSED_IMPL": "2"}),
-                                      ("lmhead", {"TG_LMHEAD_PAIR": "1"}),
+                                      ("lmhead", {"TG_LMHEAD_PAIR": "0"}),
                                       ("anchor", {"TG_FUSED_ANCHOR_MODE": "1"}),
                                       ("anchor", {"TG_FUSED_ANCHOR_MODE": "2"})])
 def test_alternative_kernel_parity(what, env):

@@ -217,9 +217,9 @@ def test_lmhead_dlogits_matches_formula(T, V, d, col0, n_cols):
                     reason="already pinned to one CTA mode by the environment")
 @pytest.mark.parametrize("pair", ["0", "1"])
 def test_lmhead_backward_in_both_cta_modes(pair):
-    """The backward chunk kernel runs as 2-CTA pairs by default and as single
-    CTAs with TG_LMHEAD_PAIR=0 (the forward the other way round); the mode is
-    read once per process, so each runs the parity tests in a subprocess."""
+    """Both LM-head kernels (forward and backward chunks) run as 2-CTA pairs by
+    default and as single CTAs with TG_LMHEAD_PAIR=0; the mode is read once
+    per process, so each runs the parity tests in a subprocess."""
     import os
     import subprocess
     import sys
