@@ -36,12 +36,18 @@ constexpr int G_BM = 128;
 constexpr int G_BN = 256;
 constexpr int G_BK = 64;
 constexpr int G_UK = 16;
-constexpr int G_STAGES = 4;
 constexpr int G_A_BYTES = G_BM * G_BK * 2;  // 16 KB
-constexpr int G_B_BYTES = G_BN * G_BK * 2;  // 32 KB
-constexpr int G_STAGE = G_A_BYTES + G_B_BYTES;
 constexpr int G_THREADS = 256;
 constexpr int G_BOX = 64 * 64 * 2;          // one MN-major box [64 K][64 MN]: 8 KB
+constexpr int G_MAX_STAGES = 6;
+// kPair = false: one CTA per 128 x 256 tile (cta_group::1), 4 stages of 48 KB.
+// kPair = true : a 2-CTA cluster per 256 x 256 tile (cta_group::2, M 256): each
+//   CTA stages its own 128 A rows and half of the B tile (128 N), so a stage is
+//   32 KB and 6 fit -- per SM the B bytes staged and read halve.
+template <bool kPair> constexpr int g_b_rows() { return kPair ? G_BN / 2 : G_BN; }
+template <bool kPair> constexpr int g_stage() { return G_A_BYTES + g_b_rows<kPair>() * G_BK * 2; }
+template <bool kPair> constexpr int g_stages() { return kPair ? 6 : 4; }
+template <bool kPair> constexpr int g_tile_m() { return kPair ? 2 * G_BM : G_BM; }
 
 // One GEMM of a launch: D [M, N] (+)= A . B, operand majors, output type.
 struct GemmJob {
@@ -63,14 +69,17 @@ struct GemmParams {
 };
 
 struct GemmSmemTail {
-  uint64_t full[G_STAGES];
-  uint64_t empty[G_STAGES];
+  uint64_t full[G_MAX_STAGES];
+  uint64_t empty[G_MAX_STAGES];
   uint64_t tfull[2];
   uint64_t tempty[2];
   uint32_t tmem_base;
 };
 
-size_t gemm_smem_bytes() { return size_t(G_STAGES) * G_STAGE + sizeof(GemmSmemTail) + 1024; }
+template <bool kPair>
+size_t gemm_smem_bytes() {
+  return size_t(g_stages<kPair>()) * g_stage<kPair>() + sizeof(GemmSmemTail) + 1024;
+}
 
 // tile t of the queue -> (job, m0, n0)
 struct TileRef {
@@ -78,60 +87,82 @@ struct TileRef {
   int64_t m0, n0;
 };
 
-__device__ __forceinline__ TileRef tile_of(const GemmParams& P, int t) {
+// (m0: the tile's first row; a pair's CTA rank r owns rows m0 + 128 r ..)
+template <int BM>
+__host__ __device__ __forceinline__ TileRef tile_of(const GemmParams& P, int t) {
   const GemmJob& J0 = P.job[0];
   const int nn0 = int((J0.N + G_BN - 1) / G_BN);
-  const int t0 = int((J0.M + G_BM - 1) / G_BM) * nn0;
+  const int t0 = int((J0.M + BM - 1) / BM) * nn0;
   TileRef r;
   if (t < t0) {
     r.j = 0;
-    r.m0 = int64_t(t / nn0) * G_BM;
+    r.m0 = int64_t(t / nn0) * BM;
     r.n0 = int64_t(t % nn0) * G_BN;
   } else {
     const int u = t - t0;
     const int nn1 = int((P.job[1].N + G_BN - 1) / G_BN);
     r.j = 1;
-    r.m0 = int64_t(u / nn1) * G_BM;
+    r.m0 = int64_t(u / nn1) * BM;
     r.n0 = int64_t(u % nn1) * G_BN;
   }
   return r;
 }
 
-__device__ __forceinline__ int n_tiles_of(const GemmJob& J) {
-  return int(((J.M + G_BM - 1) / G_BM) * ((J.N + G_BN - 1) / G_BN));
+template <int BM>
+__host__ __device__ __forceinline__ int n_tiles_of(const GemmJob& J) {
+  return int(((J.M + BM - 1) / BM) * ((J.N + G_BN - 1) / G_BN));
 }
 
+template <bool kPair>
 __global__ void __launch_bounds__(G_THREADS, 1)
     k_gemm_bf16(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
                 const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
                 const GemmParams P) {
+  constexpr int STAGE = g_stage<kPair>();
+  constexpr int NST = g_stages<kPair>();
+  constexpr int BM = g_tile_m<kPair>();       // output rows per tile (both CTAs of a pair)
+  constexpr int B_ROWS = g_b_rows<kPair>();   // B (N) columns staged per CTA
   extern __shared__ __align__(1024) unsigned char g_smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(g_smem_raw) + 1023) & ~uintptr_t(1023));
-  GemmSmemTail* tail = reinterpret_cast<GemmSmemTail*>(smem + size_t(G_STAGES) * G_STAGE);
+  GemmSmemTail* tail = reinterpret_cast<GemmSmemTail*>(smem + size_t(NST) * STAGE);
   const uint32_t ring = smem_u32(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_tiles = n_tiles_of(P.job[0]) + (P.n_jobs > 1 ? n_tiles_of(P.job[1]) : 0);
+  const uint32_t rank = kPair ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  const int tile0 = kPair ? int(cluster_id_x()) : int(blockIdx.x);
+  const int tile_stride = kPair ? int(n_clusters_x()) : int(gridDim.x);
+  const int n_tiles = n_tiles_of<BM>(P.job[0]) + (P.n_jobs > 1 ? n_tiles_of<BM>(P.job[1]) : 0);
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < G_STAGES; ++i) {
+    for (int i = 0; i < NST; ++i) {
       mbar_init(&tail->full[i], 1);
       mbar_init(&tail->empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tail->tfull[i], 1);
-      mbar_init(&tail->tempty[i], 4);
+      mbar_init(&tail->tempty[i], kPair ? 8 : 4);  // epilogue warps of the pair / of the CTA
     }
     fence_mbar_init();
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                     smem_u32(&tail->tmem_base))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (kPair) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       smem_u32(&tail->tmem_base))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       smem_u32(&tail->tmem_base))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair)
+    cluster_sync_all();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tail->tmem_base;
 
@@ -145,32 +176,46 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB1)) : "memory");
       }
       uint32_t stage = 0, phase = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const TileRef tr = tile_of(P, t);
+      for (int t = tile0; t < n_tiles; t += tile_stride) {
+        const TileRef tr = tile_of<BM>(P, t);
         const GemmJob J = tr.j ? P.job[1] : P.job[0];
         const CUtensorMap* mA = tr.j ? &tmA1 : &tmA0;
         const CUtensorMap* mB = tr.j ? &tmB1 : &tmB0;
-        const int m0 = int(tr.m0), n0 = int(tr.n0);
+        // this CTA's A rows and B columns of the tile
+        const int m0 = int(tr.m0) + int(rank) * G_BM, n0 = int(tr.n0) + int(rank) * B_ROWS;
         const int n_kb = int((J.K + G_BK - 1) / G_BK);
         for (int kb = 0; kb < n_kb; ++kb) {
           lm_wait(smem_u32(&tail->empty[stage]), phase ^ 1u);
           const uint32_t fb = smem_u32(&tail->full[stage]);
-          const uint32_t a = ring + stage * G_STAGE, b = a + G_A_BYTES;
+          const uint32_t a = ring + stage * STAGE, b = a + G_A_BYTES;
           const int k0 = kb * G_BK;
-          lm_expect_tx(fb, G_STAGE);
+          // pair: both CTAs' bytes complete on the leader's full barrier
+          uint32_t bar = fb;
+          if constexpr (kPair) {
+            if (leader) lm_expect_tx(fb, 2 * STAGE);
+            bar = lm_peer0(fb);
+          } else {
+            lm_expect_tx(fb, STAGE);
+          }
+          auto load = [&](uint32_t dst, const CUtensorMap* m, int c0, int c1) {
+            if constexpr (kPair)
+              lm_tma_2d_pair(dst, m, c0, c1, bar);
+            else
+              lm_tma_2d(dst, m, c0, c1, bar);
+          };
           if (J.a_mn) {
 #pragma unroll
-            for (int j = 0; j < G_BM / 64; ++j) lm_tma_2d(a + j * G_BOX, mA, m0 + 64 * j, k0, fb);
+            for (int j = 0; j < G_BM / 64; ++j) load(a + j * G_BOX, mA, m0 + 64 * j, k0);
           } else {
-            lm_tma_2d(a, mA, k0, m0, fb);
+            load(a, mA, k0, m0);
           }
           if (J.b_mn) {
 #pragma unroll
-            for (int j = 0; j < G_BN / 64; ++j) lm_tma_2d(b + j * G_BOX, mB, n0 + 64 * j, k0, fb);
+            for (int j = 0; j < B_ROWS / 64; ++j) load(b + j * G_BOX, mB, n0 + 64 * j, k0);
           } else {
-            lm_tma_2d(b, mB, k0, n0, fb);
+            load(b, mB, k0, n0);
           }
-          if (++stage == uint32_t(G_STAGES)) {
+          if (++stage == uint32_t(NST)) {
             stage = 0;
             phase ^= 1u;
           }
@@ -179,40 +224,55 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    // ============================ MMA issuer ============================
-    if (lane == 0) {
+    // ============================ MMA issuer (pair: the leader) ============================
+    if (lane == 0 && leader) {
       uint32_t stage = 0, phase = 0, tile = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tile) {
-        const TileRef tr = tile_of(P, t);
+      for (int t = tile0; t < n_tiles; t += tile_stride, ++tile) {
+        const TileRef tr = tile_of<BM>(P, t);
         const GemmJob J = tr.j ? P.job[1] : P.job[0];
         const bool amn = J.a_mn != 0, bmn = J.b_mn != 0;
-        const uint32_t idesc = amn ? (bmn ? umma_idesc_bf16(G_BM, G_BN, true, true)
-                                          : umma_idesc_bf16(G_BM, G_BN, true, false))
-                                   : (bmn ? umma_idesc_bf16(G_BM, G_BN, false, true)
-                                          : umma_idesc_bf16(G_BM, G_BN, false, false));
+        const uint32_t idesc = amn ? (bmn ? umma_idesc_bf16(BM, G_BN, true, true)
+                                          : umma_idesc_bf16(BM, G_BN, true, false))
+                                   : (bmn ? umma_idesc_bf16(BM, G_BN, false, true)
+                                          : umma_idesc_bf16(BM, G_BN, false, false));
         // descriptor address step per K = 16: 32 B (K-major) or 16 rows x 128 B (MN-major)
         const uint64_t a_step = amn ? 128u : 2u, b_step = bmn ? 128u : 2u;
         const int n_kb = int((J.K + G_BK - 1) / G_BK);
         const uint32_t acc = tile & 1u, acc_phase = (tile >> 1) & 1u;
-        lm_wait(smem_u32(&tail->tempty[acc]), acc_phase ^ 1u);
+        if constexpr (kPair) {
+          while (!mbar_try_wait_cluster(smem_u32(&tail->tempty[acc]), acc_phase ^ 1u)) {
+          }
+        } else {
+          lm_wait(smem_u32(&tail->tempty[acc]), acc_phase ^ 1u);
+        }
         tc_fence_after();
         const uint32_t d = tmem + acc * G_BN;
         for (int kb = 0; kb < n_kb; ++kb) {
           lm_wait(smem_u32(&tail->full[stage]), phase);
           tc_fence_after();
-          const uint32_t a = ring + stage * G_STAGE, b = a + G_A_BYTES;
+          const uint32_t a = ring + stage * STAGE, b = a + G_A_BYTES;
           const uint64_t ad = amn ? lm_sw128_mn_desc(a, G_BOX) : lm_sw128_desc(a);
           const uint64_t bd = bmn ? lm_sw128_mn_desc(b, G_BOX) : lm_sw128_desc(b);
 #pragma unroll
-          for (int k = 0; k < G_BK / G_UK; ++k)
-            lm_mma(d, ad + a_step * k, bd + b_step * k, idesc, (kb | k) != 0);
-          lm_commit(smem_u32(&tail->empty[stage]));
-          if (++stage == uint32_t(G_STAGES)) {
+          for (int k = 0; k < G_BK / G_UK; ++k) {
+            if constexpr (kPair)
+              lm_mma_pair(d, ad + a_step * k, bd + b_step * k, idesc, (kb | k) != 0);
+            else
+              lm_mma(d, ad + a_step * k, bd + b_step * k, idesc, (kb | k) != 0);
+          }
+          if constexpr (kPair)
+            lm_commit_pair(smem_u32(&tail->empty[stage]));
+          else
+            lm_commit(smem_u32(&tail->empty[stage]));
+          if (++stage == uint32_t(NST)) {
             stage = 0;
             phase ^= 1u;
           }
         }
-        lm_commit(smem_u32(&tail->tfull[acc]));
+        if constexpr (kPair)
+          lm_commit_pair(smem_u32(&tail->tfull[acc]));
+        else
+          lm_commit(smem_u32(&tail->tfull[acc]));
       }
     }
     __syncwarp();
@@ -221,11 +281,11 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     const int q = warp & 3;
     const uint32_t lane_base = uint32_t(32 * q) << 16;
     uint32_t tile = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tile) {
-      const TileRef tr = tile_of(P, t);
+    for (int t = tile0; t < n_tiles; t += tile_stride, ++tile) {
+      const TileRef tr = tile_of<BM>(P, t);
       const GemmJob J = tr.j ? P.job[1] : P.job[0];
       const uint32_t acc = tile & 1u, acc_phase = (tile >> 1) & 1u;
-      const int64_t row = tr.m0 + 32 * q + lane;
+      const int64_t row = tr.m0 + int64_t(rank) * G_BM + 32 * q + lane;
       lm_wait_sleep(smem_u32(&tail->tfull[acc]), acc_phase);
       tc_fence_after();
 #pragma unroll 1
@@ -264,30 +324,67 @@ __global__ void __launch_bounds__(G_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tail->tempty[acc]);
+      if (lane == 0) {
+        if constexpr (kPair)
+          lm_arrive_cluster(lm_peer0(smem_u32(&tail->tempty[acc])));
+        else
+          mbar_arrive(&tail->tempty[acc]);
+      }
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair)
+    cluster_sync_all();  // no CTA frees its TMEM / leaves while the pair still uses it
+  else
+    __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    if constexpr (kPair)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
+}
+
+// 2-CTA pairs by default (TG_GEMM_PAIR=0 forces single CTAs, A/B build)
+static bool gemm_pair_mode() {
+  static int mode = -2;
+  if (mode == -2) mode = ab_env("TG_GEMM_PAIR", 1);
+  return mode != 0;
+}
+
+template <bool kPair>
+static cudaError_t gemm_launch_t(const CUtensorMap (&maps)[4], const GemmParams& P, int n_sms,
+                                 cudaStream_t stream) {
+  const size_t smem = gemm_smem_bytes<kPair>();
+  cudaError_t e = cudaFuncSetAttribute(k_gemm_bf16<kPair>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  constexpr int BM = g_tile_m<kPair>();
+  int64_t tiles = 0;
+  for (int j = 0; j < P.n_jobs; ++j) tiles += n_tiles_of<BM>(P.job[j]);
+  const int64_t slots = kPair ? n_sms / 2 : n_sms;
+  const int units = int(tiles < slots ? tiles : slots);
+  if (units <= 0) return cudaSuccess;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(kPair ? 2 * units : units));
+  cfg.blockDim = dim3(G_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kPair ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_gemm_bf16<kPair>, maps[0], maps[1], maps[2], maps[3], P);
 }
 
 static cudaError_t gemm_launch(const CUtensorMap (&maps)[4], const GemmParams& P, int n_sms,
                                cudaStream_t stream) {
-  const size_t smem = gemm_smem_bytes();
-  cudaError_t e = cudaFuncSetAttribute(k_gemm_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(smem));
-  if (e != cudaSuccess) return e;
-  int64_t tiles = 0;
-  for (int j = 0; j < P.n_jobs; ++j)
-    tiles += ((P.job[j].M + G_BM - 1) / G_BM) * ((P.job[j].N + G_BN - 1) / G_BN);
-  const int grid = int(tiles < n_sms ? tiles : n_sms);
-  if (grid <= 0) return cudaSuccess;
-  k_gemm_bf16<<<grid, G_THREADS, smem, stream>>>(maps[0], maps[1], maps[2], maps[3], P);
-  return cudaGetLastError();
+  return gemm_pair_mode() ? gemm_launch_t<true>(maps, P, n_sms, stream)
+                          : gemm_launch_t<false>(maps, P, n_sms, stream);
 }
 
 // d hidden [T, d] (+)= dz [T, n] . W[col0 : col0 + n]: A dz K-major (box [128

@@ -217,18 +217,21 @@ def test_lmhead_dlogits_matches_formula(T, V, d, col0, n_cols):
                     reason="already pinned to one CTA mode by the environment")
 @pytest.mark.parametrize("pair", ["0", "1"])
 def test_lmhead_backward_in_both_cta_modes(pair):
-    """Both LM-head kernels (forward and backward chunks) run as 2-CTA pairs by
-    default and as single CTAs with TG_LMHEAD_PAIR=0; the mode is read once
-    per process, so each runs the parity tests in a subprocess."""
+    """The LM-head kernels (forward, backward chunks) and the backward GEMMs run
+    as 2-CTA pairs by default and as single CTAs with TG_LMHEAD_PAIR=0 /
+    TG_GEMM_PAIR=0; the mode is read once per process, so each runs the parity
+    tests in a subprocess."""
     import os
     import subprocess
     import sys
     from pathlib import Path
     ab = Path(__file__).resolve().parents[1] / "paper_2505_17826_b200" / "_lib" / "libtg_loss_ab.so"
     assert ab.exists(), "build the A/B variant (__graft_entry__.build())"
-    env = dict(os.environ, TG_LMHEAD_PAIR=pair, TG_LOSS_LIB=str(ab))  # switches: A/B build
+    env = dict(os.environ, TG_LMHEAD_PAIR=pair, TG_GEMM_PAIR=pair,
+               TG_LOSS_LIB=str(ab))  # switches: A/B build
     r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-q", "-x", "-p",
-                        "no:cacheprovider", "-k", "matches_torch_fp32 or backward_from_hidden or matches_formula"],
+                        "no:cacheprovider", "-k", "matches_torch_fp32 or backward_from_hidden or "
+                        "matches_formula or matches_float64 or random_shapes"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
