@@ -39,14 +39,17 @@ constexpr int G_UK = 16;
 constexpr int G_A_BYTES = G_BM * G_BK * 2;  // 16 KB
 constexpr int G_THREADS = 256;
 constexpr int G_BOX = 64 * 64 * 2;          // one MN-major box [64 K][64 MN]: 8 KB
-constexpr int G_MAX_STAGES = 6;
+#ifndef TG_GEMM_PAIR_STAGES
+#define TG_GEMM_PAIR_STAGES 6
+#endif
+constexpr int G_MAX_STAGES = TG_GEMM_PAIR_STAGES > 4 ? TG_GEMM_PAIR_STAGES : 4;
 // kPair = false: one CTA per 128 x 256 tile (cta_group::1), 4 stages of 48 KB.
 // kPair = true : a 2-CTA cluster per 256 x 256 tile (cta_group::2, M 256): each
 //   CTA stages its own 128 A rows and half of the B tile (128 N), so a stage is
 //   32 KB and 6 fit -- per SM the B bytes staged and read halve.
 template <bool kPair> constexpr int g_b_rows() { return kPair ? G_BN / 2 : G_BN; }
 template <bool kPair> constexpr int g_stage() { return G_A_BYTES + g_b_rows<kPair>() * G_BK * 2; }
-template <bool kPair> constexpr int g_stages() { return kPair ? 6 : 4; }
+template <bool kPair> constexpr int g_stages() { return kPair ? TG_GEMM_PAIR_STAGES : 4; }
 template <bool kPair> constexpr int g_tile_m() { return kPair ? 2 * G_BM : G_BM; }
 
 // One GEMM of a launch: D [M, N] (+)= A . B, operand majors, output type.
