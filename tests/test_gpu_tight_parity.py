@@ -287,3 +287,27 @@ def test_large_vocab_target_column_matches_central_differences(name):
         worst = max(worst, abs(fd - gv) / tol)
         assert abs(fd - gv) <= tol, (name, int(t), fd, gv)
     print(f"{name}: worst |fd - g| / tol = {worst:.3f}")
+
+
+# vocabularies around the anchor stash-mode boundaries (bf16): the plan picks
+# mode 1 (z + za in TMEM) while a 2-CTA slice holds <= 6 pairs, the split stash
+# (mode 3) up to 11 pairs (13 positions incl. >= 2 of look-ahead), then mode 1
+# on 4-CTA clusters (<= 6 pairs per quarter), then mode 2 (z in TMEM, za from
+# L2); ~3 rows per cluster, slices whose last position is almost empty / full
+ANCHOR_VOCABS = [(98304, 2), (98312, 2), (131080, 2), (151936, 2), (180000, 2), (180232, 4),
+                 (196616, 2)]
+
+
+@pytest.mark.parametrize("V,cl", ANCHOR_VOCABS)
+def test_anchor_stash_mode_boundaries_every_element(V, cl):
+    batch, packed = make_case(106 + V % 97, V, [53, 47, 61, 39], [2, 2], dtype=torch.bfloat16,
+                              anchor=True)
+    loss = RFTLoss(ANCHOR)
+    assert loss.route(packed) == 1 and loss.cluster_size(packed) == cl
+    out = loss(packed, dlogits="new")
+    ref = O.general_loss(batch, oracle_cfg(ANCHOR))
+    d = out.dlogits.float().cpu().numpy().astype(np.float64)
+    _check_rows(d, ref["dz"], torch.bfloat16, batch.target)
+    st, rs = out.stats_dict(), O.stats_dict(ref["stats"])
+    for k in ("loss", "anchor_loss", "sum_anchor_kl"):
+        assert st[k] == pytest.approx(rs[k], rel=1e-4, abs=1e-6), k
