@@ -504,3 +504,53 @@ def test_config5_ragged_multiturn_row_index_gather():
     assert torch.equal(a.stats, b.stats)
     lp, _, _, seq_lp = logprob_fwd(gathered)
     assert torch.allclose(lp, a.lp, atol=1e-4)
+
+
+def _neg_inf_in_some_rows(batch, packed, every=5, fill=-5.0):
+    """Keep the -inf logits (and anchor logits) only in rows r % every == 2; the
+    other rows get a finite `fill` there, on the host and on the device alike --
+    rows with and without masked vocabulary interleave in every warp's stream."""
+    keep = (np.arange(batch.logits.shape[0]) % every) == 2
+    for host, dev in ((batch.logits, packed.logits),
+                      (getattr(batch, "anchor_logits", None), packed.anchor_logits)):
+        if host is None or dev is None:
+            continue
+        m = np.isinf(host) & ~keep[:, None]
+        host[m] = fill
+        dev.copy_(torch.as_tensor(host, device=dev.device).to(dev.dtype))
+    return keep
+
+
+@pytest.mark.parametrize("shape", ["v32000", "v151936"])
+def test_masked_vocab_in_some_rows_only(shape):
+    """Rows with and without masked vocabulary interleaved in every warp's row
+    stream (the speculative phase 1 holds on the finite rows and falls back to
+    the checked path on the others), entropy bonus on (hz z)."""
+    cfg = CONFIGS["grpo_ppo_k3_ent"]
+    V, lens, gs = SHAPES[shape]
+    batch, packed = make_case(12, V, lens, gs, neg_inf=0.2)
+    _neg_inf_in_some_rows(batch, packed)
+    out = RFTLoss(cfg)(packed, dlogits="new")
+    ref = O.general_loss(batch, oracle_cfg(cfg))
+    assert out.stats_dict()["nonfinite"] == 0
+    assert bool(torch.isfinite(out.dlogits.float()).all())
+    compare(out, ref, torch.bfloat16)
+
+
+def test_fused_anchor_kl_masked_vocabulary_in_some_rows():
+    """The anchor path's phase 2 (split stash at V = 151,936) with -inf in a few
+    rows of both the logits and the anchor logits, against the two-pass route."""
+    V, lens, gs = SHAPES["v151936"]
+    cfg = RFTLossConfig.from_variant("OPMD_SIMPLE", tau=0.4, beta=0.9)
+    batch, packed = make_case(13, V, [61, 47, 70, 55], gs, dtype=torch.bfloat16, anchor=True,
+                              neg_inf=0.02)
+    _neg_inf_in_some_rows(batch, packed)
+    out = RFTLoss(cfg)(packed, dlogits="new")
+    two = RFTLoss(cfg.with_(force_two_pass=True))(packed, dlogits="new")
+    a, b = out.stats_dict(), two.stats_dict()
+    assert a["nonfinite"] == 0
+    for k in ("loss", "anchor_loss", "sum_anchor_kl", "sum_lp", "sum_entropy"):
+        assert a[k] == pytest.approx(b[k], rel=1e-4, abs=1e-5), k
+    d, r = out.dlogits.float(), two.dlogits.float()
+    assert bool(torch.isfinite(d).all())
+    assert bool(((d - r).abs() <= 2.0 ** -8 * float(r.abs().max()) + 1e-2 * r.abs()).all())
