@@ -176,6 +176,16 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines = []
+        self.first = 0  # samples before mark() (warm-up) are not reported
+        self.last = None  # samples after mark_end() (idle) are not reported
+
+    def mark(self):
+        """The timed region starts: later samples only."""
+        self.first = len(self.lines)
+
+    def mark_end(self):
+        """The timed region ended (at least one sample is kept: the next one)."""
+        self.last = len(self.lines)
 
     def start(self):
         try:
@@ -202,7 +212,8 @@ class ClockSampler:
             self.proc.kill()
         sm, smax, power, mem, reasons = [], [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        last = len(self.lines) if self.last is None else max(self.last, self.first + 1)
+        for ln in self.lines[self.first:last]:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -534,6 +545,12 @@ def main():
         st = outs[0].stats if n_mb == 1 else torch.stack([o.stats for o in outs]).sum(0)
         return allreduce_stats(st.clone())
 
+    # the clock sampler starts before the warm-up, so the GPU is not left idle
+    # (clocks ramping down) between the warm-up and the timed region; only the
+    # samples taken after mark() -- the timed region -- are reported
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
     for _ in range(args.warmup):
         st = step()
     torch.cuda.synchronize()
@@ -548,12 +565,10 @@ def main():
         a.record()
         b_.record()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks.start()
-    time.sleep(0.3)
+    clocks.mark()
     launches0 = L.tg_launch_count()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
@@ -569,6 +584,7 @@ def main():
                              torch.stack([o.stats for o in outs]).sum(0))
     t_end.record()
     torch.cuda.synchronize()
+    clocks.mark_end()
     if world > 1:
         dist.barrier()
     launches = L.tg_launch_count() - launches0
