@@ -19,6 +19,7 @@
  *   policy.scored_states            policy.py:181-191 (toy-table adapter)   tg_scored_states (host)
  *   ExperienceBuffer.sample_batch   buffer.py:240-264 (group indexing)      tg_group_by_task (host)
  *   algorithms.apply_update         algorithms.py:329-348 (SGD step)        tg_apply_update
+ *   (LLM-scale optimizer step)      SURVEY.md 8f rank 4 (fused AdamW)        tg_adamw_step
  *
  * plus the north_star registry pieces the reference does not have (GRPO std
  * advantage, RLOO, PPO clip / dual clip, k1/k2/k3(low_var_kl)/abs KL,
@@ -54,7 +55,7 @@
 extern "C" {
 #endif
 
-#define TG_ABI_VERSION 4
+#define TG_ABI_VERSION 5
 
 /* return codes */
 enum { TG_OK = 0, TG_EINVAL = 1, TG_ECUDA = 2, TG_EUNSUPPORTED = 3, TG_EWORKSPACE = 4 };
@@ -292,6 +293,26 @@ int tg_apply_update(float* table, int64_t ld_table, int64_t n_states, int64_t vo
                     const void* grad, int dtype, int64_t ld_grad, const int64_t* state_ids,
                     const int64_t* state_offsets, const int64_t* row_order, int64_t n_touched,
                     int64_t n_rows, double learning_rate, int32_t* status, void* stream);
+
+/* Fused AdamW step of a [rows, cols] parameter block -- the LM head after its
+   backward GEMMs ("LM-head backward GEMM plus a fused
+   AdamW"; the LLM-scale counterpart of algorithms.apply_update,
+   algorithms.py:329-348).  torch.optim.AdamW semantics, decoupled weight decay,
+   step = the 1-based step count t:
+     exp_avg    = exp_avg + (1 - beta1) (grad - exp_avg)
+     exp_avg_sq = beta2 exp_avg_sq + (1 - beta2) grad^2
+     param      = param (1 - lr wd) - lr / (1 - beta1^t) * exp_avg /
+                  (sqrt(exp_avg_sq) / sqrt(1 - beta2^t) + eps)
+   param (bf16 or fp32, row pitch ld_param) and grad (bf16 or fp32, row pitch
+   ld_grad) are device arrays; exp_avg / exp_avg_sq fp32 [rows, cols]
+   contiguous.  One HBM pass (22 bytes per bf16 parameter).  With `status`
+   non-NULL a read-only pass over grad runs first and a non-finite element sets
+   *status = 1 and leaves param and both moments untouched (apply_update's
+   refusal, algorithms.py:337-338); status may be NULL to skip the check. */
+int tg_adamw_step(void* param, int param_dtype, int64_t ld_param, const void* grad,
+                  int grad_dtype, int64_t ld_grad, float* exp_avg, float* exp_avg_sq,
+                  int64_t rows, int64_t cols, double lr, double beta1, double beta2, double eps,
+                  double weight_decay, int64_t step, int32_t* status, void* stream);
 
 /* Which kernel route tg_loss_fwd_bwd takes for this input: 1 = fused single
    pass (4V bytes/row; 6V with the anchor KL of regularizer_g, whose anchor

@@ -12,6 +12,7 @@ from .loss import (LossOutput, RFTLoss, lmhead_dlogits, lmhead_grad_chunk, lmhea
                    lmhead_grad_weight,
                    lmhead_logprob_fwd, lmhead_loss_fwd, lmhead_loss_fwd_bwd, logprob_fwd,
                    stats_to_metrics)
+from .optim import LMHeadAdamW, adamw_step
 from .packing import PackedBatch, PolicyError, group_by_task, pack_arrays
 from .registry import (ADVANTAGE_FNS, ENTROPY_LOSS_FNS, KL_FNS, LOSS_AGG_MODES,
                        POLICY_LOSS_FNS)
@@ -20,5 +21,6 @@ __all__ = [
     "AlgorithmError", "PolicyError", "RFTLossConfig", "Variant", "RFTLoss", "LossOutput",
     "logprob_fwd", "lmhead_logprob_fwd", "lmhead_loss_fwd", "lmhead_loss_fwd_bwd",
     "lmhead_dlogits", "lmhead_grad_chunk", "lmhead_grad_hidden", "lmhead_grad_weight", "stats_to_metrics", "PackedBatch", "pack_arrays", "group_by_task",
+    "adamw_step", "LMHeadAdamW",
     "ADVANTAGE_FNS", "POLICY_LOSS_FNS", "KL_FNS", "ENTROPY_LOSS_FNS", "LOSS_AGG_MODES",
 ]

@@ -25,7 +25,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
               "-I", str(ROOT / "include"), "-I", str(CSRC)]
 CU_SOURCES = ["tg_fused_tma.cu", "tg_stream.cu", "tg_group.cu", "tg_pack.cu", "tg_lmhead.cu",
-              "tg_gemm.cu", "tg_update.cu", "tg_api.cu"]
+              "tg_gemm.cu", "tg_update.cu", "tg_adamw.cu", "tg_api.cu"]
 CPP_SOURCES = ["tg_host.cpp"]
 
 

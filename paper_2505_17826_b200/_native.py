@@ -77,10 +77,10 @@ EXPORTED = [
     "tg_last_error", "tg_abi_version", "tg_scored_states", "tg_group_by_task",
     "tg_set_timing_events", "tg_launch_count", "tg_pack_rows", "tg_lmhead_logprob_fwd",
     "tg_lmhead_workspace_size", "tg_apply_update", "tg_lmhead_dlogits", "tg_fused_cluster_size",
-    "tg_lmhead_grad_hidden", "tg_lmhead_grad_weight", "tg_lmhead_grad_chunk",
+    "tg_lmhead_grad_hidden", "tg_lmhead_grad_weight", "tg_lmhead_grad_chunk", "tg_adamw_step",
 ]
 
-ABI_VERSION = 4  # include/tg_loss.h TG_ABI_VERSION
+ABI_VERSION = 5  # include/tg_loss.h TG_ABI_VERSION
 
 _lib = None
 
@@ -163,6 +163,10 @@ def lib() -> ctypes.CDLL:
     L.tg_lmhead_grad_chunk.argtypes = [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64,
                                        c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p,
                                        c_int64, c_int, c_void_p, c_int64, c_void_p]
+    L.tg_adamw_step.restype = c_int
+    L.tg_adamw_step.argtypes = [c_void_p, c_int, c_int64, c_void_p, c_int, c_int64, c_void_p,
+                                c_void_p, c_int64, c_int64, c_double, c_double, c_double,
+                                c_double, c_double, c_int64, c_void_p, c_void_p]
     if L.tg_abi_version() != ABI_VERSION:
         raise RuntimeError("libtg_loss ABI mismatch")
     _lib = L

@@ -69,6 +69,10 @@ int fused_max_slots();
 int fused_resident_chunks();
 int fused_resident_chunks_z();
 int fused_resident_chunks_split();
+cudaError_t launch_adamw(void* param, int pdtype, int64_t ld_param, const void* grad, int gdtype,
+                         int64_t ld_grad, float* m, float* v, int64_t rows, int64_t cols,
+                         double lr, double b1, double b2, double eps, double wd, int64_t step,
+                         int32_t* status, int n_sms, cudaStream_t st, int* n_launches);
 int fused_anchor_half_bytes(int amode);
 size_t rowmeta_bytes();
 void launch_fwd(const KParams& P, bool anchor, bool vec, int grid, cudaStream_t st);
@@ -880,6 +884,41 @@ int tg_apply_update(float* table, int64_t ld_table, int64_t n_states, int64_t vo
                                 status, reinterpret_cast<cudaStream_t>(stream));
   count_launches(n_touched > 0 ? 2 : 0);
   if (e != cudaSuccess) return fail(TG_ECUDA, "tg_apply_update: %s", cudaGetErrorString(e));
+  return TG_OK;
+}
+
+int tg_adamw_step(void* param, int param_dtype, int64_t ld_param, const void* grad,
+                  int grad_dtype, int64_t ld_grad, float* exp_avg, float* exp_avg_sq,
+                  int64_t rows, int64_t cols, double lr, double beta1, double beta2, double eps,
+                  double weight_decay, int64_t step, int32_t* status, void* stream) {
+  for (int dt : {param_dtype, grad_dtype})
+    if (dt != TG_DTYPE_BF16 && dt != TG_DTYPE_F32) return fail(TG_EINVAL, "unknown dtype %d", dt);
+  if (rows < 0 || cols < 0) return fail(TG_EINVAL, "bad sizes (%lld x %lld)", (long long)rows,
+                                        (long long)cols);
+  if (ld_param < cols || ld_grad < cols)
+    return fail(TG_EINVAL, "row pitch below cols (ld_param %lld, ld_grad %lld)",
+                (long long)ld_param, (long long)ld_grad);
+  // torch.optim.AdamW's argument checks
+  if (!(lr >= 0)) return fail(TG_EINVAL, "Invalid learning rate: %g", lr);
+  if (!(eps >= 0)) return fail(TG_EINVAL, "Invalid epsilon value: %g", eps);
+  if (!(beta1 >= 0 && beta1 < 1)) return fail(TG_EINVAL, "Invalid beta parameter at index 0: %g", beta1);
+  if (!(beta2 >= 0 && beta2 < 1)) return fail(TG_EINVAL, "Invalid beta parameter at index 1: %g", beta2);
+  if (!(weight_decay >= 0)) return fail(TG_EINVAL, "Invalid weight_decay value: %g", weight_decay);
+  if (step < 1) return fail(TG_EINVAL, "step must be >= 1, got %lld", (long long)step);
+  if (rows * cols == 0) {
+    if (status) cudaMemsetAsync(status, 0, sizeof(int32_t), reinterpret_cast<cudaStream_t>(stream));
+    return TG_OK;
+  }
+  if (!param || !grad || !exp_avg || !exp_avg_sq)
+    return fail(TG_EINVAL, "param, grad, exp_avg and exp_avg_sq are required");
+  cudaGetLastError();
+  int n = 0;
+  const DevInfo d = dev_info();
+  cudaError_t e = launch_adamw(param, param_dtype, ld_param, grad, grad_dtype, ld_grad, exp_avg,
+                               exp_avg_sq, rows, cols, lr, beta1, beta2, eps, weight_decay, step,
+                               status, d.sms, reinterpret_cast<cudaStream_t>(stream), &n);
+  count_launches(n);
+  if (e != cudaSuccess) return fail(TG_ECUDA, "tg_adamw_step: %s", cudaGetErrorString(e));
   return TG_OK;
 }
 

@@ -35,6 +35,9 @@
 //  * kA (anchor KL, regularizer_g): the anchor row's chunks ride the ring
 //    beside the logits' (a z + za half-chunk pair per ring / TMEM slot), and the
 //    epilogue adds KL(p || q) -- 6V bytes per row instead of the two-pass 10V.
+//    kA = 3 (split stash): slices larger than TMEM keep part of the pairs in
+//    shared-memory stash slots (8 TMEM + 5 shared positions per period), so a
+//    Qwen-vocabulary bf16 row runs on 2-CTA clusters over all 148 SMs.
 //  * Route 4 (TG_FLAG_UNSCALED_GRAD): unit row coefficients, dz = p - e_y for
 //    the sequence-coupled losses; the per-row scale comes afterwards.
 //  * k_fwd_tma (below) is the forward-only sibling: same ring and phase 1,
