@@ -426,7 +426,9 @@ def main():
     L = N.lib()
     if shared:  # several ranks on one device: keep every rank's buffers within HBM / world
         args.mb_groups = max(1, args.mb_groups // world)
-        args.no_e2e = True
+        # (TG_BENCH_E2E_SHARED=1: keep the e2e leg for a plumbing test at small sizes)
+        if os.environ.get("TG_BENCH_E2E_SHARED") != "1":
+            args.no_e2e = True
 
     K, Lr = args.group_size, args.resp_len
     sharded = args.variant in GLOBAL_SHARDED
@@ -691,6 +693,7 @@ def run_e2e(args, loss, dev, world, rank, n_tok_g, n_seq_g, n_groups):
     timing, every call's host stats and a sample of its host dlogits rows are
     checked against the same inputs run on the device path."""
     import torch
+    import torch.distributed as dist
 
     from paper_2505_17826_b200.packing import PackedBatch
 
@@ -773,10 +776,21 @@ def run_e2e(args, loss, dev, world, rank, n_tok_g, n_seq_g, n_groups):
     one_step()  # warm
     times = []
     for _ in range(2):
+        if world > 1:
+            dist.barrier()  # the ranks' steps start together
         t0 = time.perf_counter()
         one_step()
         times.append(time.perf_counter() - t0)
     dt = statistics.median(times)
+    # whole job: every rank's rows over the slowest rank's time
+    my_rows = float(ng * rows)
+    all_rows = my_rows
+    if world > 1:
+        agg = torch.tensor([dt, my_rows], dtype=torch.float64, device=dev)
+        dt_t, rows_t = agg[:1].clone(), agg[1:].clone()
+        dist.all_reduce(dt_t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(rows_t, op=dist.ReduceOp.SUM)
+        dt, all_rows = float(dt_t.item()), float(rows_t.item())
     # ---- correctness of the e2e results: the device path on the same inputs ----
     ok_stats, ok_rows, mismatch = True, True, None
     sample = np.random.default_rng(5).choice(rows, 8, replace=False)
@@ -798,12 +812,14 @@ def run_e2e(args, loss, dev, world, rank, n_tok_g, n_seq_g, n_groups):
         idx = torch.as_tensor(sample, device=dev)
         ok_rows &= bool(torch.equal(host_out[b][sample].to(dev), ref.dlogits[idx]))
     torch.cuda.synchronize(dev)
-    return {"value": ng * rows / dt, "unit": UNIT, "h2d_bytes_per_step": h2d_bytes,
-            "d2h_bytes_per_step": d2h_bytes,
+    scale = all_rows / my_rows  # every rank copies the same bytes per step
+    return {"value": all_rows / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d_bytes * scale),
+            "d2h_bytes_per_step": int(d2h_bytes * scale),
             "check": {"host_stats_equal_device_path": ok_stats, "first_mismatch": mismatch,
                       "host_dlogits_sample_equal_device_path": ok_rows},
-            "note": f"{ng} RFTLoss calls x {rows} rows per step, pinned host logits in and "
-                    f"dlogits + stats out, {nbuf}-deep copy/compute overlap; PCIe-bound"}
+            "note": f"{ng} RFTLoss calls x {rows} rows per step and rank, pinned host logits "
+                    f"in and dlogits + stats out, {nbuf}-deep copy/compute overlap; PCIe-bound; "
+                    f"value = all ranks' rows / the slowest rank's time ({world} rank(s))"}
 
 
 if __name__ == "__main__":
