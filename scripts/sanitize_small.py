@@ -5,8 +5,8 @@
 
 Covers the fused single-pass kernel (bf16 CL = 2 and CL = 1, fp32 CL = 4), the
 two-pass and coupled routes, the forward-only logprob kernels, the anchor KL,
-the LM-head forward (single and 2-CTA) and backward chunk kernels, the packer
-and the update kernel.  Exits non-zero on a result mismatch against the
+the LM-head forward (single and 2-CTA) and backward chunk kernels, the
+backward GEMMs, the packer, the update kernel and the fused AdamW.  Exits non-zero on a result mismatch against the
 fp32 torch reference computed here."""
 import os
 import sys
@@ -81,6 +81,18 @@ def lmhead_paths():
     assert torch.isfinite(dh).all()
 
 
+def optim_paths():
+    from paper_2505_17826_b200 import adamw_step
+    for dt in (torch.bfloat16, torch.float32):
+        for cols in (256, 77):  # vector units / the scalar path
+            w = torch.randn(33, cols, device="cuda").to(dt)
+            g = torch.randn(33, cols, device="cuda").to(dt)
+            m, v = torch.zeros(33, cols, device="cuda"), torch.zeros(33, cols, device="cuda")
+            adamw_step(w, g, m, v, 1, check_finite=True)
+            adamw_step(w, g, m, v, 2, check_finite=False)
+    torch.cuda.synchronize()
+
+
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "all"
     if which in ("all", "loss"):
@@ -89,5 +101,7 @@ if __name__ == "__main__":
         anchor_paths()
     if which in ("all", "lmhead"):
         lmhead_paths()
+    if which in ("all", "optim"):
+        optim_paths()
     torch.cuda.synchronize()
     print("sanitize_small ok", os.environ.get("TG_LMHEAD_PAIR", ""))
