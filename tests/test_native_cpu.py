@@ -286,3 +286,29 @@ def test_registry_user_components_and_errors():
         unregister(POLICY_LOSS_FNS, "cpu_test_pg")
         unregister(ADVANTAGE_FNS, "cpu_test_adv")
     assert "cpu_test_pg_alias" not in POLICY_LOSS_FNS
+
+
+def test_adamw_argument_validation():
+    """tg_adamw_step checks torch.optim.AdamW's arguments (same messages) and
+    the shapes before any device work; an empty block is a no-op."""
+    L = N.lib()
+    p = ctypes.c_void_p(16)  # never dereferenced: validation fails first
+    base = dict(pdt=N.TG_DTYPE_BF16, ldp=64, gdt=N.TG_DTYPE_BF16, ldg=64, rows=8, cols=64,
+                lr=1e-3, b1=0.9, b2=0.999, eps=1e-8, wd=0.01, step=1)
+
+    def step(**kw):
+        a = {**base, **kw}
+        return L.tg_adamw_step(p, a["pdt"], a["ldp"], p, a["gdt"], a["ldg"], p, p, a["rows"],
+                               a["cols"], a["lr"], a["b1"], a["b2"], a["eps"], a["wd"],
+                               a["step"], None, None)
+
+    cases = [(dict(lr=-1.0), b"Invalid learning rate"), (dict(eps=-1.0), b"Invalid epsilon"),
+             (dict(b1=1.0), b"Invalid beta parameter at index 0"),
+             (dict(b2=-0.1), b"Invalid beta parameter at index 1"),
+             (dict(wd=-0.5), b"Invalid weight_decay"), (dict(step=0), b"step must be >= 1"),
+             (dict(pdt=7), b"unknown dtype"), (dict(ldp=32), b"row pitch"),
+             (dict(rows=-1), b"bad sizes")]
+    for kw, msg in cases:
+        assert step(**kw) == N.TG_EINVAL, kw
+        assert msg in L.tg_last_error(), (kw, L.tg_last_error())
+    assert step(rows=0) == N.TG_OK  # nothing to update, no device work
