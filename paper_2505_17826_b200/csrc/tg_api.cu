@@ -370,13 +370,16 @@ FusedPlan fused_plan(const TgBatch* b, const TgOut* o, bool anchor = false) {
   // twice the columns per CTA).  Mode 2 where mode 1 also fits measured slower
   // (profiles/r02_anchor_modes.txt: 4.63 vs 4.99 TB/s at V = 151,936 bf16,
   // CL = 2 vs 4 -- the L2 re-read stalls phase 2 and 7 % of it misses), so it
-  // only serves rows mode 1 cannot hold (fp32 at Qwen vocabulary: 6V bytes
-  // instead of the two-pass 10V).  TG_FUSED_ANCHOR_MODE forces one (A/B build).
+  // only serves rows neither mode 1 nor mode 3 holds (e.g. bf16 rows of ~200 k
+  // columns: still 6V bytes instead of the two-pass 10V).  TG_FUSED_ANCHOR_MODE
+  // forces one (A/B build).
   //
   // Mode 3 (split stash: 8 TMEM + 5 shared-memory z + za pair positions) holds
   // a 2-CTA slice at V = 151,936 bf16, so those rows run on 2-CTA clusters over
-  // all 148 SMs instead of mode 1's 4-CTA clusters on 132.  Per cluster size
-  // the order is mode 1, mode 3 (pass 0), then mode 2 (pass 1).
+  // all 148 SMs instead of mode 1's 4-CTA clusters on 132 (5.29 vs 4.99 TB/s),
+  // and fp32 rows at that vocabulary on 4-CTA clusters (5.93 vs 5.17 TB/s for
+  // mode 2; profiles/r02_anchor_split.txt).  Per cluster size the order is
+  // mode 1, mode 3 (pass 0), then mode 2 (pass 1).
   const int force_mode = anchor ? env_int("TG_FUSED_ANCHOR_MODE", 0) : 0;
   static const int kModeOrder[2][2] = {{1, 3}, {2, 0}};
   const int n_pass = anchor ? (force_mode ? 1 : 2) : 1;
