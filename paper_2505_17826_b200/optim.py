@@ -83,3 +83,26 @@ class LMHeadAdamW:
         adamw_step(self.weight, d_weight, self.exp_avg, self.exp_avg_sq, self.t + 1, self.lr,
                    self.betas, self.eps, self.weight_decay, self.check_finite)
         self.t += 1  # only after a successful (non-refused) step
+
+    def state_dict(self) -> dict:
+        """Checkpoint of the optimizer state (moments cloned, on their device),
+        the counterpart of torch.optim.Optimizer.state_dict for this parameter."""
+        return {"step": self.t, "exp_avg": self.exp_avg.clone(),
+                "exp_avg_sq": self.exp_avg_sq.clone(),
+                "hyper": {"lr": self.lr, "betas": tuple(self.betas), "eps": self.eps,
+                          "weight_decay": self.weight_decay}}
+
+    def load_state_dict(self, state: dict) -> None:
+        """Resume from ``state_dict()``: the next step continues the bias
+        correction at step + 1 with the saved moments."""
+        for k in ("exp_avg", "exp_avg_sq"):
+            if tuple(state[k].shape) != tuple(self.weight.shape):
+                raise ValueError(f"{k} shape {tuple(state[k].shape)} does not match the weight")
+        self.exp_avg.copy_(state["exp_avg"])
+        self.exp_avg_sq.copy_(state["exp_avg_sq"])
+        self.t = int(state["step"])
+        h = state.get("hyper", {})
+        self.lr = h.get("lr", self.lr)
+        self.betas = tuple(h.get("betas", self.betas))
+        self.eps = h.get("eps", self.eps)
+        self.weight_decay = h.get("weight_decay", self.weight_decay)

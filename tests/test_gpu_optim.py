@@ -142,3 +142,35 @@ def test_lmhead_training_steps_with_fused_adamw():
         opt.step(dw)
     assert opt.t == 3 and all(np.isfinite(losses))
     assert losses[-1] < losses[0], losses
+
+
+def test_checkpoint_resume_is_bitwise():
+    """state_dict / load_state_dict: 2 steps, checkpoint (weight + optimizer
+    state through torch.save), resume in a fresh optimizer, 2 more steps ==
+    4 uninterrupted steps, bit for bit."""
+    import io
+    g = torch.Generator(device="cuda").manual_seed(21)
+    w0 = (torch.randn(96, 512, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    grads = [(torch.randn(96, 512, device="cuda", generator=g) * 1e-2).to(torch.bfloat16)
+             for _ in range(4)]
+    w_a = w0.clone()
+    opt_a = LMHeadAdamW(w_a, **HP)
+    for gr in grads:
+        opt_a.step(gr)
+    w_b = w0.clone()
+    opt_b = LMHeadAdamW(w_b, **HP)
+    for gr in grads[:2]:
+        opt_b.step(gr)
+    buf = io.BytesIO()
+    torch.save({"weight": w_b, "opt": opt_b.state_dict()}, buf)
+    buf.seek(0)
+    ck = torch.load(buf)
+    w_c = ck["weight"].clone()
+    opt_c = LMHeadAdamW(w_c)  # default hyper-parameters, restored from the checkpoint
+    opt_c.load_state_dict(ck["opt"])
+    assert opt_c.t == 2 and opt_c.betas == HP["betas"]
+    for gr in grads[2:]:
+        opt_c.step(gr)
+    assert torch.equal(w_c, w_a)
+    assert torch.equal(opt_c.exp_avg, opt_a.exp_avg) and torch.equal(opt_c.exp_avg_sq,
+                                                                     opt_a.exp_avg_sq)
