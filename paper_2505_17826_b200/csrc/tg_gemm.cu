@@ -69,6 +69,11 @@ struct GemmJob {
 struct GemmParams {
   GemmJob job[2];
   int n_jobs;
+  // Tail split: the last n_half tiles of the queue (those of the final,
+  // partial wave, when they fill at most half of it) run as two 256 x 128
+  // half tiles each -- the last wave then takes half as long.  Work item w <
+  // n_tiles - n_half is tile w; the 2 n_half items after it are the halves.
+  int n_half;
 };
 
 struct GemmSmemTail {
@@ -84,10 +89,11 @@ size_t gemm_smem_bytes() {
   return size_t(g_stages<kPair>()) * g_stage<kPair>() + sizeof(GemmSmemTail) + 1024;
 }
 
-// tile t of the queue -> (job, m0, n0)
+// tile t of the queue -> (job, m0, n0, width)
 struct TileRef {
   int j;
   int64_t m0, n0;
+  int nw;  // N columns of the tile (G_BN, or G_BN / 2 for a tail half)
 };
 
 // (m0: the tile's first row; a pair's CTA rank r owns rows m0 + 128 r ..)
@@ -108,6 +114,19 @@ __host__ __device__ __forceinline__ TileRef tile_of(const GemmParams& P, int t) 
     r.m0 = int64_t(u / nn1) * BM;
     r.n0 = int64_t(u % nn1) * G_BN;
   }
+  r.nw = G_BN;
+  return r;
+}
+
+// work item w of a launch with n_tiles tiles and the last P.n_half split
+template <int BM>
+__host__ __device__ __forceinline__ TileRef item_of(const GemmParams& P, int n_tiles, int w) {
+  const int first_half = n_tiles - P.n_half;
+  if (w < first_half) return tile_of<BM>(P, w);
+  const int h = w - first_half;
+  TileRef r = tile_of<BM>(P, first_half + h / 2);
+  r.n0 += int64_t(h & 1) * (G_BN / 2);
+  r.nw = G_BN / 2;
   return r;
 }
 
@@ -136,6 +155,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
   const int tile0 = kPair ? int(cluster_id_x()) : int(blockIdx.x);
   const int tile_stride = kPair ? int(n_clusters_x()) : int(gridDim.x);
   const int n_tiles = n_tiles_of<BM>(P.job[0]) + (P.n_jobs > 1 ? n_tiles_of<BM>(P.job[1]) : 0);
+  const int n_items = n_tiles + P.n_half;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NST; ++i) {
@@ -179,13 +199,15 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB1)) : "memory");
       }
       uint32_t stage = 0, phase = 0;
-      for (int t = tile0; t < n_tiles; t += tile_stride) {
-        const TileRef tr = tile_of<BM>(P, t);
+      for (int t = tile0; t < n_items; t += tile_stride) {
+        const TileRef tr = item_of<BM>(P, n_tiles, t);
         const GemmJob J = tr.j ? P.job[1] : P.job[0];
         const CUtensorMap* mA = tr.j ? &tmA1 : &tmA0;
         const CUtensorMap* mB = tr.j ? &tmB1 : &tmB0;
-        // this CTA's A rows and B columns of the tile
-        const int m0 = int(tr.m0) + int(rank) * G_BM, n0 = int(tr.n0) + int(rank) * B_ROWS;
+        // this CTA's A rows and B columns of the tile (a tail half: half of them)
+        const int b_rows = tr.nw == G_BN ? B_ROWS : B_ROWS / 2;
+        const int m0 = int(tr.m0) + int(rank) * G_BM, n0 = int(tr.n0) + int(rank) * b_rows;
+        const uint32_t stage_bytes = uint32_t(G_A_BYTES + b_rows * G_BK * 2);
         const int n_kb = int((J.K + G_BK - 1) / G_BK);
         for (int kb = 0; kb < n_kb; ++kb) {
           lm_wait(smem_u32(&tail->empty[stage]), phase ^ 1u);
@@ -195,10 +217,10 @@ __global__ void __launch_bounds__(G_THREADS, 1)
           // pair: both CTAs' bytes complete on the leader's full barrier
           uint32_t bar = fb;
           if constexpr (kPair) {
-            if (leader) lm_expect_tx(fb, 2 * STAGE);
+            if (leader) lm_expect_tx(fb, 2 * stage_bytes);
             bar = lm_peer0(fb);
           } else {
-            lm_expect_tx(fb, STAGE);
+            lm_expect_tx(fb, stage_bytes);
           }
           auto load = [&](uint32_t dst, const CUtensorMap* m, int c0, int c1) {
             if constexpr (kPair)
@@ -214,7 +236,8 @@ __global__ void __launch_bounds__(G_THREADS, 1)
           }
           if (J.b_mn) {
 #pragma unroll
-            for (int j = 0; j < B_ROWS / 64; ++j) load(b + j * G_BOX, mB, n0 + 64 * j, k0);
+            for (int j = 0; j < B_ROWS / 64; ++j)
+              if (64 * j < b_rows) load(b + j * G_BOX, mB, n0 + 64 * j, k0);
           } else {
             load(b, mB, k0, n0);
           }
@@ -230,14 +253,11 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     // ============================ MMA issuer (pair: the leader) ============================
     if (lane == 0 && leader) {
       uint32_t stage = 0, phase = 0, tile = 0;
-      for (int t = tile0; t < n_tiles; t += tile_stride, ++tile) {
-        const TileRef tr = tile_of<BM>(P, t);
+      for (int t = tile0; t < n_items; t += tile_stride, ++tile) {
+        const TileRef tr = item_of<BM>(P, n_tiles, t);
         const GemmJob J = tr.j ? P.job[1] : P.job[0];
         const bool amn = J.a_mn != 0, bmn = J.b_mn != 0;
-        const uint32_t idesc = amn ? (bmn ? umma_idesc_bf16(BM, G_BN, true, true)
-                                          : umma_idesc_bf16(BM, G_BN, true, false))
-                                   : (bmn ? umma_idesc_bf16(BM, G_BN, false, true)
-                                          : umma_idesc_bf16(BM, G_BN, false, false));
+        const uint32_t idesc = umma_idesc_bf16(BM, tr.nw, amn, bmn);
         // descriptor address step per K = 16: 32 B (K-major) or 16 rows x 128 B (MN-major)
         const uint64_t a_step = amn ? 128u : 2u, b_step = bmn ? 128u : 2u;
         const int n_kb = int((J.K + G_BK - 1) / G_BK);
@@ -284,15 +304,15 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     const int q = warp & 3;
     const uint32_t lane_base = uint32_t(32 * q) << 16;
     uint32_t tile = 0;
-    for (int t = tile0; t < n_tiles; t += tile_stride, ++tile) {
-      const TileRef tr = tile_of<BM>(P, t);
+    for (int t = tile0; t < n_items; t += tile_stride, ++tile) {
+      const TileRef tr = item_of<BM>(P, n_tiles, t);
       const GemmJob J = tr.j ? P.job[1] : P.job[0];
       const uint32_t acc = tile & 1u, acc_phase = (tile >> 1) & 1u;
       const int64_t row = tr.m0 + int64_t(rank) * G_BM + 32 * q + lane;
       lm_wait_sleep(smem_u32(&tail->tfull[acc]), acc_phase);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < G_BN; c += 32) {
+      for (int c = 0; c < tr.nw; c += 32) {
         float v[32];
         __syncwarp();
         lm_tmem_ld32(tmem + lane_base + acc * G_BN + uint32_t(c), v);
@@ -349,6 +369,13 @@ __global__ void __launch_bounds__(G_THREADS, 1)
   }
 }
 
+// tail split on by default (TG_GEMM_TAIL=0 turns it off, A/B build)
+static bool gemm_tail_split() {
+  static int mode = -2;
+  if (mode == -2) mode = ab_env("TG_GEMM_TAIL", 1);
+  return mode != 0;
+}
+
 // 2-CTA pairs by default (TG_GEMM_PAIR=0 forces single CTAs, A/B build)
 static bool gemm_pair_mode() {
   static int mode = -2;
@@ -365,9 +392,18 @@ static cudaError_t gemm_launch_t(const CUtensorMap (&maps)[4], const GemmParams&
   if (e != cudaSuccess) return e;
   constexpr int BM = g_tile_m<kPair>();
   int64_t tiles = 0;
-  for (int j = 0; j < P.n_jobs; ++j) tiles += n_tiles_of<BM>(P.job[j]);
+  bool b_mn_all = true;  // the half tiles load MN-major B boxes (64 columns each)
+  for (int j = 0; j < P.n_jobs; ++j) {
+    tiles += n_tiles_of<BM>(P.job[j]);
+    b_mn_all &= P.job[j].b_mn != 0;
+  }
   const int64_t slots = kPair ? n_sms / 2 : n_sms;
-  const int units = int(tiles < slots ? tiles : slots);
+  // tail split: a last wave at most half full runs as half tiles
+  GemmParams Q = P;
+  const int64_t rem = tiles % slots;
+  Q.n_half = (gemm_tail_split() && b_mn_all && rem > 0 && 2 * rem <= slots) ? int(rem) : 0;
+  const int64_t items = tiles + Q.n_half;
+  const int units = int(items < slots ? items : slots);
   if (units <= 0) return cudaSuccess;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(kPair ? 2 * units : units));
@@ -381,7 +417,7 @@ static cudaError_t gemm_launch_t(const CUtensorMap (&maps)[4], const GemmParams&
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_gemm_bf16<kPair>, maps[0], maps[1], maps[2], maps[3], P);
+  return cudaLaunchKernelEx(&cfg, k_gemm_bf16<kPair>, maps[0], maps[1], maps[2], maps[3], Q);
 }
 
 static cudaError_t gemm_launch(const CUtensorMap (&maps)[4], const GemmParams& P, int n_sms,
