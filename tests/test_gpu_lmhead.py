@@ -236,7 +236,7 @@ def test_lmhead_backward_in_both_cta_modes(pair):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("TG_LMHEAD_SEEDS", 24))))
 def test_lmhead_random_shapes(seed):
     """Seeded random shapes for both LM-head kernels: row counts off the tile
     grid (including 1), vocabularies off the 256-column tile, several d, and a
@@ -344,3 +344,29 @@ def test_grad_chunk_one_launch_matches_float64(T, n, d, col0):
     assert bool(((dh.double() + 1.0 - want_h).abs() <= 1e-5 * bound_h + 1e-6).all())
     err_w = (dw.double() - want_w).abs()
     assert bool((err_w <= 2.0 ** -8 * want_w.abs() + 1e-5 * bound_w + 1e-6).all())
+
+
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("TG_LMHEAD_SEEDS", 24))))
+def test_grad_chunk_random_shapes(seed):
+    """Seeded random shapes for the backward GEMM pair in one launch: rows,
+    chunk widths and d off the 256 / 128 tile grids (tail-split half tiles
+    and partial pair tiles included), against float64 products."""
+    from paper_2505_17826_b200 import lmhead_grad_chunk
+    r = np.random.default_rng(900 + seed)
+    T = int(r.integers(1, 1200))
+    n = int(r.integers(1, 400)) * 8
+    d = int(r.choice([64, 128, 192, 256, 320, 512, 1536]))  # (d % 64 == 0: the API rule)
+    col0 = int(r.integers(0, 64))
+    V = col0 + n + int(r.integers(0, 9))
+    dz, w, h = _gemm_operands(T, n, d, V, col0, seed=seed)
+    wc = w[col0:col0 + n].double()
+    want_h = dz.double() @ wc
+    bound_h = dz.double().abs() @ wc.abs()
+    want_w = dz.double().T @ h.double()
+    bound_w = dz.double().abs().T @ h.double().abs()
+    dh = torch.zeros(T, d, device="cuda")
+    dw = torch.empty(n, d, dtype=torch.bfloat16, device="cuda")
+    lmhead_grad_chunk(dz, h, w, col0, dh, dw, accumulate=bool(seed % 2))
+    assert bool(((dh.double() - want_h).abs() <= 1e-5 * bound_h + 1e-6).all()), (T, n, d)
+    err_w = (dw.double() - want_w).abs()
+    assert bool((err_w <= 2.0 ** -8 * want_w.abs() + 1e-5 * bound_w + 1e-6).all()), (T, n, d)
