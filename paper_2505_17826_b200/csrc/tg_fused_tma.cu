@@ -327,6 +327,9 @@ __device__ __forceinline__ int seq_of_row(const KParams& P, int64_t row) {
 }
 
 // ---- phase 1: one chunk (kVecPerThread vectors per consumer thread) ---------
+#ifndef TG_SKIP_EMPTY
+#define TG_SKIP_EMPTY 1
+#endif
 // kPartial: the chunk may run past the slice end (lanes there load a neutral
 // -1e30 vector, which adds exactly 0 to the sums, so every lane takes part in
 // the warp vote).  kMaskTail: the chunk holds the tail padding.
@@ -444,6 +447,9 @@ __device__ __forceinline__ void phase1_chunk(Acc1& acc, RingIt& it, const RingBa
     uint64_t s2 = pk2(0.f, 0.f), t2 = pk2(0.f, 0.f);
 #pragma unroll
     for (int g = 0; g < kVecPerThread; ++g) {
+      // a vector past the slice end for the whole (virtual) warp adds exactly
+      // 0: skip its math (the last, partial chunk of a slice)
+      if (kPartial && TG_SKIP_EMPTY && vbase + g * kConsumers + (tid & ~31) >= sl.v1) continue;
 #pragma unroll
       for (int w = 0; w < Vec<T>::N / 2; ++w) {
         const uint64_t x = pair<T>(u[g], w);
@@ -899,8 +905,11 @@ __device__ __forceinline__ void phase1_chunk_a(AccA& acc, typename AGeo<kMode>::
   {  // speculative: the current reference maxima, accepted when the sums are safe
     uint64_t s2 = pk2(0.f, 0.f), t2 = s2, u2 = s2, sq2 = s2;
 #pragma unroll
-    for (int g = 0; g < kVA; ++g)
+    for (int g = 0; g < kVA; ++g) {
+      // (a vector past the slice end for the whole virtual warp adds exactly 0)
+      if (kPartial && TG_SKIP_EMPTY && vbase + g * kConsumers + (tid & ~31) >= sl.v1) continue;
       accumulate_a<T>(u[g], u[kVA + g], acc.z.a.nm2, acc.nmq2, s2, t2, u2, sq2);
+    }
     float a0, a1;
     upk2(s2, a0, a1);
     const float sc = a0 + a1;
