@@ -422,6 +422,7 @@ FusedPlan fused_plan(const TgBatch* b, const TgOut* o, bool anchor = false) {
       // mode 3: L2 look-ahead of the stash positions behind the landing slots
       // (kernel argument bits 16..31)
       if (amode == 3) fp.prefetch_rows |= env_int("TG_PREFETCH_CHUNKS", 6) << 16;
+      else fp.prefetch_rows |= env_int("TG_PREFETCH_CHUNKS", 0) << 16;  // (A/B only)
       fp.n_slots = n_slots;
       fp.n_ctas = int(clusters * cl);
       return fp;

@@ -1373,22 +1373,23 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         }
         const char* src = slice_ptr(row);
         for (int j = 0; j < sl.nchunk; ++j) {
-          if constexpr (kA == 3) {
-            // L2 look-ahead by positions: the landing slots hold only a few
-            // pairs, so the pairs behind them are pulled into L2 early and
-            // their TMA loads then see L2 latency
-            if (lane == 0 && pf_chunks > 0) {
-              for (; pc < it.c + pf_chunks; ++pc) {
-                const int64_t prow = cid + int64_t(pc / uint32_t(sl.nchunk)) * ncl;
-                if (prow >= NR) break;
-                const uint32_t poff = (pc % uint32_t(sl.nchunk)) * kStep;
-                const uint32_t pb = min(kStep, slice_bytes - poff);
-                prefetch_l2(slice_ptr(prow) + poff, pb);
+          // L2 look-ahead by positions (anchor mode 3: the landing slots hold
+          // only a few pairs, so the pairs behind them are pulled into L2
+          // early and their TMA loads then see L2 latency)
+          if (lane == 0 && pf_chunks > 0) {
+            for (; pc < it.c + pf_chunks; ++pc) {
+              const int64_t prow = cid + int64_t(pc / uint32_t(sl.nchunk)) * ncl;
+              if (prow >= NR) break;
+              const uint32_t poff = (pc % uint32_t(sl.nchunk)) * kStep;
+              const uint32_t pb = min(kStep, slice_bytes - poff);
+              prefetch_l2(slice_ptr(prow) + poff, pb);
+              if constexpr (kA != 0)
                 prefetch_l2(reinterpret_cast<const char*>(P.anchor) + prow * P.ld_anchor * ESZ +
                                 int64_t(sl.v0) * 16 + poff,
                             pb);
-              }
             }
+          }
+          if constexpr (kA == 3) {
             if (it.in_tmem() != (lane == 0)) {  // the other issuer's position
               it.next();
               continue;
