@@ -148,8 +148,19 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   return r;
 }
 
+// TG_WAIT_FULL_SLEEP: the consumers' data waits park the warp in the mbarrier
+// (try_wait with a suspend-time hint) instead of re-polling (A/B; measured
+// neutral for the headline, -0.4 % for 2-chunk rows: re-poll by default)
+#ifndef TG_WAIT_FULL_SLEEP
+#define TG_WAIT_FULL_SLEEP 0
+#endif
 __device__ __forceinline__ void wait_full(uint32_t bar, uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) {
+  if (TG_WAIT_FULL_SLEEP) {
+    while (!mbar_try_wait_sleep(bar, parity)) {
+    }
+  } else {
+    while (!mbar_try_wait(bar, parity)) {
+    }
   }
 }
 
@@ -1140,14 +1151,19 @@ __device__ __forceinline__ void phase2_row_a(const Slice& sl, typename AGeo<kMod
 // Back-off (ns) of the producer's slot waits, the epilogue's partial waits and
 // the consumers' broadcast waits; a negative value selects a try_wait with a
 // suspend-time hint (the warp sleeps until the phase completes).
+// Round 2 (profiles/r02_wait_park.txt): parking the producer's and the
+// broadcast waits in the mbarrier (suspend-time hint) rather than re-polling
+// every 64 ns, and letting the epilogue's cluster-scope partial wait spin,
+// gives the headline +0.4 % on the same box (fewer issued instructions under
+// the power cap).  CL = 1 keeps its spinning epilogue / broadcast waits.
 #ifndef TG_SLEEP_PROD
-#define TG_SLEEP_PROD 64
+#define TG_SLEEP_PROD -1
 #endif
 #ifndef TG_SLEEP_EPI
-#define TG_SLEEP_EPI 64
+#define TG_SLEEP_EPI -1
 #endif
 #ifndef TG_SLEEP_BCAST
-#define TG_SLEEP_BCAST 64
+#define TG_SLEEP_BCAST -1
 #endif
 template <int kSleep>
 __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
@@ -1397,7 +1413,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
           }
           {
             TG_PROF_T0();
-            mbar_wait_u32<TG_SLEEP_PROD>(it.empty(rb), it.phase() ^ 1u);
+            // (CL = 1, short rows: the 64 ns re-poll measured 0.9 % faster)
+            mbar_wait_u32<(CL == 1 ? 64 : TG_SLEEP_PROD)>(it.empty(rb), it.phase() ^ 1u);
             TG_PROF_ADD(tail, 3);
           }
           // kA: a half chunk of z and the same columns of the anchor row in one slot
